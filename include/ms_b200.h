@@ -1,0 +1,160 @@
+/* ms_b200.h — C-ABI of the B200 device layer (sm_100a preemptible tenant kernels,
+ * preempt flag, HP doorbell, device-side timing).
+ *
+ * The reference has no device layer: its "device" is the simulated wave model
+ * (engine.hpp:682-945) and its host<->device crossings are modelled events.  Each entry
+ * point below is the live counterpart of one of those modelled crossings (SURVEY.md
+ * §8b), and is what the C++ scheduler core's B200 backend (csrc/live) binds:
+ *   issue_instance (LP slice)        engine.hpp:702-720   -> ms_lp_run
+ *   p_flag_ = true on HP activation  engine.hpp:949-968   -> ms_preempt_raise
+ *   scheduler SyncBegin/SyncEnd      engine.hpp:621-627   -> ms_lp_wait / ms_lp_poll
+ *   tick launcher / consolidation    engine.hpp:1047-1115 -> ms_lp_set_budget / ms_lp_run ranges
+ *   issue_instance (HP kernel) +     engine.hpp:548-560,  -> ms_hp_arm (ahead of time) + ms_hp_ring
+ *   its modelled launch_overhead       705, 718              (no launch on the critical path)
+ *   KernelDone of an HP segment      engine.hpp:871-889   -> ms_hp_poll / ms_hp_wait
+ *
+ * Conventions: return 0 on success, negative on error (MS_E_CUDA = CUDA failure, text via
+ * ms_last_error); no exceptions cross the ABI; device pointers are uint64_t; device
+ * timestamps are %globaltimer ns; host timestamps are CLOCK_MONOTONIC ns.
+ * Threading: one owner thread per ms_dev drives launches; ms_preempt_raise and
+ * ms_hp_ring are plain release stores to the host-mapped page and may be called from any
+ * thread.
+ */
+#ifndef MS_B200_H_
+#define MS_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef MS_OK
+#define MS_OK 0
+#define MS_E_ARG (-1)
+#endif
+#define MS_E_CUDA (-5)
+#define MS_E_TIMEOUT (-6)
+#define MS_E_NODEV (-7)
+
+typedef struct ms_dev ms_dev;
+
+typedef struct ms_dev_info {
+  int32_t ordinal, sm_count, cc_major, cc_minor;
+  int32_t stream_memops; /* 1 if cuStreamWaitValue32 is usable on this driver */
+  int32_t prio_low, prio_high;
+  int64_t hbm_bytes;
+  char name[64];
+} ms_dev_info;
+
+int ms_dev_open(int ordinal, ms_dev** dev);
+int ms_dev_close(ms_dev* dev);
+int ms_dev_get_info(ms_dev* dev, ms_dev_info* info);
+int ms_dev_sync(ms_dev* dev);
+const char* ms_last_error(void);
+int64_t ms_host_now_ns(void);
+
+/* device memory helpers (tests / bench data setup) */
+int ms_mem_alloc(ms_dev* dev, size_t bytes, uint64_t* dptr);
+int ms_mem_free(ms_dev* dev, uint64_t dptr);
+int ms_memcpy_h2d(ms_dev* dev, uint64_t dst, const void* src, size_t bytes);
+int ms_memcpy_d2h(ms_dev* dev, void* dst, uint64_t src, size_t bytes);
+int ms_memset(ms_dev* dev, uint64_t dst, int value, size_t bytes);
+/* deterministic synthetic bf16 tensor (generator of oracle/tenant_ref.c) */
+int ms_fill_synth_bf16(ms_dev* dev, uint64_t dst, uint64_t n, uint64_t seed, uint64_t tensor, float scale);
+
+/* ---- LP (preemptible) kernels ------------------------------------------------------ */
+#define MS_LP_GEMM 1 /* C[m,n] = A[m,k] * B[n,k]^T, bf16 in/out, fp32 accumulate (tcgen05) */
+#define MS_LP_AXPY 2 /* y = alpha * x + y over n_elems bf16 (HBM streamer) */
+
+typedef struct ms_lp_desc {
+  int32_t kind;
+  int32_t block_n;    /* GEMM tile N: 64, 128 or 256 (tile M is 128, k-block 64) */
+  int32_t group_m;    /* GEMM raster group (L2 reuse), 0 = default 16 */
+  int32_t tile_elems; /* AXPY tile (elements, multiple of 2048), 0 = default 8192 */
+  int32_t ctas_per_sm;/* AXPY residency, 0 = default 4 */
+  int32_t pad;
+  uint64_t a, b, c;
+  int64_t m, n, k;
+  uint64_t x, y;
+  float alpha;
+  float pad2;
+  int64_t n_elems;
+} ms_lp_desc;
+
+typedef struct ms_lp_status {
+  uint64_t run_id;
+  uint64_t begin, end;        /* range of the last launch (fresh tiles) */
+  uint64_t redo_in;           /* redo tiles the last launch started with */
+  uint64_t cursor;            /* next never-claimed fresh tile */
+  uint64_t redo_count;        /* claimed-but-unfinished tiles carried to the next run */
+  uint64_t tiles_done;        /* tiles completed by the last run */
+  int32_t preempted;          /* the run ended because the epoch advanced */
+  int32_t done;               /* the run has exited */
+  int64_t t_launch_host;      /* host ns at ms_lp_run */
+  uint64_t t_start, t_seen, t_exit; /* device ns: first CTA start, first epoch observation, last exit */
+} ms_lp_status;
+
+/* Register a preemptible LP kernel; *total_tiles = size of its linear tile space. */
+int ms_lp_register(ms_dev* dev, const ms_lp_desc* desc, int* id, uint64_t* total_tiles);
+/* Launch (async, low-priority stream) over fresh tiles [begin, end) plus the redo tiles
+ * carried from the previous run; tiles >= budget are not started (budget <= end). */
+int ms_lp_run(ms_dev* dev, int id, uint64_t begin, uint64_t end, uint64_t budget);
+/* Move the running launch's soft end (harvest budget word). */
+int ms_lp_set_budget(ms_dev* dev, int id, uint64_t budget);
+/* Non-blocking: fills *st; returns 1 if the last launch has exited, 0 if running. */
+int ms_lp_poll(ms_dev* dev, int id, ms_lp_status* st);
+int ms_lp_wait(ms_dev* dev, int id, int64_t timeout_ns, ms_lp_status* st);
+/* Drop the redo carry-over (start a fresh pass). */
+int ms_lp_reset(ms_dev* dev, int id);
+
+/* ---- preemption flag ---------------------------------------------------------------- */
+/* epoch += 1 (release store to the host-mapped word); every LP run launched with an older
+ * epoch drains its current tile / k-blocks and exits. */
+int ms_preempt_raise(ms_dev* dev, uint32_t* epoch, int64_t* t_host_ns);
+uint32_t ms_preempt_epoch(ms_dev* dev);
+
+/* ---- HP chains --------------------------------------------------------------------- */
+#define MS_HP_GEMM 1      /* C = A * B^T (non-preemptible tcgen05 GEMM) */
+#define MS_HP_BIAS_GELU 2 /* c = gelu(a + bias) over m x n */
+
+typedef struct ms_hp_op {
+  int32_t kind;
+  int32_t block_n;
+  uint64_t a, b, c, bias;
+  int64_t m, n, k;
+} ms_hp_op;
+
+typedef struct ms_hp_times {
+  uint32_t seq;
+  uint32_t done;
+  uint64_t t_gate;      /* device ns the gate saw the doorbell (0 for direct launches) */
+  uint64_t t_first_cta; /* first CTA of the first chain kernel */
+  uint64_t t_done;      /* last CTA of the last chain kernel */
+} ms_hp_times;
+
+int ms_hp_register_chain(ms_dev* dev, const ms_hp_op* ops, int n_ops, int* chain_id);
+/* Pre-enqueue gate(seq) + the chain's kernels on the highest-priority stream. */
+int ms_hp_arm(ms_dev* dev, int chain_id, uint32_t seq);
+/* Ring the doorbell: release store doorbell = seq (host ns of the store in *t_host_ns). */
+int ms_hp_ring(ms_dev* dev, uint32_t seq, int64_t* t_host_ns);
+/* Baseline path: launch the chain now with no gate (host launch on the critical path). */
+int ms_hp_launch_direct(ms_dev* dev, int chain_id, uint32_t seq);
+int ms_hp_poll(ms_dev* dev, int chain_id, uint32_t seq, ms_hp_times* t);
+int ms_hp_wait(ms_dev* dev, int chain_id, uint32_t seq, int64_t timeout_ns, ms_hp_times* t);
+
+/* ---- clocks ------------------------------------------------------------------------- */
+/* Ping-pong through the host page; device_ns ~= host_ns + *offset_ns (min-RTT sample). */
+int ms_clock_calibrate(ms_dev* dev, int rounds, int64_t* offset_ns, int64_t* rtt_min_ns);
+
+/* ---- kernel timing (CUDA events on the launching stream) ---------------------------- */
+/* Time `reps` back-to-back full runs of LP kernel `id` over [0, total); returns mean ms. */
+int ms_lp_time_full(ms_dev* dev, int id, int reps, float* ms_per_run);
+/* Time `reps` direct launches of an HP chain; returns mean ms per chain. */
+int ms_hp_time_chain(ms_dev* dev, int chain_id, int reps, float* ms_per_chain);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MS_B200_H_ */

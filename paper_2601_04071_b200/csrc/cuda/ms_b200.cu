@@ -1,0 +1,638 @@
+// B200 device layer: implementation of include/ms_b200.h.
+//
+// Owns per device: a low-priority LP stream, a highest-priority HP stream, the pinned
+// host-mapped control page (MsHostPage), the device mirror of the preempt epoch, the
+// per-kernel control blocks, and the registered LP kernels / HP chains with their TMA
+// descriptors.  No CPU fallback: every entry point fails with MS_E_CUDA / MS_E_NODEV when
+// the device or the sm_100a images are unavailable.
+#include <cudaTypedefs.h>
+#include <time.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ms_b200.h"
+#include "stream_kernels.cuh"
+#include "tc_gemm.cuh"
+
+using namespace msdev;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& what) {
+  g_err = what;
+  return code;
+}
+
+#define MS_CUDA(expr)                                                                              \
+  do {                                                                                             \
+    cudaError_t e__ = (expr);                                                                      \
+    if (e__ != cudaSuccess)                                                                        \
+      return fail(MS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__));                 \
+  } while (0)
+
+int64_t now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<int64_t>(ts.tv_sec) * 1000000000ll + ts.tv_nsec;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int encode_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  // bf16 [rows, cols] row-major, box = 64 cols (128 B, swizzle 128B) x box_rows.
+  if (!g_encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return fail(MS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return 0;
+}
+
+constexpr int kRedoCap = 8192;
+
+struct LpSlot {
+  bool used = false;
+  ms_lp_desc desc{};
+  uint64_t total_tiles = 0;
+  int tiles_m = 0, tiles_n = 0;
+  CUtensorMap tma_a{}, tma_b{};
+  unsigned long long* redo[2] = {nullptr, nullptr};
+  uint64_t run_id = 0;
+  uint64_t redo_carry = 0;  // redo entries waiting in redo[run_id % 2] for the next run
+  uint64_t last_begin = 0, last_end = 0, last_redo_in = 0;
+  int64_t t_launch_host = 0;
+  bool launched = false;
+};
+
+struct HpOpRt {
+  ms_hp_op op{};
+  CUtensorMap tma_a{}, tma_b{};
+  int tiles_m = 0, tiles_n = 0;
+  int ctl_index = 0;
+};
+
+struct HpChain {
+  bool used = false;
+  std::vector<HpOpRt> ops;
+};
+
+}  // namespace
+
+struct ms_dev {
+  int ordinal = 0;
+  cudaDeviceProp prop{};
+  int prio_low = 0, prio_high = 0;
+  cudaStream_t lp = nullptr, hp = nullptr, aux = nullptr;
+  MsHostPage* page = nullptr;    // host view
+  MsHostPage* page_d = nullptr;  // device view of the same page
+  MsDevMirror* mirror = nullptr;
+  MsLpCtl* ctl = nullptr;        // [MS_MAX_LP + MS_MAX_HP_CHAINS * 16]
+  MsHpCtl* hp_ctl = nullptr;     // [MS_MAX_HP_CHAINS]
+  unsigned long long* dummy_redo = nullptr;
+  LpSlot lp_slots[MS_MAX_LP];
+  HpChain chains[MS_MAX_HP_CHAINS];
+  int next_hp_ctl = MS_MAX_LP;
+  int stream_memops = 0;
+};
+
+namespace {
+
+int set_smem_attrs() {
+  static bool done = false;
+  if (done) return 0;
+  MS_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               GemmCfg<256>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               GemmCfg<128>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               GemmCfg<64>::kSmemBytes));
+  done = true;
+  return 0;
+}
+
+TileRun base_run(ms_dev* d, int ctl_index) {
+  TileRun r{};
+  r.ctl = d->ctl + ctl_index;
+  r.redo_in = d->dummy_redo;
+  r.redo_out = d->dummy_redo + 16;
+  r.host_epoch = &d->page_d->epoch;
+  r.host_budget = &d->page_d->budget[0];
+  r.mirror = d->mirror;
+  return r;
+}
+
+int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
+                cudaStream_t st) {
+  switch (block_n) {
+    case 256:
+      tc_gemm_kernel<256><<<grid, 256, GemmCfg<256>::kSmemBytes, st>>>(ta, tb, p);
+      break;
+    case 128:
+      tc_gemm_kernel<128><<<grid, 256, GemmCfg<128>::kSmemBytes, st>>>(ta, tb, p);
+      break;
+    case 64:
+      tc_gemm_kernel<64><<<grid, 256, GemmCfg<64>::kSmemBytes, st>>>(ta, tb, p);
+      break;
+    default:
+      return fail(MS_E_ARG, "block_n must be 64, 128 or 256");
+  }
+  MS_CUDA(cudaGetLastError());
+  (void)d;
+  return 0;
+}
+
+int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq) {
+  const HpOpRt& o = ch.ops[i];
+  TileRun r = base_run(d, o.ctl_index);
+  r.hp_ctl = d->hp_ctl + chain_id;
+  r.hp_rec = &d->page_d->hp[chain_id];
+  r.hp_first = i == 0;
+  r.hp_last = i + 1 == ch.ops.size();
+  r.hp_seq = seq;
+  if (o.op.kind == MS_HP_GEMM) {
+    GemmParams p{};
+    p.run = r;
+    p.run.begin = 0;
+    p.run.end = p.run.budget0 = static_cast<unsigned long long>(o.tiles_m) * o.tiles_n;
+    p.m = static_cast<int>(o.op.m);
+    p.n = static_cast<int>(o.op.n);
+    p.k = static_cast<int>(o.op.k);
+    p.tiles_m = o.tiles_m;
+    p.tiles_n = o.tiles_n;
+    p.group_m = 16;
+    p.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+    const int grid = static_cast<int>(std::min<uint64_t>(p.run.end, d->prop.multiProcessorCount));
+    return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, p, grid, d->hp);
+  }
+  BiasGeluParams p{};
+  p.run = r;
+  p.run.begin = 0;
+  p.run.end = p.run.budget0 = static_cast<unsigned long long>(o.op.m);
+  p.x = reinterpret_cast<const __nv_bfloat16*>(o.op.a);
+  p.bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
+  p.out = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+  p.rows = static_cast<int>(o.op.m);
+  p.cols = static_cast<int>(o.op.n);
+  const int grid = static_cast<int>(std::min<int64_t>(o.op.m, d->prop.multiProcessorCount));
+  bias_gelu_kernel<<<grid, 256, 0, d->hp>>>(p);
+  MS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ms_last_error(void) { return g_err.c_str(); }
+int64_t ms_host_now_ns(void) { return now_ns(); }
+
+int ms_dev_open(int ordinal, ms_dev** out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= ordinal) return fail(MS_E_NODEV, "no CUDA device");
+  auto* d = new ms_dev();
+  d->ordinal = ordinal;
+  MS_CUDA(cudaSetDevice(ordinal));
+  MS_CUDA(cudaGetDeviceProperties(&d->prop, ordinal));
+  if (d->prop.major != 10) {
+    delete d;
+    return fail(MS_E_NODEV, "ms_b200 requires an sm_100 (B200) device");
+  }
+  MS_CUDA(cudaDeviceGetStreamPriorityRange(&d->prio_low, &d->prio_high));
+  MS_CUDA(cudaStreamCreateWithPriority(&d->lp, cudaStreamNonBlocking, d->prio_low));
+  MS_CUDA(cudaStreamCreateWithPriority(&d->hp, cudaStreamNonBlocking, d->prio_high));
+  MS_CUDA(cudaStreamCreateWithPriority(&d->aux, cudaStreamNonBlocking, d->prio_low));
+  MS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&d->page), sizeof(MsHostPage),
+                        cudaHostAllocMapped | cudaHostAllocPortable));
+  std::memset(d->page, 0, sizeof(MsHostPage));
+  MS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d->page_d), d->page, 0));
+  MS_CUDA(cudaMalloc(&d->mirror, sizeof(MsDevMirror)));
+  MS_CUDA(cudaMemset(d->mirror, 0, sizeof(MsDevMirror)));
+  const int n_ctl = MS_MAX_LP + MS_MAX_HP_CHAINS * 16;
+  MS_CUDA(cudaMalloc(&d->ctl, sizeof(MsLpCtl) * n_ctl));
+  MS_CUDA(cudaMalloc(&d->hp_ctl, sizeof(MsHpCtl) * MS_MAX_HP_CHAINS));
+  MS_CUDA(cudaMemset(d->hp_ctl, 0, sizeof(MsHpCtl) * MS_MAX_HP_CHAINS));
+  MS_CUDA(cudaMalloc(&d->dummy_redo, 64 * sizeof(unsigned long long)));
+  init_ctl_kernel<<<(n_ctl + 127) / 128, 128>>>(d->ctl, n_ctl, d->hp_ctl, MS_MAX_HP_CHAINS);
+  MS_CUDA(cudaGetLastError());
+  MS_CUDA(cudaDeviceSynchronize());
+  if (int rc = set_smem_attrs()) return rc;
+  int attr = 0;
+  cudaDeviceGetAttribute(&attr, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_USE_STREAM_MEM_OPS_V1), ordinal);
+  d->stream_memops = attr;
+  *out = d;
+  return 0;
+}
+
+int ms_dev_close(ms_dev* d) {
+  if (!d) return 0;
+  cudaSetDevice(d->ordinal);
+  cudaDeviceSynchronize();
+  for (auto& s : d->lp_slots)
+    for (auto* r : s.redo)
+      if (r) cudaFree(r);
+  cudaFree(d->mirror);
+  cudaFree(d->ctl);
+  cudaFree(d->hp_ctl);
+  cudaFree(d->dummy_redo);
+  cudaFreeHost(d->page);
+  cudaStreamDestroy(d->lp);
+  cudaStreamDestroy(d->hp);
+  cudaStreamDestroy(d->aux);
+  delete d;
+  return 0;
+}
+
+int ms_dev_get_info(ms_dev* d, ms_dev_info* info) {
+  std::memset(info, 0, sizeof(*info));
+  info->ordinal = d->ordinal;
+  info->sm_count = d->prop.multiProcessorCount;
+  info->cc_major = d->prop.major;
+  info->cc_minor = d->prop.minor;
+  info->stream_memops = d->stream_memops;
+  info->prio_low = d->prio_low;
+  info->prio_high = d->prio_high;
+  info->hbm_bytes = static_cast<int64_t>(d->prop.totalGlobalMem);
+  std::snprintf(info->name, sizeof info->name, "%s", d->prop.name);
+  return 0;
+}
+
+int ms_dev_sync(ms_dev* d) {
+  MS_CUDA(cudaSetDevice(d->ordinal));
+  MS_CUDA(cudaDeviceSynchronize());
+  return 0;
+}
+
+int ms_mem_alloc(ms_dev* d, size_t bytes, uint64_t* p) {
+  MS_CUDA(cudaSetDevice(d->ordinal));
+  void* ptr = nullptr;
+  MS_CUDA(cudaMalloc(&ptr, bytes));
+  *p = reinterpret_cast<uint64_t>(ptr);
+  return 0;
+}
+int ms_mem_free(ms_dev*, uint64_t p) {
+  MS_CUDA(cudaFree(reinterpret_cast<void*>(p)));
+  return 0;
+}
+int ms_memcpy_h2d(ms_dev* d, uint64_t dst, const void* src, size_t bytes) {
+  MS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice, d->aux));
+  MS_CUDA(cudaStreamSynchronize(d->aux));
+  return 0;
+}
+int ms_memcpy_d2h(ms_dev* d, void* dst, uint64_t src, size_t bytes) {
+  MS_CUDA(cudaMemcpyAsync(dst, reinterpret_cast<const void*>(src), bytes, cudaMemcpyDeviceToHost, d->aux));
+  MS_CUDA(cudaStreamSynchronize(d->aux));
+  return 0;
+}
+int ms_memset(ms_dev* d, uint64_t dst, int value, size_t bytes) {
+  MS_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(dst), value, bytes, d->aux));
+  MS_CUDA(cudaStreamSynchronize(d->aux));
+  return 0;
+}
+int ms_fill_synth_bf16(ms_dev* d, uint64_t dst, uint64_t n, uint64_t seed, uint64_t tensor, float scale) {
+  synth_fill_kernel<<<d->prop.multiProcessorCount * 8, 256, 0, d->aux>>>(reinterpret_cast<__nv_bfloat16*>(dst), n,
+                                                                         seed, tensor, scale);
+  MS_CUDA(cudaGetLastError());
+  MS_CUDA(cudaStreamSynchronize(d->aux));
+  return 0;
+}
+
+// ------------------------------------------------------------------ LP kernels
+int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_tiles) {
+  int slot = -1;
+  for (int i = 0; i < MS_MAX_LP; ++i)
+    if (!d->lp_slots[i].used) {
+      slot = i;
+      break;
+    }
+  if (slot < 0) return fail(MS_E_ARG, "too many LP kernels");
+  LpSlot& s = d->lp_slots[slot];
+  s = LpSlot{};
+  s.desc = *desc;
+  if (desc->kind == MS_LP_GEMM) {
+    const int bn = desc->block_n ? desc->block_n : 256;
+    s.desc.block_n = bn;
+    if (bn != 64 && bn != 128 && bn != 256) return fail(MS_E_ARG, "block_n must be 64/128/256");
+    if (desc->m % kBM || desc->n % bn || desc->k % kBK || desc->k < kBK)
+      return fail(MS_E_ARG, "GEMM shape must be a multiple of (128, block_n, 64)");
+    if (desc->m > (1ll << 31) || desc->n > (1ll << 31) || desc->k > (1ll << 31)) return fail(MS_E_ARG, "shape too large");
+    s.tiles_m = static_cast<int>(desc->m / kBM);
+    s.tiles_n = static_cast<int>(desc->n / bn);
+    s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n;
+    if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
+    if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, bn)) return rc;
+  } else if (desc->kind == MS_LP_AXPY) {
+    s.desc.tile_elems = desc->tile_elems ? desc->tile_elems : 8192;
+    s.desc.ctas_per_sm = desc->ctas_per_sm ? desc->ctas_per_sm : 4;
+    if (s.desc.tile_elems % (kStreamThreads * 8) || s.desc.tile_elems > kStreamThreads * 8 * 8)
+      return fail(MS_E_ARG, "tile_elems must be a multiple of 2048 and <= 16384");
+    if (desc->n_elems % 8) return fail(MS_E_ARG, "n_elems must be a multiple of 8");
+    s.total_tiles = (static_cast<uint64_t>(desc->n_elems) + s.desc.tile_elems - 1) / s.desc.tile_elems;
+  } else {
+    return fail(MS_E_ARG, "unknown LP kernel kind");
+  }
+  for (auto*& r : s.redo) MS_CUDA(cudaMalloc(&r, kRedoCap * sizeof(unsigned long long)));
+  s.used = true;
+  *id = slot;
+  *total_tiles = s.total_tiles;
+  return 0;
+}
+
+int ms_lp_run(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget) {
+  if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
+  LpSlot& s = d->lp_slots[id];
+  if (end > s.total_tiles || begin > end) return fail(MS_E_ARG, "tile range out of bounds");
+  if (budget > end) budget = end;
+  const uint64_t run_id = ++s.run_id;
+  const uint64_t nr_in = s.redo_carry;
+  TileRun r = base_run(d, id);
+  r.begin = begin;
+  r.end = end;
+  r.budget0 = budget;
+  r.nr_in = static_cast<unsigned int>(nr_in);
+  r.redo_in = s.redo[(run_id - 1) & 1];
+  r.redo_out = s.redo[run_id & 1];
+  r.preemptible = 1;
+  r.run_epoch = __atomic_load_n(&d->page->epoch, __ATOMIC_ACQUIRE);
+  r.host_budget = &d->page_d->budget[id];
+  r.slot = id;
+  r.exit_rec = &d->page_d->lp_exit[id];
+  r.run_id = run_id;
+  __atomic_store_n(&d->page->budget[id], ((run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
+  s.last_begin = begin;
+  s.last_end = end;
+  s.last_redo_in = nr_in;
+  s.t_launch_host = now_ns();
+  s.launched = true;
+  const uint64_t work = (end - begin) + nr_in;
+  if (s.desc.kind == MS_LP_GEMM) {
+    GemmParams p{};
+    p.run = r;
+    p.m = static_cast<int>(s.desc.m);
+    p.n = static_cast<int>(s.desc.n);
+    p.k = static_cast<int>(s.desc.k);
+    p.tiles_m = s.tiles_m;
+    p.tiles_n = s.tiles_n;
+    p.group_m = s.desc.group_m ? s.desc.group_m : 16;
+    p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount)));
+    return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, p, grid, d->lp);
+  }
+  StreamParams p{};
+  p.run = r;
+  p.x = reinterpret_cast<const __nv_bfloat16*>(s.desc.x);
+  p.y = reinterpret_cast<__nv_bfloat16*>(s.desc.y);
+  p.alpha = s.desc.alpha;
+  p.n = static_cast<unsigned long long>(s.desc.n_elems);
+  p.tile_elems = s.desc.tile_elems;
+  const uint64_t cap = static_cast<uint64_t>(d->prop.multiProcessorCount) * s.desc.ctas_per_sm;
+  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
+  const int vpt = s.desc.tile_elems / (kStreamThreads * 8);
+  switch (vpt) {
+    case 1: axpy_kernel<1><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
+    case 2: axpy_kernel<2><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
+    case 4: axpy_kernel<4><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
+    case 8: axpy_kernel<8><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
+    default: return fail(MS_E_ARG, "tile_elems must be 2048 * {1,2,4,8}");
+  }
+  MS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int ms_lp_set_budget(ms_dev* d, int id, uint64_t budget) {
+  LpSlot& s = d->lp_slots[id];
+  if (budget > s.last_end) budget = s.last_end;
+  __atomic_store_n(&d->page->budget[id], ((s.run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
+  return 0;
+}
+
+int ms_lp_poll(ms_dev* d, int id, ms_lp_status* st) {
+  LpSlot& s = d->lp_slots[id];
+  const MsLpExit& e = d->page->lp_exit[id];
+  const uint64_t rid = __atomic_load_n(&e.run_id, __ATOMIC_ACQUIRE);
+  std::memset(st, 0, sizeof(*st));
+  st->run_id = s.run_id;
+  st->begin = s.last_begin;
+  st->end = s.last_end;
+  st->redo_in = s.last_redo_in;
+  st->t_launch_host = s.t_launch_host;
+  if (!s.launched || rid != s.run_id) return 0;
+  st->cursor = e.cursor;
+  st->redo_count = e.redo_count;
+  st->tiles_done = e.tiles_done;
+  st->preempted = static_cast<int32_t>(e.preempted);
+  st->t_start = e.t_start;
+  st->t_seen = e.t_seen;
+  st->t_exit = e.t_exit;
+  st->done = 1;
+  s.redo_carry = e.redo_count;
+  return 1;
+}
+
+int ms_lp_wait(ms_dev* d, int id, int64_t timeout_ns, ms_lp_status* st) {
+  const int64_t t0 = now_ns();
+  for (;;) {
+    const int r = ms_lp_poll(d, id, st);
+    if (r) return 0;
+    if (timeout_ns >= 0 && now_ns() - t0 > timeout_ns) {
+      const cudaError_t e = cudaStreamQuery(d->lp);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail(MS_E_CUDA, std::string("LP stream error: ") + cudaGetErrorString(e));
+      return fail(MS_E_TIMEOUT, "LP run did not exit in time");
+    }
+  }
+}
+
+int ms_lp_reset(ms_dev* d, int id) {
+  d->lp_slots[id].redo_carry = 0;
+  return 0;
+}
+
+int ms_preempt_raise(ms_dev* d, uint32_t* epoch, int64_t* t_host) {
+  const uint32_t e = __atomic_add_fetch(&d->page->epoch, 1u, __ATOMIC_RELEASE);
+  if (t_host) *t_host = now_ns();
+  if (epoch) *epoch = e;
+  return 0;
+}
+
+uint32_t ms_preempt_epoch(ms_dev* d) { return __atomic_load_n(&d->page->epoch, __ATOMIC_ACQUIRE); }
+
+// ------------------------------------------------------------------ HP chains
+int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_id) {
+  int cid = -1;
+  for (int i = 0; i < MS_MAX_HP_CHAINS; ++i)
+    if (!d->chains[i].used) {
+      cid = i;
+      break;
+    }
+  if (cid < 0 || n_ops < 1 || n_ops > 16) return fail(MS_E_ARG, "bad HP chain");
+  HpChain ch;
+  for (int i = 0; i < n_ops; ++i) {
+    HpOpRt o;
+    o.op = ops[i];
+    o.ctl_index = d->next_hp_ctl++;
+    if (o.ctl_index >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
+    if (o.op.kind == MS_HP_GEMM) {
+      const int bn = o.op.block_n ? o.op.block_n : 64;
+      o.op.block_n = bn;
+      if (o.op.m % kBM || o.op.n % bn || o.op.k % kBK) return fail(MS_E_ARG, "HP GEMM shape");
+      o.tiles_m = static_cast<int>(o.op.m / kBM);
+      o.tiles_n = static_cast<int>(o.op.n / bn);
+      if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
+      if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
+    } else if (o.op.kind == MS_HP_BIAS_GELU) {
+      if (o.op.n % (8 * 256) && o.op.n % 8) return fail(MS_E_ARG, "bias_gelu cols must be a multiple of 8");
+    } else {
+      return fail(MS_E_ARG, "unknown HP op");
+    }
+    ch.ops.push_back(o);
+  }
+  ch.used = true;
+  d->chains[cid] = ch;
+  *chain_id = cid;
+  return 0;
+}
+
+int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
+  const HpChain& ch = d->chains[cid];
+  if (!ch.used) return fail(MS_E_ARG, "bad chain");
+  gate_kernel<<<1, 32, 0, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid]);
+  MS_CUDA(cudaGetLastError());
+  for (size_t i = 0; i < ch.ops.size(); ++i)
+    if (int rc = launch_hp_op(d, cid, ch, i, seq)) return rc;
+  return 0;
+}
+
+int ms_hp_ring(ms_dev* d, uint32_t seq, int64_t* t_host) {
+  __atomic_store_n(&d->page->doorbell, seq, __ATOMIC_RELEASE);
+  if (t_host) *t_host = now_ns();
+  return 0;
+}
+
+int ms_hp_launch_direct(ms_dev* d, int cid, uint32_t seq) {
+  const HpChain& ch = d->chains[cid];
+  if (!ch.used) return fail(MS_E_ARG, "bad chain");
+  for (size_t i = 0; i < ch.ops.size(); ++i)
+    if (int rc = launch_hp_op(d, cid, ch, i, seq)) return rc;
+  return 0;
+}
+
+int ms_hp_poll(ms_dev* d, int cid, uint32_t seq, ms_hp_times* t) {
+  const MsHpRecord& r = d->page->hp[cid];
+  const uint32_t done = __atomic_load_n(&r.seq_done, __ATOMIC_ACQUIRE);
+  std::memset(t, 0, sizeof(*t));
+  t->seq = seq;
+  if (static_cast<int32_t>(done - seq) < 0) return 0;
+  t->done = 1;
+  t->t_gate = __atomic_load_n(&r.seq_gate, __ATOMIC_ACQUIRE) == seq ? r.t_gate : 0;
+  t->t_first_cta = r.t_first_cta;
+  t->t_done = r.t_done;
+  return 1;
+}
+
+int ms_hp_wait(ms_dev* d, int cid, uint32_t seq, int64_t timeout_ns, ms_hp_times* t) {
+  const int64_t t0 = now_ns();
+  for (;;) {
+    if (ms_hp_poll(d, cid, seq, t)) return 0;
+    if (timeout_ns >= 0 && now_ns() - t0 > timeout_ns) {
+      const cudaError_t e = cudaStreamQuery(d->hp);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail(MS_E_CUDA, std::string("HP stream error: ") + cudaGetErrorString(e));
+      return fail(MS_E_TIMEOUT, "HP chain did not complete in time");
+    }
+  }
+}
+
+// ------------------------------------------------------------------ clocks / timing
+int ms_clock_calibrate(ms_dev* d, int rounds, int64_t* offset_ns, int64_t* rtt_min) {
+  if (rounds < 1) rounds = 1;
+  unsigned long long* stamps = nullptr;
+  MS_CUDA(cudaMalloc(&stamps, sizeof(unsigned long long) * rounds));
+  __atomic_store_n(&d->page->ping, 0u, __ATOMIC_RELEASE);
+  __atomic_store_n(&d->page->pong, 0u, __ATOMIC_RELEASE);
+  echo_kernel<<<1, 1, 0, d->aux>>>(&d->page_d->ping, &d->page_d->pong, stamps, rounds);
+  MS_CUDA(cudaGetLastError());
+  std::vector<int64_t> t0(rounds), t1(rounds);
+  for (int k = 1; k <= rounds; ++k) {
+    t0[k - 1] = now_ns();
+    __atomic_store_n(&d->page->ping, static_cast<uint32_t>(k), __ATOMIC_RELEASE);
+    const int64_t deadline = t0[k - 1] + 1000000000ll;
+    while (__atomic_load_n(&d->page->pong, __ATOMIC_ACQUIRE) < static_cast<uint32_t>(k)) {
+      if (now_ns() > deadline) {
+        cudaFree(stamps);
+        return fail(MS_E_TIMEOUT, "clock echo timed out");
+      }
+    }
+    t1[k - 1] = now_ns();
+  }
+  MS_CUDA(cudaStreamSynchronize(d->aux));
+  std::vector<unsigned long long> g(rounds);
+  MS_CUDA(cudaMemcpy(g.data(), stamps, sizeof(unsigned long long) * rounds, cudaMemcpyDeviceToHost));
+  cudaFree(stamps);
+  int best = 0;
+  for (int i = 1; i < rounds; ++i)
+    if (t1[i] - t0[i] < t1[best] - t0[best]) best = i;
+  *rtt_min = t1[best] - t0[best];
+  *offset_ns = static_cast<int64_t>(g[best]) - (t0[best] + t1[best]) / 2;
+  return 0;
+}
+
+int ms_lp_time_full(ms_dev* d, int id, int reps, float* ms_per_run) {
+  LpSlot& s = d->lp_slots[id];
+  cudaEvent_t a, b;
+  MS_CUDA(cudaEventCreate(&a));
+  MS_CUDA(cudaEventCreate(&b));
+  ms_lp_reset(d, id);
+  ms_lp_status st;
+  if (int rc = ms_lp_run(d, id, 0, s.total_tiles, s.total_tiles)) return rc;  // warm-up
+  if (int rc = ms_lp_wait(d, id, 20000000000ll, &st)) return rc;
+  MS_CUDA(cudaEventRecord(a, d->lp));
+  for (int i = 0; i < reps; ++i)
+    if (int rc = ms_lp_run(d, id, 0, s.total_tiles, s.total_tiles)) return rc;
+  MS_CUDA(cudaEventRecord(b, d->lp));
+  MS_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  MS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  *ms_per_run = ms / reps;
+  ms_lp_poll(d, id, &st);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return 0;
+}
+
+int ms_hp_time_chain(ms_dev* d, int cid, int reps, float* ms_per_chain) {
+  cudaEvent_t a, b;
+  MS_CUDA(cudaEventCreate(&a));
+  MS_CUDA(cudaEventCreate(&b));
+  if (int rc = ms_hp_launch_direct(d, cid, 0)) return rc;
+  MS_CUDA(cudaStreamSynchronize(d->hp));
+  MS_CUDA(cudaEventRecord(a, d->hp));
+  for (int i = 0; i < reps; ++i)
+    if (int rc = ms_hp_launch_direct(d, cid, 0)) return rc;
+  MS_CUDA(cudaEventRecord(b, d->hp));
+  MS_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  MS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  *ms_per_chain = ms / reps;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return 0;
+}
+
+}  // extern "C"

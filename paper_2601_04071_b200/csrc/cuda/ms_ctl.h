@@ -1,0 +1,75 @@
+// Layout of the control words shared by the host runtime and the sm_100a kernels.
+//
+// HBM / host-memory placement:
+//   * HostPage   — one 4 KB pinned, host-mapped page per device (cudaHostAllocMapped).
+//                  Host -> device: preempt epoch, HP doorbell, LP budgets (release
+//                  stores by the host, one elected device poller reads them with
+//                  ld.acquire.sys).  Device -> host: LP exit records and HP completion
+//                  records (st.release.sys), polled by the scheduler thread instead of
+//                  cudaStreamSynchronize.
+//   * DevMirror  — device-memory copies of the epoch / budgets, 8 copies on separate
+//                  128 B lines so 148 CTAs' polls spread over L2 slices.  Written only by
+//                  the elected poller (CTA 0 of the running LP kernel).
+//   * LpCtl      — per registered LP kernel: the tile-claim counter (the cursor), the
+//                  exit counter, and timestamps; self-resetting at the end of each run.
+#pragma once
+#include <stdint.h>
+
+#define MS_MAX_LP 8
+#define MS_MAX_HP_CHAINS 8
+#define MS_MIRROR_COPIES 8
+#define MS_MIRROR_STRIDE 32  // uint32 elements = 128 B
+
+struct MsLpExit {                 // device -> host, one per LP slot (64 B)
+  uint64_t run_id;                // written last (release); host waits for its run id
+  uint64_t cursor;                // next never-claimed tile of [begin, end)
+  uint64_t redo_count;            // claimed-but-unfinished tiles carried to the next run
+  uint64_t tiles_done;            // tiles completed in this run
+  uint64_t t_start;               // first CTA start (globaltimer ns)
+  uint64_t t_seen;                // first CTA to observe the preempt epoch (0 = none)
+  uint64_t t_exit;                // last CTA exit
+  uint64_t preempted;             // 1 if the run ended because of the epoch
+};
+
+struct MsHpRecord {               // device -> host, one per HP chain slot (64 B)
+  uint32_t seq_done;              // written last (release)
+  uint32_t seq_gate;              // gate released for this seq
+  uint64_t t_gate;                // gate kernel observed the doorbell
+  uint64_t t_first_cta;           // first CTA of the first chain kernel started
+  uint64_t t_done;                // last CTA of the last chain kernel finished
+  uint64_t pad[4];
+};
+
+struct MsHostPage {
+  uint32_t epoch;                 // preempt epoch (monotonic)
+  uint32_t pad0[31];
+  uint32_t doorbell;              // HP doorbell sequence
+  uint32_t pad1[31];
+  uint64_t budget[MS_MAX_LP];     // soft end (tile id) per LP slot
+  uint64_t pad2[16 - MS_MAX_LP];
+  MsLpExit lp_exit[MS_MAX_LP];
+  MsHpRecord hp[MS_MAX_HP_CHAINS];
+  uint32_t ping, pad3[31];        // clock calibration echo
+  uint32_t pong, pad4[31];
+};
+
+struct MsDevMirror {
+  uint32_t epoch[MS_MIRROR_COPIES * MS_MIRROR_STRIDE];
+  uint64_t budget[MS_MAX_LP][16];
+};
+
+struct MsLpCtl {
+  unsigned long long claim;       // virtual claim index: redo_in entries first, then fresh tiles
+  unsigned long long tiles_done;
+  unsigned long long t_start;     // min over CTAs
+  unsigned long long t_seen;      // min over CTAs that saw the epoch
+  unsigned int exited;            // CTAs finished
+  unsigned int redo_out_n;
+  unsigned int preempted;
+  unsigned int pad[9];
+};
+
+struct MsHpCtl {                  // per HP chain slot, device memory
+  unsigned long long t_first_cta;
+  unsigned int exited[16];        // per chain kernel exit counters
+};

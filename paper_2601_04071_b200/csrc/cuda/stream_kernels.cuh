@@ -1,0 +1,219 @@
+// HBM-streaming tenant kernels and the HP doorbell gate.
+//
+//  * axpy_kernel     — LP persistent preemptible streamer:
+//                      y <- bf16(fma(a, x, y)) over linear tiles of `tile_elems` bf16,
+//                      16 B vector loads, 8 loads in flight per thread, 4 CTAs/SM;
+//                      one tile (8192 elems = 48 KB of traffic) is the preemption grain.
+//  * bias_gelu_kernel— HP epilogue kernel of the config-1 chain (tanh-GELU(x + bias)).
+//  * gate_kernel     — HP doorbell (north_star (b)): a 1-warp kernel
+//                      pre-enqueued at the head of each armed HP chain on the
+//                      highest-priority stream; it spins on the host-mapped doorbell
+//                      (ld.acquire.sys) and exits when the host rings, releasing the
+//                      already-enqueued chain kernels with no host launch on the path.
+//  * synth_fill_kernel — deterministic synthetic tensors (same generator as
+//                      oracle/tenant_ref.c: splitmix64-keyed uniform, bf16 RNE).
+#pragma once
+
+#include "tile_run.cuh"
+
+namespace msdev {
+
+struct StreamParams {
+  TileRun run;
+  const __nv_bfloat16* x;
+  __nv_bfloat16* y;
+  float alpha;
+  unsigned long long n;
+  int tile_elems;  // multiple of 256 * 8
+};
+
+constexpr int kStreamThreads = 256;  // streaming warps 0-7; warp 8 = poller
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_plain(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t axpy2(float a, uint32_t xv, uint32_t yv) {
+  const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&xv);
+  const __nv_bfloat162 y2 = *reinterpret_cast<const __nv_bfloat162*>(&yv);
+  const float lo = __fmaf_rn(a, __low2float(x2), __low2float(y2));
+  const float hi = __fmaf_rn(a, __high2float(x2), __high2float(y2));
+  return pack_bf16x2(lo, hi);
+}
+
+template <int VPT>  // 16-byte vectors per thread per tile
+__global__ void __launch_bounds__(kStreamThreads + 32) axpy_kernel(const __grid_constant__ StreamParams p) {
+  __shared__ uint32_t preempt, producer_done, tiles_done;
+  __shared__ long long tile_sh[2];
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    preempt = 0;
+    producer_done = 0;
+    tiles_done = 0;
+    cta_started(p.run);
+  }
+  __syncthreads();
+  if (warp == kStreamThreads / 32) {
+    if ((threadIdx.x & 31) == 0 && p.run.preemptible) run_poller(p.run, &preempt, &producer_done);
+  } else {
+    const int tid = threadIdx.x;
+    for (int j = 0;; ++j) {
+      if (tid == 0) {
+        long long t = -1;
+        if (!(p.run.preemptible && ld_volatile_smem(&preempt))) t = claim_tile(p.run);
+        tile_sh[j & 1] = t;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
+      const long long t = tile_sh[j & 1];
+      if (t < 0) break;
+      const unsigned long long base = static_cast<unsigned long long>(t) * p.tile_elems;
+      uint4 xv[VPT], yv[VPT];
+      bool ok[VPT];
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        const unsigned long long e = base + (static_cast<unsigned long long>(v) * kStreamThreads + tid) * 8;
+        ok[v] = e + 8 <= p.n;
+        if (ok[v]) {
+          xv[v] = ld_stream(p.x + e);
+          yv[v] = ld_plain(p.y + e);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VPT; ++v) {
+        if (!ok[v]) continue;
+        const unsigned long long e = base + (static_cast<unsigned long long>(v) * kStreamThreads + tid) * 8;
+        uint4 o;
+        o.x = axpy2(p.alpha, xv[v].x, yv[v].x);
+        o.y = axpy2(p.alpha, xv[v].y, yv[v].y);
+        o.z = axpy2(p.alpha, xv[v].z, yv[v].z);
+        o.w = axpy2(p.alpha, xv[v].w, yv[v].w);
+        st_stream(p.y + e, o);
+      }
+      if (tid == 0) ++tiles_done;
+    }
+    if (tid == 0) st_volatile_smem(&producer_done, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cta_exit(p.run, tiles_done);
+}
+
+// ---------------------------------------------------------------- HP elementwise
+struct BiasGeluParams {
+  TileRun run;  // non-preemptible; tiles = rows
+  const __nv_bfloat16* x;
+  const __nv_bfloat16* bias;
+  __nv_bfloat16* out;
+  int rows, cols;
+};
+
+__global__ void __launch_bounds__(256) bias_gelu_kernel(const __grid_constant__ BiasGeluParams p) {
+  __shared__ long long tile_sh;
+  __shared__ uint32_t tiles_done;
+  if (threadIdx.x == 0) {
+    tiles_done = 0;
+    cta_started(p.run);
+  }
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) tile_sh = claim_tile(p.run);
+    __syncthreads();
+    const long long r = tile_sh;
+    if (r < 0) break;
+    for (int c = threadIdx.x * 8; c < p.cols; c += blockDim.x * 8) {
+      const uint4 xv = *reinterpret_cast<const uint4*>(p.x + static_cast<size_t>(r) * p.cols + c);
+      const uint4 bv = *reinterpret_cast<const uint4*>(p.bias + c);
+      const uint32_t* xs = &xv.x;
+      const uint32_t* bs = &bv.x;
+      uint4 o;
+      uint32_t* os = &o.x;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&xs[i]);
+        const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&bs[i]);
+        float v0 = __low2float(x2) + __low2float(b2);
+        float v1 = __high2float(x2) + __high2float(b2);
+        v0 = 0.5f * v0 * (1.0f + tanhf(k0 * (v0 + k1 * v0 * v0 * v0)));
+        v1 = 0.5f * v1 * (1.0f + tanhf(k0 * (v1 + k1 * v1 * v1 * v1)));
+        os[i] = pack_bf16x2(v0, v1);
+      }
+      *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(r) * p.cols + c) = o;
+    }
+    if (threadIdx.x == 0) ++tiles_done;
+  }
+  if (threadIdx.x == 0) cta_exit(p.run, tiles_done);
+}
+
+// ---------------------------------------------------------------- HP doorbell gate
+__global__ void gate_kernel(const uint32_t* doorbell, unsigned int seq, MsHpRecord* rec) {
+  if (threadIdx.x != 0) return;
+  while (static_cast<int>(ld_acquire_sys(doorbell) - seq) < 0) __nanosleep(20);
+  const unsigned long long t = globaltimer();
+  st_relaxed_sys_u64(&rec->t_gate, t);
+  st_release_sys_u32(&rec->seq_gate, seq);
+}
+
+// ---------------------------------------------------------------- clock calibration echo
+__global__ void echo_kernel(const uint32_t* ping, uint32_t* pong, unsigned long long* stamps, int rounds) {
+  for (int k = 1; k <= rounds; ++k) {
+    while (ld_acquire_sys(ping) < static_cast<uint32_t>(k)) {
+    }
+    stamps[k - 1] = globaltimer();
+    st_release_sys_u32(pong, static_cast<uint32_t>(k));
+  }
+}
+
+// ---------------------------------------------------------------- synthetic tensors
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t d_hash_combine(uint64_t a, uint64_t b) {
+  return d_splitmix64(a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2)));
+}
+
+__global__ void synth_fill_kernel(__nv_bfloat16* out, unsigned long long n, unsigned long long seed,
+                                  unsigned long long tensor, float scale) {
+  const uint64_t base = d_hash_combine(seed, tensor);
+  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const uint64_t x = d_splitmix64(d_hash_combine(base, i));
+    const float u = static_cast<float>(x >> 40) * 5.9604644775390625e-08f;
+    const float v = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), scale);
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void init_ctl_kernel(MsLpCtl* ctl, int n, MsHpCtl* hp, int n_hp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    ctl[i].claim = 0;
+    ctl[i].tiles_done = 0;
+    ctl[i].t_start = ~0ull;
+    ctl[i].t_seen = ~0ull;
+    ctl[i].exited = 0;
+    ctl[i].redo_out_n = 0;
+    ctl[i].preempted = 0;
+  }
+  if (i < n_hp) hp[i].t_first_cta = ~0ull;
+}
+
+}  // namespace msdev

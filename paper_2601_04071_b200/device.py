@@ -1,0 +1,247 @@
+"""ctypes view of libms_b200.so (include/ms_b200.h): the sm_100a device layer.
+
+Plain C types cross the boundary (device pointers are ints).  Any failure raises
+DeviceError carrying ms_last_error(); there is no CPU fallback — a missing library or
+GPU is an error, never a silent downgrade.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _native
+
+MS_LP_GEMM, MS_LP_AXPY = 1, 2
+MS_HP_GEMM, MS_HP_BIAS_GELU = 1, 2
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+class DevInfo(C.Structure):
+    _fields_ = [("ordinal", C.c_int32), ("sm_count", C.c_int32), ("cc_major", C.c_int32),
+                ("cc_minor", C.c_int32), ("stream_memops", C.c_int32), ("prio_low", C.c_int32),
+                ("prio_high", C.c_int32), ("hbm_bytes", C.c_int64), ("name", C.c_char * 64)]
+
+
+class LpDesc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("group_m", C.c_int32),
+                ("tile_elems", C.c_int32), ("ctas_per_sm", C.c_int32), ("pad", C.c_int32),
+                ("a", C.c_uint64), ("b", C.c_uint64), ("c", C.c_uint64),
+                ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
+                ("x", C.c_uint64), ("y", C.c_uint64), ("alpha", C.c_float), ("pad2", C.c_float),
+                ("n_elems", C.c_int64)]
+
+
+class LpStatus(C.Structure):
+    _fields_ = [("run_id", C.c_uint64), ("begin", C.c_uint64), ("end", C.c_uint64),
+                ("redo_in", C.c_uint64), ("cursor", C.c_uint64), ("redo_count", C.c_uint64),
+                ("tiles_done", C.c_uint64), ("preempted", C.c_int32), ("done", C.c_int32),
+                ("t_launch_host", C.c_int64), ("t_start", C.c_uint64), ("t_seen", C.c_uint64),
+                ("t_exit", C.c_uint64)]
+
+    def asdict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class HpOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("a", C.c_uint64), ("b", C.c_uint64),
+                ("c", C.c_uint64), ("bias", C.c_uint64), ("m", C.c_int64), ("n", C.c_int64),
+                ("k", C.c_int64)]
+
+
+class HpTimes(C.Structure):
+    _fields_ = [("seq", C.c_uint32), ("done", C.c_uint32), ("t_gate", C.c_uint64),
+                ("t_first_cta", C.c_uint64), ("t_done", C.c_uint64)]
+
+    def asdict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        _native.core()  # libms_b200 links libmicroslice; make sure it is resolvable first
+        L = _native._load("libms_b200.so")
+        P, I, U32, U64, I64, F = C.c_void_p, C.c_int, C.c_uint32, C.c_uint64, C.c_int64, C.c_float
+        sig = {
+            "ms_dev_open": (I, [I, C.POINTER(P)]), "ms_dev_close": (I, [P]),
+            "ms_dev_get_info": (I, [P, C.POINTER(DevInfo)]), "ms_dev_sync": (I, [P]),
+            "ms_last_error": (C.c_char_p, []), "ms_host_now_ns": (I64, []),
+            "ms_mem_alloc": (I, [P, C.c_size_t, C.POINTER(U64)]), "ms_mem_free": (I, [P, U64]),
+            "ms_memcpy_h2d": (I, [P, U64, P, C.c_size_t]), "ms_memcpy_d2h": (I, [P, P, U64, C.c_size_t]),
+            "ms_memset": (I, [P, U64, I, C.c_size_t]),
+            "ms_fill_synth_bf16": (I, [P, U64, U64, U64, U64, F]),
+            "ms_lp_register": (I, [P, C.POINTER(LpDesc), C.POINTER(I), C.POINTER(U64)]),
+            "ms_lp_run": (I, [P, I, U64, U64, U64]), "ms_lp_set_budget": (I, [P, I, U64]),
+            "ms_lp_poll": (I, [P, I, C.POINTER(LpStatus)]),
+            "ms_lp_wait": (I, [P, I, I64, C.POINTER(LpStatus)]), "ms_lp_reset": (I, [P, I]),
+            "ms_preempt_raise": (I, [P, C.POINTER(U32), C.POINTER(I64)]), "ms_preempt_epoch": (U32, [P]),
+            "ms_hp_register_chain": (I, [P, C.POINTER(HpOp), I, C.POINTER(I)]),
+            "ms_hp_arm": (I, [P, I, U32]), "ms_hp_ring": (I, [P, U32, C.POINTER(I64)]),
+            "ms_hp_launch_direct": (I, [P, I, U32]),
+            "ms_hp_poll": (I, [P, I, U32, C.POINTER(HpTimes)]),
+            "ms_hp_wait": (I, [P, I, U32, I64, C.POINTER(HpTimes)]),
+            "ms_clock_calibrate": (I, [P, I, C.POINTER(I64), C.POINTER(I64)]),
+            "ms_lp_time_full": (I, [P, I, I, C.POINTER(F)]),
+            "ms_hp_time_chain": (I, [P, I, I, C.POINTER(F)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def _ck(rc: int) -> int:
+    if rc < 0:
+        raise DeviceError(f"ms_b200 rc={rc}: {lib().ms_last_error().decode(errors='replace')}")
+    return rc
+
+
+def host_now_ns() -> int:
+    return lib().ms_host_now_ns()
+
+
+@dataclass
+class LpKernel:
+    id: int
+    total_tiles: int
+
+
+class Device:
+    """One B200 under this process's scheduler (one ms_dev per GPU, no sharing)."""
+
+    def __init__(self, ordinal: int = 0):
+        self._h = C.c_void_p()
+        _ck(lib().ms_dev_open(ordinal, C.byref(self._h)))
+        info = DevInfo()
+        _ck(lib().ms_dev_get_info(self._h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in DevInfo._fields_}
+        self.info["name"] = info.name.decode()
+
+    def close(self):
+        if self._h:
+            lib().ms_dev_close(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- memory
+    def alloc(self, nbytes: int) -> int:
+        p = C.c_uint64()
+        _ck(lib().ms_mem_alloc(self._h, nbytes, C.byref(p)))
+        return p.value
+
+    def free(self, ptr: int):
+        _ck(lib().ms_mem_free(self._h, ptr))
+
+    def h2d(self, dst: int, src_ptr: int, nbytes: int):
+        _ck(lib().ms_memcpy_h2d(self._h, dst, src_ptr, nbytes))
+
+    def d2h(self, dst_ptr: int, src: int, nbytes: int):
+        _ck(lib().ms_memcpy_d2h(self._h, dst_ptr, src, nbytes))
+
+    def memset(self, dst: int, value: int, nbytes: int):
+        _ck(lib().ms_memset(self._h, dst, value, nbytes))
+
+    def fill_synth(self, dst: int, n: int, seed: int, tensor: int, scale: float = 1.0):
+        _ck(lib().ms_fill_synth_bf16(self._h, dst, n, seed, tensor, scale))
+
+    def sync(self):
+        _ck(lib().ms_dev_sync(self._h))
+
+    # ---- LP
+    def lp_register_gemm(self, a: int, b: int, c: int, m: int, n: int, k: int, block_n: int = 256,
+                         group_m: int = 16) -> LpKernel:
+        d = LpDesc(kind=MS_LP_GEMM, block_n=block_n, group_m=group_m, a=a, b=b, c=c, m=m, n=n, k=k)
+        return self._lp_register(d)
+
+    def lp_register_axpy(self, x: int, y: int, n_elems: int, alpha: float, tile_elems: int = 8192,
+                         ctas_per_sm: int = 4) -> LpKernel:
+        d = LpDesc(kind=MS_LP_AXPY, tile_elems=tile_elems, ctas_per_sm=ctas_per_sm, x=x, y=y,
+                   alpha=alpha, n_elems=n_elems)
+        return self._lp_register(d)
+
+    def _lp_register(self, d: LpDesc) -> LpKernel:
+        kid, tiles = C.c_int(), C.c_uint64()
+        _ck(lib().ms_lp_register(self._h, C.byref(d), C.byref(kid), C.byref(tiles)))
+        return LpKernel(kid.value, tiles.value)
+
+    def lp_run(self, k: LpKernel, begin: int, end: int, budget: int | None = None):
+        _ck(lib().ms_lp_run(self._h, k.id, begin, end, end if budget is None else budget))
+
+    def lp_set_budget(self, k: LpKernel, budget: int):
+        _ck(lib().ms_lp_set_budget(self._h, k.id, budget))
+
+    def lp_poll(self, k: LpKernel) -> dict | None:
+        st = LpStatus()
+        return st.asdict() if _ck(lib().ms_lp_poll(self._h, k.id, C.byref(st))) else None
+
+    def lp_wait(self, k: LpKernel, timeout_s: float = 30.0) -> dict:
+        st = LpStatus()
+        _ck(lib().ms_lp_wait(self._h, k.id, int(timeout_s * 1e9), C.byref(st)))
+        return st.asdict()
+
+    def lp_reset(self, k: LpKernel):
+        _ck(lib().ms_lp_reset(self._h, k.id))
+
+    def lp_time_full(self, k: LpKernel, reps: int = 5) -> float:
+        ms = C.c_float()
+        _ck(lib().ms_lp_time_full(self._h, k.id, reps, C.byref(ms)))
+        return ms.value
+
+    # ---- preemption
+    def preempt_raise(self) -> tuple[int, int]:
+        e, t = C.c_uint32(), C.c_int64()
+        _ck(lib().ms_preempt_raise(self._h, C.byref(e), C.byref(t)))
+        return e.value, t.value
+
+    def epoch(self) -> int:
+        return lib().ms_preempt_epoch(self._h)
+
+    # ---- HP
+    def hp_register_chain(self, ops: list[dict]) -> int:
+        arr = (HpOp * len(ops))(*[HpOp(**o) for o in ops])
+        cid = C.c_int()
+        _ck(lib().ms_hp_register_chain(self._h, arr, len(ops), C.byref(cid)))
+        return cid.value
+
+    def hp_arm(self, chain: int, seq: int):
+        _ck(lib().ms_hp_arm(self._h, chain, seq))
+
+    def hp_ring(self, seq: int) -> int:
+        t = C.c_int64()
+        _ck(lib().ms_hp_ring(self._h, seq, C.byref(t)))
+        return t.value
+
+    def hp_launch_direct(self, chain: int, seq: int):
+        _ck(lib().ms_hp_launch_direct(self._h, chain, seq))
+
+    def hp_poll(self, chain: int, seq: int) -> dict | None:
+        t = HpTimes()
+        return t.asdict() if _ck(lib().ms_hp_poll(self._h, chain, seq, C.byref(t))) else None
+
+    def hp_wait(self, chain: int, seq: int, timeout_s: float = 10.0) -> dict:
+        t = HpTimes()
+        _ck(lib().ms_hp_wait(self._h, chain, seq, int(timeout_s * 1e9), C.byref(t)))
+        return t.asdict()
+
+    def hp_time_chain(self, chain: int, reps: int = 20) -> float:
+        ms = C.c_float()
+        _ck(lib().ms_hp_time_chain(self._h, chain, reps, C.byref(ms)))
+        return ms.value
+
+    # ---- clocks
+    def calibrate(self, rounds: int = 300) -> tuple[int, int]:
+        off, rtt = C.c_int64(), C.c_int64()
+        _ck(lib().ms_clock_calibrate(self._h, rounds, C.byref(off), C.byref(rtt)))
+        return off.value, rtt.value
