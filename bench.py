@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the µs-scale preemption path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[0], the synthetic 2-tenant trace, run LIVE on the GPU):
+HP = small-GEMM-chain inference (4 x C[128x4096] = A W^T over 4096x4096 bf16 weights +
+bias/GELU, Poisson 50 req/s, 8 iterations, memcpy+sync hint U[500,1000] us per
+iteration) co-located with LP = bf16 8192^3 GEMM loop, driven by the C++ scheduler core
+(Algorithm 1) through the C-ABI (ms_live_run).  A "step" = one live trace window of
+--step-s seconds (a fresh Poisson trace per step).
+
+value = p99 preemption latency (us), reference definition (engine.hpp:826-834): HP
+launch issue (doorbell ring) -> first HP CTA on the GPU, nearest-rank p99 over every HP
+activation of the timed steps (max over ranks' samples).  The other two BASELINE metrics
+(HP SLO attainment, LP throughput vs exclusive) and the kernel-boundary baseline ride
+along in the same line.  Multi-GPU: one independent scheduler per GPU (replicas, no
+collective), launched under torchrun.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "p50/p99 preemption latency (µs); HP SLO attainment %; LP throughput vs exclusive"
+WORKLOAD = ("cfg1 (BASELINE configs[0]) live on B200: HP 4x[128x4096x4096] bf16 GEMM chain + bias/GELU, "
+            "Poisson 50 req/s, 8 iters, memcpy+sync hint U[500,1000]us  vs  LP bf16 8192^3 GEMM loop")
+
+
+def percentile(xs, q):  # nearest rank (metrics.hpp:21-28)
+    if not xs:
+        return None
+    s = sorted(xs)
+    return s[min(len(s) - 1, int(math.floor(q * len(s))))]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- dist helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def gather(obj, ws):
+    if ws == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * ws
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def cpu_reference(scenarios, threads: int):
+    """The reference's own CPU scheduler (oracle/_ref: Engine::run(), compiled from
+    /root/reference) replaying the same trace windows, one window per host thread."""
+    from oracle import ref as R
+    results = [None] * len(scenarios)
+
+    def work(i):
+        sc = scenarios[i]
+        t = time.perf_counter()
+        r = R.run_scenario(sc, "splitkernel", delays=True)
+        ex = R.run_scenario(sc, "exclusive")
+        exlp = R.run_scenario(sc, "exclusive_lp")
+        results[i] = {"delays": r["delays"], "wall": time.perf_counter() - t, "events": r["timeline"]["n"],
+                      "lp": float(r["counters"]["lp_work_units"]), "lp_ex": float(exlp["counters"]["lp_work_units"])}
+
+    t0 = time.perf_counter()
+    pool = []
+    for i in range(len(scenarios)):
+        th = threading.Thread(target=work, args=(i,))
+        pool.append(th)
+        th.start()
+        while sum(t.is_alive() for t in pool) >= threads:
+            time.sleep(0.001)
+    for th in pool:
+        th.join()
+    wall = time.perf_counter() - t0
+    delays = [d for r in results for d in r["delays"]]
+    return {"p99_us": percentile(delays, 0.99) / 1e3 if delays else None,
+            "p50_us": percentile(delays, 0.50) / 1e3 if delays else None,
+            "wall_s": wall, "events": sum(r["events"] for r in results),
+            "lp_norm": (sum(r["lp"] for r in results) / max(1e-9, sum(r["lp_ex"] for r in results)))}
+
+
+def run_reference_arm(args, ws, rank):
+    """--impl reference: the reference CPU implementation of the path (oracle/_ref) on this
+    box's host cores, same config / metric / unit, each step = one bounded replay sample."""
+    if rank != 0:
+        return
+    from paper_2601_04071_b200 import scenarios as S
+    threads = max(1, os.cpu_count() or 1)
+    calib = json.loads((ROOT / "profiles" / "calib_b200.json").read_text()) if \
+        (ROOT / "profiles" / "calib_b200.json").exists() else {}
+    mk = lambda i: S.config1(seed=1000 + i, horizon_s=args.step_s, calib=calib)  # noqa: E731
+    cpu_reference([mk(100 + i) for i in range(args.warmup)], threads)
+    t = time.perf_counter()
+    res = cpu_reference([mk(i) for i in range(args.steps)], threads)
+    wall = time.perf_counter() - t
+    line = {"metric": METRIC, "value": res["p99_us"], "unit": "us", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "step": f"replay of one {args.step_s}s trace window (seed 1000+i)",
+                       "parallelism": "replicas"},
+            "p50_us": res["p50_us"], "lp_throughput_vs_exclusive": res["lp_norm"],
+            "cpu_baseline": {"value": res["p99_us"], "unit": "us", "cores": threads, "kind": "reference",
+                             "sample": f"{args.steps} x {args.step_s}s config-1 windows, splitkernel+exclusive+"
+                                       f"exclusive_lp replays, {res['events']} decision events, "
+                                       f"{res['events'] / max(wall, 1e-9):.0f} events/s"},
+            "e2e": {"value": res["p99_us"], "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--step-s", type=float, default=1.0)
+    ap.add_argument("--warmup-s", type=float, default=0.25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        import torch
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+    if args.impl == "reference":
+        run_reference_arm(args, ws, rank)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import torch
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config1, live_run
+
+    dev = Device(local)
+    w = Config1(dev)
+    calib = w.calibrate(reps=5)
+    if rank == 0:
+        (ROOT / "profiles").mkdir(exist_ok=True)
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
+        (ROOT / "gpurun_out" / "calib_b200.json").write_text(json.dumps(calib, indent=1))
+    base_seed = 1000 + 10_000 * rank
+    sc = lambda i, h: w.scenario(seed=base_seed + i, horizon_s=h)  # noqa: E731
+
+    # --- reference runs for the other two metrics (same trace windows as the timed steps)
+    ex_rows, exlp_tiles, exlp_s = [], 0, 0.0
+    for i in range(args.steps):
+        ex = live_run(dev, sc(i, args.step_s), "exclusive", w.binding(), w.options(timeline=False))
+        ex_rows += ex["requests"]["rows"]
+    ttft = percentile([r[1] for r in ex_rows if r[4]], 0.99)
+    tpot = percentile([r[2] for r in ex_rows if r[4]], 0.99)
+    slo = {"ttft_ns": ttft, "tpot_ns": tpot}
+    exlp = live_run(dev, sc(0, args.step_s), "exclusive_lp", w.binding(), w.options(timeline=False))
+    exlp_rate = exlp["lp"]["tiles_per_s"]
+
+    def attainment(rows):  # slo_attainment (metrics.hpp:96-105): incomplete requests count against
+        ok = sum(1 for r in rows if r[4] and r[1] <= slo["ttft_ns"] and r[2] <= slo["tpot_ns"])
+        return ok / max(1, len(rows))
+
+    # --- warm-up (untimed)
+    for i in range(args.warmup):
+        live_run(dev, sc(500 + i, args.warmup_s), "splitkernel", w.binding(), w.options(timeline=False))
+
+    # --- timed steps
+    torch.cuda.synchronize(local)
+    barrier(ws)
+    samples, lp_exit, rows, tiles, launches, chains = [], [], [], 0, 0, 0
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            r = live_run(dev, sc(i, args.step_s), "splitkernel", w.binding(), w.options(timeline=False, slo=slo))
+            samples += r["samples"]["preempt_ring_to_first_hp_cta"]
+            lp_exit += r["samples"]["preempt_flag_to_last_lp_exit"]
+            rows += r["requests"]["rows"]
+            tiles += r["lp"]["tiles_done"]
+            launches += r["lp"]["launches"]
+            chains += r["hp_chains"]
+        torch.cuda.synchronize(local)
+        wall = time.perf_counter() - t0
+    barrier(ws)
+    step_ms = 1e3 * wall / args.steps
+
+    # --- kernel-boundary temporal-sharing baseline (REEF-like) on the same windows
+    kb_rows, kb_tiles, kb_samples = [], 0, []
+    for i in range(args.steps):
+        r = live_run(dev, sc(i, args.step_s), "reef", w.binding(), w.options(timeline=False))
+        kb_rows += r["requests"]["rows"]
+        kb_tiles += r["lp"]["tiles_done"]
+        kb_samples += r["samples"]["ring_to_first_hp_cta_all"]
+
+    # --- e2e: same metric through the C-ABI with the HP request buffers in pinned host
+    # memory (H2D of the input after the doorbell, D2H of the output before completion)
+    e2e = live_run(dev, sc(0, args.step_s), "splitkernel", w.binding(e2e=True), w.options(timeline=False))
+    e2e_samples = e2e["samples"]["preempt_ring_to_first_hp_cta"]
+
+    mine = {"samples": samples, "lp_exit": lp_exit, "rows": rows, "tiles": tiles, "kb_rows": kb_rows,
+            "kb_tiles": kb_tiles, "kb_samples": kb_samples, "exlp_rate": exlp_rate, "ex_rows": ex_rows,
+            "step_ms": step_ms, "wall": wall, "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"],
+            "launches": launches, "chains": chains, "clocks": clk.summary(), "calib": calib,
+            "slo": slo}
+    allr = gather(mine, ws)
+    if rank != 0:
+        dev.close()
+        return
+
+    S_ = [x for r in allr for x in r["samples"]]
+    LX = [x for r in allr for x in r["lp_exit"]]
+    horizon_total = args.steps * args.step_s
+    lp_rate = sum(r["tiles"] for r in allr) / horizon_total
+    kb_rate = sum(r["kb_tiles"] for r in allr) / horizon_total
+    ex_rate = sum(r["exlp_rate"] for r in allr)
+    att = sum(attainment(r["rows"]) * len(r["rows"]) for r in allr) / max(1, sum(len(r["rows"]) for r in allr))
+    att_ex = sum(attainment(r["ex_rows"]) * len(r["ex_rows"]) for r in allr) / max(1, sum(len(r["ex_rows"]) for r in allr))
+    att_kb = sum(attainment(r["kb_rows"]) * len(r["kb_rows"]) for r in allr) / max(1, sum(len(r["kb_rows"]) for r in allr))
+    E2E = [x for r in allr for x in r["e2e"]]
+
+    # roofline of the dominant kernel (LP tcgen05 GEMM, 2*8192^3 per launch), timed alone
+    # with CUDA events on its stream (ms_lp_time_full); peak = measured burst bf16.
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
+        else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+    peak = peaks.get("bf16_tflops", 1590.0)
+    achieved = 2.0 * 8192 ** 3 / (calib["lp_gemm_ms"] * 1e-3) / 1e12
+    ncu = ROOT / "profiles" / "ncu_summary.json"
+    traffic = None
+    if ncu.exists():
+        traffic = json.loads(ncu.read_text()).get("tc_gemm_kernel<256>", {}).get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": percentile(S_, 0.99) / 1e3, "unit": "us", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max(r["step_ms"] for r in allr), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "step": f"one live {args.step_s}s trace window (fresh Poisson trace)",
+                   "l2": "LP operands 384 MB > 126 MB L2 (no flush needed)", "parallelism": f"replicas x{ws}",
+                   "preemption_latency_def": "HP doorbell ring -> first HP CTA (%globaltimer, drift-corrected)"},
+        "p50_us": percentile(S_, 0.50) / 1e3,
+        "preempt_samples": len(S_),
+        "lp_exit_p50_us": percentile(LX, 0.50) / 1e3 if LX else None,
+        "lp_exit_p99_us": percentile(LX, 0.99) / 1e3 if LX else None,
+        "slo_attainment": att, "slo_attainment_exclusive": att_ex,
+        "lp_throughput_vs_exclusive": lp_rate / max(1e-9, ex_rate),
+        "kernel_boundary_baseline": {"slo_attainment": att_kb, "lp_throughput_vs_exclusive": kb_rate / max(1e-9, ex_rate),
+                                     "p99_us": percentile([x for r in allr for x in r["kb_samples"]], 0.99) / 1e3},
+        "lp_vs_kernel_boundary": lp_rate / max(1e-9, kb_rate),
+        "slo_ns": allr[0]["slo"],
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "tc_gemm_kernel<256> (LP 8192^3 bf16, 2048 128x256 tiles)",
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
+        "e2e": {"value": percentile(E2E, 0.99) / 1e3 if E2E else None, "unit": "us",
+                "h2d_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),
+                "d2h_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),
+                "what": "same metric, HP request input H2D from pinned host after the doorbell, output D2H"},
+        "gpu_launches": int(sum(r["launches"] + 6 * r["chains"] for r in allr)),
+        "clocks": allr[0]["clocks"],
+        "calib": allr[0]["calib"],
+    }
+    if not args.no_cpu_baseline:
+        from paper_2601_04071_b200 import scenarios as S
+        cb = cpu_reference([S.config1(seed=1000 + i, horizon_s=args.step_s, calib=calib) for i in range(2)], 1)
+        line["cpu_baseline"] = {"value": cb["p99_us"], "unit": "us", "cores": 1, "kind": "reference",
+                                "sample": f"reference Engine::run() replay of 2 x {args.step_s}s config-1 windows "
+                                          f"(splitkernel+exclusive+exclusive_lp), {cb['events']} events in "
+                                          f"{cb['wall_s']:.2f}s; modelled delay floor = launch_overhead",
+                                "lp_throughput_vs_exclusive": cb["lp_norm"]}
+    print(json.dumps(line), flush=True)
+    dev.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

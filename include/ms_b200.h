@@ -55,6 +55,10 @@ int ms_dev_sync(ms_dev* dev);
 const char* ms_last_error(void);
 int64_t ms_host_now_ns(void);
 
+/* pinned host memory (e2e request buffers) */
+int ms_host_alloc(ms_dev* dev, size_t bytes, uint64_t* hptr);
+int ms_host_free(ms_dev* dev, uint64_t hptr);
+
 /* device memory helpers (tests / bench data setup) */
 int ms_mem_alloc(ms_dev* dev, size_t bytes, uint64_t* dptr);
 int ms_mem_free(ms_dev* dev, uint64_t dptr);
@@ -101,6 +105,14 @@ int ms_lp_register(ms_dev* dev, const ms_lp_desc* desc, int* id, uint64_t* total
 /* Launch (async, low-priority stream) over fresh tiles [begin, end) plus the redo tiles
  * carried from the previous run; tiles >= budget are not started (budget <= end). */
 int ms_lp_run(ms_dev* dev, int id, uint64_t begin, uint64_t end, uint64_t budget);
+/* Same with flags: MS_RUN_NONPREEMPTIBLE runs the range to completion without polling the
+ * epoch (kernel-boundary temporal-sharing baseline). */
+#define MS_RUN_NONPREEMPTIBLE 1
+int ms_lp_run_ex(ms_dev* dev, int id, uint64_t begin, uint64_t end, uint64_t budget, int flags);
+/* Claim counter of the running launch as last published by its poller (redo entries
+ * first, then fresh tiles), for harvest-budget pacing. */
+uint64_t ms_lp_progress(ms_dev* dev, int id);
+uint64_t ms_lp_total_tiles(ms_dev* dev, int id);
 /* Move the running launch's soft end (harvest budget word). */
 int ms_lp_set_budget(ms_dev* dev, int id, uint64_t budget);
 /* Non-blocking: fills *st; returns 1 if the last launch has exited, 0 if running. */
@@ -118,6 +130,8 @@ uint32_t ms_preempt_epoch(ms_dev* dev);
 /* ---- HP chains --------------------------------------------------------------------- */
 #define MS_HP_GEMM 1      /* C = A * B^T (non-preemptible tcgen05 GEMM) */
 #define MS_HP_BIAS_GELU 2 /* c = gelu(a + bias) over m x n */
+#define MS_HP_H2D 3       /* copy m bytes: pinned host a -> device c (e2e request input) */
+#define MS_HP_D2H 4       /* copy m bytes: device a -> pinned host c (e2e request output) */
 
 typedef struct ms_hp_op {
   int32_t kind;
@@ -135,6 +149,8 @@ typedef struct ms_hp_times {
 } ms_hp_times;
 
 int ms_hp_register_chain(ms_dev* dev, const ms_hp_op* ops, int n_ops, int* chain_id);
+/* Next value of the device's monotonic doorbell sequence (never reused on this ms_dev). */
+uint32_t ms_hp_next_seq(ms_dev* dev);
 /* Pre-enqueue gate(seq) + the chain's kernels on the highest-priority stream. */
 int ms_hp_arm(ms_dev* dev, int chain_id, uint32_t seq);
 /* Ring the doorbell: release store doorbell = seq (host ns of the store in *t_host_ns). */

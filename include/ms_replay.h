@@ -106,6 +106,11 @@ int ms_generate_bursty_arrivals(double rate, double burstiness, int64_t horizon_
 int ms_replay_run(const char* scenario_json, const char* policy, int flags, char** out_json, char* err,
                   size_t err_len);
 
+/* Same with EngineOptions (engine.hpp:84-90) as JSON:
+ * {"hint_filter": ["tagA+tagB", ...], "global_floor": bool, "util_sample_period_ns": n}. */
+int ms_replay_run_opts(const char* scenario_json, const char* policy, const char* options_json, int flags,
+                       char** out_json, char* err, size_t err_len);
+
 /* Scenario JSON round trip through ScenarioSpec (scenario_io.hpp:128-465). */
 int ms_scenario_normalize(const char* scenario_json, char** out_json, char* err, size_t err_len);
 

@@ -47,6 +47,7 @@ def lib() -> C.CDLL:
             "msref_generate_bursty_arrivals": (C.c_int, [D, D, I64, U64, I64, C.POINTER(I64), S, C.POINTER(S),
                                                          P, S]),
             "msref_replay_run": (C.c_int, [P, P, C.c_int, C.POINTER(C.c_void_p), P, S]),
+            "msref_replay_run_opts": (C.c_int, [P, P, P, C.c_int, C.POINTER(C.c_void_p), P, S]),
             "msref_parallel_runs": (C.c_int, [P, P, C.c_int, C.POINTER(D), P, S]),
             "msref_free": (None, [C.c_void_p]),
         }
@@ -182,11 +183,12 @@ def generate_bursty_arrivals(rate, burstiness, horizon_ns, seed, dwell_ns=2_000_
         return list(out[: n.value])
 
 
-def run_scenario(scenario, policy, ndjson=False, report=False, delays=False):
+def run_scenario(scenario, policy, ndjson=False, report=False, delays=False, options=None):
     flags = (1 if ndjson else 0) | (2 if report else 0) | (4 if delays else 0)
     out, err = C.c_void_p(), C.create_string_buffer(4096)
     L = lib()
-    _chk(L.msref_replay_run(_j(scenario), policy.encode(), flags, C.byref(out), err, 4096), err)
+    opts = json.dumps(options).encode() if options else None
+    _chk(L.msref_replay_run_opts(_j(scenario), policy.encode(), opts, flags, C.byref(out), err, 4096), err)
     s = C.cast(out, C.c_char_p).value.decode()
     L.msref_free(out)
     return json.loads(s)

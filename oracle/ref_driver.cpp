@@ -312,14 +312,24 @@ int msref_generate_bursty_arrivals(double rate, double b, int64_t horizon, uint6
 }
 
 // Engine(ScenarioSpec, Policy).run() on the reference; same digest schema as ms_replay_run.
-int msref_replay_run(const char* scenario_json, const char* policy, int flags, char** out_json, char* err,
-                     size_t el) {
+int msref_replay_run_opts(const char* scenario_json, const char* policy, const char* options_json, int flags,
+                          char** out_json, char* err, size_t el) {
   return guarded(err, el, [&] {
     ScenarioSpec sc = scenario_from_json(json::parse(scenario_json));
     auto pol = parse_policy(policy);
     if (!pol) throw ValidationError("policy", "unknown policy");
+    EngineOptions eo;
+    if (options_json && *options_json) {
+      json o = json::parse(options_json);
+      if (o.contains("hint_filter")) {
+        eo.hint_filter.emplace();
+        for (const auto& k : o.at("hint_filter")) eo.hint_filter->insert(k.get<std::string>());
+      }
+      if (o.value("global_floor", false)) eo.rounding = CapacityRounding::GlobalFloor;
+      eo.util_sample_period = o.value("util_sample_period_ns", (long long)eo.util_sample_period);
+    }
     auto t0 = std::chrono::steady_clock::now();
-    RunArtifacts art = run_scenario(sc, *pol);
+    RunArtifacts art = run_scenario(sc, *pol, eo);
     double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::string text;
     json d = digest(art, (flags & 1) != 0, &text);
@@ -331,13 +341,18 @@ int msref_replay_run(const char* scenario_json, const char* policy, int flags, c
       d["delays"] = delays;
     }
     if (flags & 2) {
-      RunArtifacts ex = run_scenario(sc, Policy::Exclusive);
-      RunArtifacts exlp = run_scenario(sc, Policy::ExclusiveLp);
+      RunArtifacts ex = run_scenario(sc, Policy::Exclusive, eo);
+      RunArtifacts exlp = run_scenario(sc, Policy::ExclusiveLp, eo);
       d["report"] = report_to_json(build_report(art, compute_slo(ex), exlp.lp_throughput_per_s()));
     }
     *out_json = dup(d.dump());
     return 0;
   });
+}
+
+int msref_replay_run(const char* scenario_json, const char* policy, int flags, char** out_json, char* err,
+                     size_t el) {
+  return msref_replay_run_opts(scenario_json, policy, nullptr, flags, out_json, err, el);
 }
 
 // CPU baseline: `n_threads` independent Engine::run() of the scenario under `policy`

@@ -78,6 +78,7 @@ def core() -> C.CDLL:
             "ms_generate_bursty_arrivals": (C.c_int, [D, D, I64, U64, I64, C.POINTER(I64), S, C.POINTER(S),
                                                       P, S]),
             "ms_replay_run": (C.c_int, [P, P, C.c_int, C.POINTER(C.c_void_p), P, S]),
+            "ms_replay_run_opts": (C.c_int, [P, P, P, C.c_int, C.POINTER(C.c_void_p), P, S]),
             "ms_scenario_normalize": (C.c_int, [P, C.POINTER(C.c_void_p), P, S]),
             "ms_free": (None, [C.c_void_p]),
         }
@@ -113,8 +114,9 @@ def _js(x) -> bytes:
     return (x if isinstance(x, str) else json.dumps(x)).encode()
 
 
-def replay_run(scenario, policy: str, flags: int = 0) -> dict:
-    """Engine(ScenarioSpec, Policy).run() on the replay backend; returns the artifacts digest."""
+def replay_run(scenario, policy: str, flags: int = 0, options: dict | None = None) -> dict:
+    """Engine(ScenarioSpec, Policy, EngineOptions).run() on the replay backend; returns the artifacts digest."""
     lib, err, out = core(), errbuf(), C.c_void_p()
-    check(lib.ms_replay_run(_js(scenario), policy.encode(), flags, C.byref(out), err, len(err)), err)
+    opts = json.dumps(options).encode() if options else None
+    check(lib.ms_replay_run_opts(_js(scenario), policy.encode(), opts, flags, C.byref(out), err, len(err)), err)
     return json.loads(take_string(lib, out))

@@ -110,6 +110,7 @@ struct ms_dev {
   HpChain chains[MS_MAX_HP_CHAINS];
   int next_hp_ctl = MS_MAX_LP;
   int stream_memops = 0;
+  uint32_t hp_seq = 0;  // monotonic doorbell sequence of this device
 };
 
 namespace {
@@ -158,13 +159,28 @@ int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap
   return 0;
 }
 
+bool is_copy(const ms_hp_op& op) { return op.kind == MS_HP_H2D || op.kind == MS_HP_D2H; }
+
 int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq) {
   const HpOpRt& o = ch.ops[i];
+  if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
+    MS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(o.op.c), reinterpret_cast<const void*>(o.op.a),
+                            static_cast<size_t>(o.op.m), cudaMemcpyDefault, d->hp));
+    if (i + 1 == ch.ops.size()) {
+      hp_notify_kernel<<<1, 1, 0, d->hp>>>(d->hp_ctl + chain_id, &d->page_d->hp[chain_id], seq);
+      MS_CUDA(cudaGetLastError());
+    }
+    return 0;
+  }
+  // first / last *kernel* of the chain carry the chain's start stamp / completion record
+  size_t first_k = 0, last_k = ch.ops.size() - 1;
+  while (first_k < ch.ops.size() && is_copy(ch.ops[first_k].op)) ++first_k;
+  while (last_k > 0 && is_copy(ch.ops[last_k].op)) --last_k;
   TileRun r = base_run(d, o.ctl_index);
   r.hp_ctl = d->hp_ctl + chain_id;
   r.hp_rec = &d->page_d->hp[chain_id];
-  r.hp_first = i == 0;
-  r.hp_last = i + 1 == ch.ops.size();
+  r.hp_first = i == first_k;
+  r.hp_last = i == last_k && !is_copy(ch.ops.back().op);
   r.hp_seq = seq;
   if (o.op.kind == MS_HP_GEMM) {
     GemmParams p{};
@@ -279,6 +295,18 @@ int ms_dev_sync(ms_dev* d) {
   return 0;
 }
 
+int ms_host_alloc(ms_dev* d, size_t bytes, uint64_t* p) {
+  MS_CUDA(cudaSetDevice(d->ordinal));
+  void* ptr = nullptr;
+  MS_CUDA(cudaHostAlloc(&ptr, bytes, cudaHostAllocPortable));
+  *p = reinterpret_cast<uint64_t>(ptr);
+  return 0;
+}
+int ms_host_free(ms_dev*, uint64_t p) {
+  MS_CUDA(cudaFreeHost(reinterpret_cast<void*>(p)));
+  return 0;
+}
+
 int ms_mem_alloc(ms_dev* d, size_t bytes, uint64_t* p) {
   MS_CUDA(cudaSetDevice(d->ordinal));
   void* ptr = nullptr;
@@ -355,6 +383,10 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
 }
 
 int ms_lp_run(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget) {
+  return ms_lp_run_ex(d, id, begin, end, budget, 0);
+}
+
+int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget, int flags) {
   if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
   LpSlot& s = d->lp_slots[id];
   if (end > s.total_tiles || begin > end) return fail(MS_E_ARG, "tile range out of bounds");
@@ -368,13 +400,15 @@ int ms_lp_run(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget) 
   r.nr_in = static_cast<unsigned int>(nr_in);
   r.redo_in = s.redo[(run_id - 1) & 1];
   r.redo_out = s.redo[run_id & 1];
-  r.preemptible = 1;
+  r.preemptible = (flags & MS_RUN_NONPREEMPTIBLE) ? 0 : 1;
+  r.host_progress = reinterpret_cast<unsigned long long*>(&d->page_d->progress[id]);
   r.run_epoch = __atomic_load_n(&d->page->epoch, __ATOMIC_ACQUIRE);
   r.host_budget = &d->page_d->budget[id];
   r.slot = id;
   r.exit_rec = &d->page_d->lp_exit[id];
   r.run_id = run_id;
   __atomic_store_n(&d->page->budget[id], ((run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
+  __atomic_store_n(&d->page->progress[id], 0ull, __ATOMIC_RELEASE);
   s.last_begin = begin;
   s.last_end = end;
   s.last_redo_in = nr_in;
@@ -413,6 +447,14 @@ int ms_lp_run(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget) 
   }
   MS_CUDA(cudaGetLastError());
   return 0;
+}
+
+uint64_t ms_lp_total_tiles(ms_dev* d, int id) {
+  return (id >= 0 && id < MS_MAX_LP && d->lp_slots[id].used) ? d->lp_slots[id].total_tiles : 0;
+}
+
+uint64_t ms_lp_progress(ms_dev* d, int id) {
+  return __atomic_load_n(&d->page->progress[id], __ATOMIC_ACQUIRE);
 }
 
 int ms_lp_set_budget(ms_dev* d, int id, uint64_t budget) {
@@ -497,7 +539,9 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
       if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
     } else if (o.op.kind == MS_HP_BIAS_GELU) {
-      if (o.op.n % (8 * 256) && o.op.n % 8) return fail(MS_E_ARG, "bias_gelu cols must be a multiple of 8");
+      if (o.op.n % 8) return fail(MS_E_ARG, "bias_gelu cols must be a multiple of 8");
+    } else if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
+      if (o.op.m <= 0) return fail(MS_E_ARG, "copy size must be > 0");
     } else {
       return fail(MS_E_ARG, "unknown HP op");
     }
@@ -518,6 +562,8 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
     if (int rc = launch_hp_op(d, cid, ch, i, seq)) return rc;
   return 0;
 }
+
+uint32_t ms_hp_next_seq(ms_dev* d) { return ++d->hp_seq; }
 
 int ms_hp_ring(ms_dev* d, uint32_t seq, int64_t* t_host) {
   __atomic_store_n(&d->page->doorbell, seq, __ATOMIC_RELEASE);

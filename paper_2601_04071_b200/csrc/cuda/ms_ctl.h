@@ -46,7 +46,7 @@ struct MsHostPage {
   uint32_t doorbell;              // HP doorbell sequence
   uint32_t pad1[31];
   uint64_t budget[MS_MAX_LP];     // soft end (tile id) per LP slot
-  uint64_t pad2[16 - MS_MAX_LP];
+  uint64_t progress[MS_MAX_LP];   // device -> host: claim counter of the running LP run
   MsLpExit lp_exit[MS_MAX_LP];
   MsHpRecord hp[MS_MAX_HP_CHAINS];
   uint32_t ping, pad3[31];        // clock calibration echo

@@ -169,6 +169,16 @@ __global__ void gate_kernel(const uint32_t* doorbell, unsigned int seq, MsHpReco
   st_release_sys_u32(&rec->seq_gate, seq);
 }
 
+// Completion record of a chain whose last op is a copy (e2e mode): written after the D2H.
+__global__ void hp_notify_kernel(MsHpCtl* ctl, MsHpRecord* rec, unsigned int seq) {
+  const unsigned long long t = globaltimer();
+  st_relaxed_sys_u64(&rec->t_first_cta, ctl->t_first_cta);
+  st_relaxed_sys_u64(&rec->t_done, t);
+  fence_sys();
+  st_release_sys_u32(&rec->seq_done, seq);
+  ctl->t_first_cta = ~0ull;
+}
+
 // ---------------------------------------------------------------- clock calibration echo
 __global__ void echo_kernel(const uint32_t* ping, uint32_t* pong, unsigned long long* stamps, int rounds) {
   for (int k = 1; k <= rounds; ++k) {

@@ -33,6 +33,7 @@ struct TileRun {
   MsDevMirror* mirror;
   int slot;
   MsLpExit* exit_rec;
+  unsigned long long* host_progress;  // CTA 0's poller publishes the claim counter here
   unsigned long long run_id;
   // HP chain notification (null for LP runs)
   MsHpCtl* hp_ctl;
@@ -83,6 +84,8 @@ __device__ __forceinline__ void run_poller(const TileRun& r, uint32_t* preempt, 
     }
     uint32_t e;
     if (leader) {
+      if (r.host_progress)
+        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(r.host_progress), ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&r.ctl->claim)));
       e = ld_acquire_sys(r.host_epoch);
       st_relaxed_gpu_u64(&r.mirror->budget[r.slot][0], ld_acquire_sys_u64(r.host_budget));
       if (e > mirrored) {

@@ -306,12 +306,27 @@ int ms_generate_bursty_arrivals(double rate, double burstiness, int64_t horizon_
 
 int ms_replay_run(const char* scenario_json, const char* policy, int flags, char** out_json, char* err,
                   size_t err_len) {
+  return ms_replay_run_opts(scenario_json, policy, nullptr, flags, out_json, err, err_len);
+}
+
+int ms_replay_run_opts(const char* scenario_json, const char* policy, const char* options_json, int flags,
+                       char** out_json, char* err, size_t err_len) {
   return guarded(err, err_len, [&] {
     const ScenarioSpec sc = scenario_from_json(parse_or_throw(scenario_json));
     const auto pol = parse_policy(policy ? policy : "");
     if (!pol) throw ValidationError("policy", std::string("unknown policy '") + (policy ? policy : "") + "'");
+    EngineOptions eo;
+    if (options_json && *options_json) {
+      const json o = json::parse(options_json);
+      if (o.contains("hint_filter")) {
+        eo.hint_filter.emplace();
+        for (const json& k : o.at("hint_filter")) eo.hint_filter->insert(k.get<std::string>());
+      }
+      if (o.value("global_floor", false)) eo.rounding = CapacityRounding::GlobalFloor;
+      eo.util_sample_period = o.value("util_sample_period_ns", static_cast<long long>(eo.util_sample_period));
+    }
     const auto t0 = std::chrono::steady_clock::now();
-    Engine eng(sc, *pol);
+    Engine eng(sc, *pol, eo);
     RunArtifacts art = eng.run();
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     json d = digest(art);
@@ -324,8 +339,8 @@ int ms_replay_run(const char* scenario_json, const char* policy, int flags, char
       d["delays"] = std::move(delays);
     }
     if (flags & MS_RUN_REPORT) {
-      const RunArtifacts ex = run_scenario(sc, Policy::Exclusive);
-      const RunArtifacts exlp = run_scenario(sc, Policy::ExclusiveLp);
+      const RunArtifacts ex = run_scenario(sc, Policy::Exclusive, eo);
+      const RunArtifacts exlp = run_scenario(sc, Policy::ExclusiveLp, eo);
       const SloThresholds slo = compute_slo(ex);
       d["report"] = report_to_json(build_report(art, slo, exlp.lp_throughput_per_s()));
     }

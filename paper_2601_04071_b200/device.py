@@ -12,7 +12,7 @@ from dataclasses import dataclass
 from . import _native
 
 MS_LP_GEMM, MS_LP_AXPY = 1, 2
-MS_HP_GEMM, MS_HP_BIAS_GELU = 1, 2
+MS_HP_GEMM, MS_HP_BIAS_GELU, MS_HP_H2D, MS_HP_D2H = 1, 2, 3, 4
 
 
 class DeviceError(RuntimeError):
@@ -73,6 +73,7 @@ def lib() -> C.CDLL:
             "ms_dev_get_info": (I, [P, C.POINTER(DevInfo)]), "ms_dev_sync": (I, [P]),
             "ms_last_error": (C.c_char_p, []), "ms_host_now_ns": (I64, []),
             "ms_mem_alloc": (I, [P, C.c_size_t, C.POINTER(U64)]), "ms_mem_free": (I, [P, U64]),
+            "ms_host_alloc": (I, [P, C.c_size_t, C.POINTER(U64)]), "ms_host_free": (I, [P, U64]),
             "ms_memcpy_h2d": (I, [P, U64, P, C.c_size_t]), "ms_memcpy_d2h": (I, [P, P, U64, C.c_size_t]),
             "ms_memset": (I, [P, U64, I, C.c_size_t]),
             "ms_fill_synth_bf16": (I, [P, U64, U64, U64, U64, F]),
@@ -83,6 +84,8 @@ def lib() -> C.CDLL:
             "ms_preempt_raise": (I, [P, C.POINTER(U32), C.POINTER(I64)]), "ms_preempt_epoch": (U32, [P]),
             "ms_hp_register_chain": (I, [P, C.POINTER(HpOp), I, C.POINTER(I)]),
             "ms_hp_arm": (I, [P, I, U32]), "ms_hp_ring": (I, [P, U32, C.POINTER(I64)]),
+            "ms_hp_next_seq": (U32, [P]), "ms_lp_total_tiles": (U64, [P, I]), "ms_lp_progress": (U64, [P, I]),
+            "ms_lp_run_ex": (I, [P, I, U64, U64, U64, I]),
             "ms_hp_launch_direct": (I, [P, I, U32]),
             "ms_hp_poll": (I, [P, I, U32, C.POINTER(HpTimes)]),
             "ms_hp_wait": (I, [P, I, U32, I64, C.POINTER(HpTimes)]),
@@ -140,6 +143,14 @@ class Device:
         p = C.c_uint64()
         _ck(lib().ms_mem_alloc(self._h, nbytes, C.byref(p)))
         return p.value
+
+    def host_alloc(self, nbytes: int) -> int:
+        p = C.c_uint64()
+        _ck(lib().ms_host_alloc(self._h, nbytes, C.byref(p)))
+        return p.value
+
+    def host_free(self, ptr: int):
+        _ck(lib().ms_host_free(self._h, ptr))
 
     def free(self, ptr: int):
         _ck(lib().ms_mem_free(self._h, ptr))
@@ -214,6 +225,9 @@ class Device:
         cid = C.c_int()
         _ck(lib().ms_hp_register_chain(self._h, arr, len(ops), C.byref(cid)))
         return cid.value
+
+    def hp_next_seq(self) -> int:
+        return lib().ms_hp_next_seq(self._h)
 
     def hp_arm(self, chain: int, seq: int):
         _ck(lib().ms_hp_arm(self._h, chain, seq))

@@ -1,0 +1,110 @@
+"""Live B200 runs of the BASELINE configs through the C++ scheduler (include/ms_live.h).
+
+Python only allocates the tenants' synthetic tensors, registers the sm_100a kernels,
+and hands the scenario + bindings to ms_live_run, which runs Algorithm 1 in C++ on
+this thread in real time.  Policies: splitkernel (this system), exclusive (HP alone ->
+SLO), exclusive_lp (LP alone -> LP throughput reference), reef (kernel-boundary
+temporal sharing baseline).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+
+from . import scenarios
+from .device import Device, _ck, lib as dev_lib
+
+SEED = 20260117
+
+
+def _live_lib():
+    L = dev_lib()
+    if not hasattr(L, "_ms_live_sig"):
+        L.ms_live_run.restype = C.c_int
+        L.ms_live_run.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                  C.POINTER(C.c_void_p)]
+        L.ms_live_free.argtypes = [C.c_void_p]
+        L._ms_live_sig = True
+    return L
+
+
+def live_run(dev: Device, scenario: dict, policy: str, binding: dict, options: dict | None = None) -> dict:
+    L = _live_lib()
+    out = C.c_void_p()
+    rc = L.ms_live_run(dev._h, json.dumps(scenario).encode(), policy.encode(), json.dumps(binding).encode(),
+                       json.dumps(options or {}).encode(), C.byref(out))
+    if rc != 0:
+        raise RuntimeError(f"ms_live_run({policy}) failed rc={rc}: {L.ms_last_error().decode(errors='replace')}")
+    s = C.cast(out, C.c_char_p).value.decode()
+    L.ms_live_free(out)
+    return json.loads(s)
+
+
+class Config1:
+    """Config 1 tenants on one B200: HP = 4 x (C[128x4096] = A[128x4096] W_i^T) + bias/GELU,
+    LP = bf16 GEMM loop M = N = K = 8192 (128x256 tiles, 2048 tiles per GEMM)."""
+
+    M_HP, H = 128, 4096
+    N_LP = 8192
+
+    def __init__(self, dev: Device, seed: int = SEED):
+        self.dev = dev
+        n, H, M = self.N_LP, self.H, self.M_HP
+        self.a = dev.alloc(n * n * 2)
+        self.b = dev.alloc(n * n * 2)
+        self.c = dev.alloc(n * n * 2)
+        dev.fill_synth(self.a, n * n, seed, 1, 1.0)
+        dev.fill_synth(self.b, n * n, seed, 2, 1.0 / math.sqrt(n))
+        self.lp = dev.lp_register_gemm(self.a, self.b, self.c, n, n, n, block_n=256)
+        self.act = [dev.alloc(M * H * 2) for _ in range(5)]
+        self.w = [dev.alloc(H * H * 2) for _ in range(4)]
+        self.bias = dev.alloc(H * 2)
+        dev.fill_synth(self.act[0], M * H, seed, 100, 1.0)
+        for i, w in enumerate(self.w):
+            dev.fill_synth(w, H * H, seed, 101 + i, 1.0 / math.sqrt(H))
+        dev.fill_synth(self.bias, H, seed, 110, 0.1)
+        ops = [dict(kind=1, block_n=64, a=self.act[i], b=self.w[i], c=self.act[i + 1], bias=0, m=M, n=H, k=H)
+               for i in range(4)]
+        ops.append(dict(kind=2, block_n=0, a=self.act[4], b=0, c=self.act[0], bias=self.bias, m=M, n=H, k=0))
+        self.chain = dev.hp_register_chain(ops)
+        # e2e chain: the request's input activation arrives from pinned host memory after
+        # the doorbell and the output returns to pinned host memory before completion.
+        self.io_bytes = M * H * 2
+        self.host_in = dev.host_alloc(self.io_bytes)
+        self.host_out = dev.host_alloc(self.io_bytes)
+        self.act_out = dev.alloc(self.io_bytes)
+        dev.d2h(self.host_in, self.act[0], self.io_bytes)
+        e2e = [dict(kind=3, block_n=0, a=self.host_in, b=0, c=self.act[0], bias=0, m=self.io_bytes, n=0, k=0)]
+        e2e += ops[:4]
+        e2e.append(dict(kind=2, block_n=0, a=self.act[4], b=0, c=self.act_out, bias=self.bias, m=M, n=H, k=0))
+        e2e.append(dict(kind=4, block_n=0, a=self.act_out, b=0, c=self.host_out, bias=0, m=self.io_bytes, n=0, k=0))
+        self.chain_e2e = dev.hp_register_chain(e2e)
+        self.calib = None
+
+    def binding(self, e2e: bool = False) -> dict:
+        return {"lp": {"lp_gemm_8192": self.lp.id}, "hp": {"hp_infer": [self.chain_e2e if e2e else self.chain]}}
+
+    def calibrate(self, reps: int = 5) -> dict:
+        """Measured per-tile / per-chain times feeding both the live pacing and the replay
+        scenario (KernelSpec calibrated from the B200 kernels)."""
+        ms_gemm = self.dev.lp_time_full(self.lp, reps)
+        waves = math.ceil(self.lp.total_tiles / self.dev.info["sm_count"])
+        ms_chain = self.dev.hp_time_chain(self.chain, 20)
+        tile_ns = int(ms_gemm * 1e6 / waves)
+        self.calib = {
+            "lp_gemm_ms": ms_gemm,
+            "lp_gemm_tile_ns": tile_ns,
+            "hp_chain_ms": ms_chain,
+            "hp_gemm_tile_ns": int(ms_chain * 1e6 * 0.95 / 4),
+            "hp_ew_tile_ns": max(1000, int(ms_chain * 1e6 * 0.05)),
+        }
+        return self.calib
+
+    def scenario(self, seed: int, horizon_s: float) -> dict:
+        return scenarios.config1(seed=seed, horizon_s=horizon_s, calib=self.calib or {})
+
+    def options(self, **kw) -> dict:
+        o = {"tile_ns": {"lp_gemm_8192": (self.calib or {}).get("lp_gemm_tile_ns", 57000)}, "timeline": True}
+        o.update(kw)
+        return o

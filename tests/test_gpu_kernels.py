@@ -1,0 +1,122 @@
+"""Tenant-kernel numeric parity on B200 (north_star: fp32 rel <= 1e-3, bf16 rel <= 1e-2)
+against the C restatement in oracle/tenant_ref.c, all through the C-ABI."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = 1e-2  # bf16 outputs (north_star)
+SEED = 99
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2601_04071_b200.device import Device
+    d = Device(0)
+    yield d
+    d.close()
+
+
+@pytest.fixture(scope="module")
+def T():
+    from oracle import tenant
+    return tenant
+
+
+def d2h(dev, ptr, n):
+    out = np.empty(n, np.uint16)
+    dev.d2h(out.ctypes.data, ptr, n * 2)
+    return out
+
+
+def test_synthetic_generator_is_bit_identical(dev, T):
+    n = 1 << 20
+    p = dev.alloc(2 * n)
+    for tensor, scale in ((1, 1.0), (9, 0.03125), (77, float(np.float32(1 / math.sqrt(4096))))):
+        dev.fill_synth(p, n, SEED, tensor, scale)
+        assert np.array_equal(d2h(dev, p, n), T.synth_bf16(n, SEED, tensor, scale))
+    dev.free(p)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (256, 512, 320, 256), (384, 384, 1024, 128),
+                                      (128, 1024, 512, 64), (1024, 2048, 2048, 256)])
+def test_gemm_matches_oracle(dev, T, M, N, K, bn):
+    a, b, c = dev.alloc(M * K * 2), dev.alloc(N * K * 2), dev.alloc(M * N * 2)
+    s = float(np.float32(1 / math.sqrt(K)))
+    dev.fill_synth(a, M * K, SEED, 1, 1.0)
+    dev.fill_synth(b, N * K, SEED, 2, s)
+    dev.memset(c, 0xFF, M * N * 2)
+    k = dev.lp_register_gemm(a, b, c, M, N, K, block_n=bn)
+    dev.lp_run(k, 0, k.total_tiles)
+    st = dev.lp_wait(k, 30)
+    assert st["tiles_done"] == k.total_tiles and st["cursor"] == k.total_tiles and st["redo_count"] == 0
+    rows = list(range(M)) if M <= 384 else list(range(0, M, 7))
+    want = T.gemm_rows(T.synth_bf16(M * K, SEED, 1, 1.0), T.synth_bf16(N * K, SEED, 2, s), rows, N, K)
+    got = T.bf16_to_f32(d2h(dev, c, M * N).reshape(M, N)[rows].reshape(-1)).reshape(len(rows), N)
+    rel = np.max(np.abs(got - want)) / np.max(np.abs(want))
+    assert rel <= BF16_TOL, rel
+    for p in (a, b, c):
+        dev.free(p)
+
+
+def test_gemm_8192_sampled_tiles(dev, T):
+    """Full config-1 LP GEMM; >= 64 sampled output rows spanning every M tile."""
+    n = 8192
+    a, b, c = dev.alloc(n * n * 2), dev.alloc(n * n * 2), dev.alloc(n * n * 2)
+    s = float(np.float32(1 / math.sqrt(n)))
+    dev.fill_synth(a, n * n, SEED, 1, 1.0)
+    dev.fill_synth(b, n * n, SEED, 2, s)
+    k = dev.lp_register_gemm(a, b, c, n, n, n, block_n=256)
+    dev.lp_run(k, 0, k.total_tiles)
+    dev.lp_wait(k, 60)
+    rows = [t * 128 + (t * 37) % 128 for t in range(64)]
+    want = T.gemm_rows(T.synth_bf16(n * n, SEED, 1, 1.0), T.synth_bf16(n * n, SEED, 2, s), rows, n, n)
+    C = d2h(dev, c, n * n).reshape(n, n)
+    got = T.bf16_to_f32(C[rows].reshape(-1)).reshape(len(rows), n)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+    for p in (a, b, c):
+        dev.free(p)
+
+
+@pytest.mark.parametrize("n,tile", [(1 << 20, 8192), (3 * 8192 + 8 * 5, 2048), (1 << 24, 16384)])
+def test_axpy_bit_exact(dev, T, n, tile):
+    x, y = dev.alloc(2 * n), dev.alloc(2 * n)
+    dev.fill_synth(x, n, SEED, 11, 1.0)
+    dev.fill_synth(y, n, SEED, 12, 1.0)
+    k = dev.lp_register_axpy(x, y, n, -0.375, tile_elems=tile)
+    dev.lp_run(k, 0, k.total_tiles)
+    dev.lp_wait(k, 30)
+    want = T.axpy(T.synth_bf16(n, SEED, 12, 1.0), T.synth_bf16(n, SEED, 11, 1.0), -0.375)
+    assert np.array_equal(d2h(dev, y, n), want)
+    dev.free(x)
+    dev.free(y)
+
+
+def test_hp_chain_matches_oracle(dev, T):
+    """Config-1 HP chain: 4 chained GEMMs + bias/GELU; fp32-accumulated bf16 ops."""
+    M, H = 128, 1024
+    act = [dev.alloc(M * H * 2) for _ in range(5)]
+    ws = [dev.alloc(H * H * 2) for _ in range(4)]
+    bias = dev.alloc(H * 2)
+    s = float(np.float32(1 / math.sqrt(H)))
+    dev.fill_synth(act[0], M * H, SEED, 100, 1.0)
+    for i, w in enumerate(ws):
+        dev.fill_synth(w, H * H, SEED, 101 + i, s)
+    dev.fill_synth(bias, H, SEED, 110, 0.1)
+    ops = [dict(kind=1, block_n=64, a=act[i], b=ws[i], c=act[i + 1], bias=0, m=M, n=H, k=H) for i in range(4)]
+    out = dev.alloc(M * H * 2)
+    ops.append(dict(kind=2, block_n=0, a=act[4], b=0, c=out, bias=bias, m=M, n=H, k=0))
+    chain = dev.hp_register_chain(ops)
+    dev.hp_launch_direct(chain, dev.hp_next_seq())
+    dev.sync()
+    x = T.synth_bf16(M * H, SEED, 100, 1.0)
+    for i in range(4):   # oracle chain, rounding to bf16 between ops like the device does
+        y = T.gemm_rows(x, T.synth_bf16(H * H, SEED, 101 + i, s), list(range(M)), H, H).reshape(-1)
+        x = np.ascontiguousarray((y.view(np.uint32) + 0x7FFF + ((y.view(np.uint32) >> 16) & 1)) >> 16).astype(np.uint16)
+        got_i = T.bf16_to_f32(d2h(dev, act[i + 1], M * H))
+        ref_i = T.bf16_to_f32(x)
+        assert np.max(np.abs(got_i - ref_i)) / np.max(np.abs(ref_i)) <= BF16_TOL, i
+    want = T.bf16_to_f32(T.bias_gelu(d2h(dev, act[4], M * H), T.synth_bf16(H, SEED, 110, 0.1), M, H))
+    got = T.bf16_to_f32(d2h(dev, out, M * H))
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL

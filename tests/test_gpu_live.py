@@ -1,0 +1,28 @@
+"""Live Algorithm-1 run on B200 through ms_live_run: HP requests are served, LP work is
+harvested and preempted, and every preemption is measured."""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_live_config1_short():
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config1, live_run
+    dev = Device(0)
+    w = Config1(dev)
+    w.calibrate(reps=2)
+    sc = w.scenario(seed=11, horizon_s=0.4)
+    ex = live_run(dev, sc, "exclusive", w.binding(), w.options())
+    sk = live_run(dev, sc, "splitkernel", w.binding(), w.options())
+    kb = live_run(dev, sc, "reef", w.binding(), w.options())
+    lp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options())
+    assert ex["requests"]["n"] == sk["requests"]["n"] > 5
+    assert sk["requests"]["completed"] >= sk["requests"]["n"] - 1
+    assert sk["lp"]["tiles_done"] > 0 and sk["lp"]["preemptions"] > 0
+    assert sk["preempt_ring_to_first_hp_cta"]["n"] >= sk["hp_chains"] - 1
+    assert 0 < sk["preempt_ring_to_first_hp_cta"]["p50_ns"] < 200_000
+    assert lp["lp"]["tiles_done"] > sk["lp"]["tiles_done"] > 0
+    assert kb["lp"]["tiles_done"] > 0
+    e2e = live_run(dev, sc, "splitkernel", w.binding(e2e=True), w.options())
+    assert e2e["hp_chains"] > 0 and e2e["requests"]["completed"] > 0
+    dev.close()
