@@ -102,6 +102,8 @@ typedef struct ms_lp_status {
 
 /* Register a preemptible LP kernel; *total_tiles = size of its linear tile space. */
 int ms_lp_register(ms_dev* dev, const ms_lp_desc* desc, int* id, uint64_t* total_tiles);
+/* Release a slot (waits for the LP stream). */
+int ms_lp_unregister(ms_dev* dev, int id);
 /* Launch (async, low-priority stream) over fresh tiles [begin, end) plus the redo tiles
  * carried from the previous run; tiles >= budget are not started (budget <= end). */
 int ms_lp_run(ms_dev* dev, int id, uint64_t begin, uint64_t end, uint64_t budget);

@@ -351,7 +351,9 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     }
   if (slot < 0) return fail(MS_E_ARG, "too many LP kernels");
   LpSlot& s = d->lp_slots[slot];
+  const uint64_t keep_run_id = s.run_id;
   s = LpSlot{};
+  s.run_id = keep_run_id;
   s.desc = *desc;
   if (desc->kind == MS_LP_GEMM) {
     const int bn = desc->block_n ? desc->block_n : 256;
@@ -379,6 +381,20 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
   s.used = true;
   *id = slot;
   *total_tiles = s.total_tiles;
+  return 0;
+}
+
+int ms_lp_unregister(ms_dev* d, int id) {
+  if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
+  MS_CUDA(cudaStreamSynchronize(d->lp));
+  LpSlot& s = d->lp_slots[id];
+  for (auto*& r : s.redo) {
+    if (r) cudaFree(r);
+    r = nullptr;
+  }
+  const uint64_t keep_run_id = s.run_id;  // run ids stay monotonic per slot (exit records)
+  s = LpSlot{};
+  s.run_id = keep_run_id;
   return 0;
 }
 

@@ -15,7 +15,7 @@
 #pragma once
 #include <stdint.h>
 
-#define MS_MAX_LP 8
+#define MS_MAX_LP 16
 #define MS_MAX_HP_CHAINS 8
 #define MS_MIRROR_COPIES 8
 #define MS_MIRROR_STRIDE 32  // uint32 elements = 128 B

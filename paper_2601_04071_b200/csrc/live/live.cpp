@@ -94,6 +94,8 @@ class LiveRun {
     want_hp_ = policy_ != "exclusive_lp";
     want_lp_ = policy_ != "exclusive";
     eager_ = opts.value("eager", false);
+    direct_hp_ = opts.value("direct_hp", false);  // profiler-safe: no gate kernels
+    calibrate_ = opts.value("calibrate", true);
     record_ = opts.value("timeline", true);
     ms_dev_info info{};
     ms_dev_get_info(dev_, &info);
@@ -181,7 +183,7 @@ class LiveRun {
 
   // ---------------------------------------------------------------- HP driver
   void arm(HpTask& h, std::size_t seg) {
-    if (h.chain[seg] < 0 || h.armed[seg]) return;
+    if (direct_hp_ || h.chain[seg] < 0 || h.armed[seg]) return;
     const uint32_t s = ms_hp_next_seq(dev_);
     last_seq_ = s;
     check(ms_hp_arm(dev_, h.chain[seg], s), "ms_hp_arm");
@@ -222,13 +224,18 @@ class LiveRun {
     if (hp_active_ == 0) hp_turned_active();
     ++hp_active_;
     int64_t t_ring = 0;
-    h.seq = h.armed[h.seg];
-    h.armed[h.seg] = 0;
-    if (reef_ && lp_running_) {
-      // kernel-boundary sharing: the HP chain is released now but cannot get SMs before
-      // the running (non-preemptible) LP kernel drains.
+    if (direct_hp_) {
+      // Baseline / profiler-safe path: a host launch sits on the critical path.
+      h.seq = ms_hp_next_seq(dev_);
+      t_ring = mono_ns();
+      check(ms_hp_launch_direct(dev_, h.chain[h.seg], h.seq), "ms_hp_launch_direct");
+    } else {
+      // Kernel-boundary sharing (reef) also rings immediately: the released chain cannot
+      // get SMs before the running non-preemptible LP kernel drains.
+      h.seq = h.armed[h.seg];
+      h.armed[h.seg] = 0;
+      check(ms_hp_ring(dev_, h.seq, &t_ring), "ms_hp_ring");
     }
-    check(ms_hp_ring(dev_, h.seq, &t_ring), "ms_hp_ring");
     h.ring_t = t_ring - t0_;
     h.inflight = true;
     emit(h.ring_t, EventKind::Launch, h.index, h.spec->name, "seq=" + std::to_string(h.seq));
@@ -478,6 +485,7 @@ class LiveRun {
   json lp_bind_ = json::object();
   json tile_ns_ = json::object();
   bool harvest_ = false, reef_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
+  bool direct_hp_ = false, calibrate_ = true;
   int n_sm_ = 148;
   int64_t t0_ = 0, off0_ = 0, off1_ = 0, c0_ = 0, c1_ = 0;
   uint32_t last_seq_ = 0;
@@ -541,7 +549,7 @@ json LiveRun::run() {
   int64_t rtt = 0, rtt1 = 0;
   {
     const int64_t a = mono_ns();
-    check(ms_clock_calibrate(dev_, 200, &off0_, &rtt), "ms_clock_calibrate");
+    if (calibrate_) check(ms_clock_calibrate(dev_, 200, &off0_, &rtt), "ms_clock_calibrate");
     c0_ = (a + mono_ns()) / 2;
   }
   // Pre-arm segment 0 of every HP task; schedule arrivals.
@@ -606,7 +614,8 @@ json LiveRun::run() {
   ms_dev_sync(dev_);
   {
     const int64_t a = mono_ns();
-    check(ms_clock_calibrate(dev_, 200, &off1_, &rtt1), "ms_clock_calibrate");
+    if (calibrate_) check(ms_clock_calibrate(dev_, 200, &off1_, &rtt1), "ms_clock_calibrate");
+    else off1_ = off0_;
     c1_ = (a + mono_ns()) / 2;
   }
   // Convert the device-side samples and emit the device-timed decision events.

@@ -85,7 +85,7 @@ def lib() -> C.CDLL:
             "ms_hp_register_chain": (I, [P, C.POINTER(HpOp), I, C.POINTER(I)]),
             "ms_hp_arm": (I, [P, I, U32]), "ms_hp_ring": (I, [P, U32, C.POINTER(I64)]),
             "ms_hp_next_seq": (U32, [P]), "ms_lp_total_tiles": (U64, [P, I]), "ms_lp_progress": (U64, [P, I]),
-            "ms_lp_run_ex": (I, [P, I, U64, U64, U64, I]),
+            "ms_lp_run_ex": (I, [P, I, U64, U64, U64, I]), "ms_lp_unregister": (I, [P, I]),
             "ms_hp_launch_direct": (I, [P, I, U32]),
             "ms_hp_poll": (I, [P, I, U32, C.POINTER(HpTimes)]),
             "ms_hp_wait": (I, [P, I, U32, I64, C.POINTER(HpTimes)]),
@@ -186,6 +186,9 @@ class Device:
         kid, tiles = C.c_int(), C.c_uint64()
         _ck(lib().ms_lp_register(self._h, C.byref(d), C.byref(kid), C.byref(tiles)))
         return LpKernel(kid.value, tiles.value)
+
+    def lp_unregister(self, k: LpKernel):
+        _ck(lib().ms_lp_unregister(self._h, k.id))
 
     def lp_run(self, k: LpKernel, begin: int, end: int, budget: int | None = None):
         _ck(lib().ms_lp_run(self._h, k.id, begin, end, end if budget is None else budget))

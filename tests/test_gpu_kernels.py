@@ -56,6 +56,7 @@ def test_gemm_matches_oracle(dev, T, M, N, K, bn):
     got = T.bf16_to_f32(d2h(dev, c, M * N).reshape(M, N)[rows].reshape(-1)).reshape(len(rows), N)
     rel = np.max(np.abs(got - want)) / np.max(np.abs(want))
     assert rel <= BF16_TOL, rel
+    dev.lp_unregister(k)
     for p in (a, b, c):
         dev.free(p)
 
@@ -75,6 +76,7 @@ def test_gemm_8192_sampled_tiles(dev, T):
     C = d2h(dev, c, n * n).reshape(n, n)
     got = T.bf16_to_f32(C[rows].reshape(-1)).reshape(len(rows), n)
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+    dev.lp_unregister(k)
     for p in (a, b, c):
         dev.free(p)
 
@@ -89,6 +91,7 @@ def test_axpy_bit_exact(dev, T, n, tile):
     dev.lp_wait(k, 30)
     want = T.axpy(T.synth_bf16(n, SEED, 12, 1.0), T.synth_bf16(n, SEED, 11, 1.0), -0.375)
     assert np.array_equal(d2h(dev, y, n), want)
+    dev.lp_unregister(k)
     dev.free(x)
     dev.free(y)
 
