@@ -173,6 +173,29 @@ def run_reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def aggregate_ranks(allr, horizon_total):
+    """Whole-job aggregation of the per-rank (per-GPU replica) results: preemption samples
+    are pooled (p99 over all ranks), SLO attainment = sum met / sum requests, LP rates
+    add up."""
+    slo = allr[0]["slo"]
+
+    def att(rows_key):
+        met = tot = 0
+        for r in allr:
+            rows = r[rows_key]
+            s_ = r.get("slo", slo)
+            met += sum(1 for x in rows if x[4] and x[1] <= s_["ttft_ns"] and x[2] <= s_["tpot_ns"])
+            tot += len(rows)
+        return met / max(1, tot)
+
+    return {"S": [x for r in allr for x in r["samples"]], "LX": [x for r in allr for x in r["lp_exit"]],
+            "E2E": [x for r in allr for x in r["e2e"]],
+            "lp_rate": sum(r["tiles"] for r in allr) / horizon_total,
+            "kb_rate": sum(r["kb_tiles"] for r in allr) / horizon_total,
+            "ex_rate": sum(r["exlp_rate"] for r in allr),
+            "att": att("rows"), "att_ex": att("ex_rows"), "att_kb": att("kb_rows")}
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -230,10 +253,6 @@ def main():
     exlp = live_run(dev, sc(0, args.step_s), "exclusive_lp", w.binding(), w.options(timeline=False))
     exlp_rate = exlp["lp"]["tiles_per_s"]
 
-    def attainment(rows):  # slo_attainment (metrics.hpp:96-105): incomplete requests count against
-        ok = sum(1 for r in rows if r[4] and r[1] <= slo["ttft_ns"] and r[2] <= slo["tpot_ns"])
-        return ok / max(1, len(rows))
-
     # --- warm-up (untimed)
     for i in range(args.warmup):
         live_run(dev, sc(500 + i, args.warmup_s), "splitkernel", w.binding(), w.options(timeline=False))
@@ -280,16 +299,10 @@ def main():
         dev.close()
         return
 
-    S_ = [x for r in allr for x in r["samples"]]
-    LX = [x for r in allr for x in r["lp_exit"]]
-    horizon_total = args.steps * args.step_s
-    lp_rate = sum(r["tiles"] for r in allr) / horizon_total
-    kb_rate = sum(r["kb_tiles"] for r in allr) / horizon_total
-    ex_rate = sum(r["exlp_rate"] for r in allr)
-    att = sum(attainment(r["rows"]) * len(r["rows"]) for r in allr) / max(1, sum(len(r["rows"]) for r in allr))
-    att_ex = sum(attainment(r["ex_rows"]) * len(r["ex_rows"]) for r in allr) / max(1, sum(len(r["ex_rows"]) for r in allr))
-    att_kb = sum(attainment(r["kb_rows"]) * len(r["kb_rows"]) for r in allr) / max(1, sum(len(r["kb_rows"]) for r in allr))
-    E2E = [x for r in allr for x in r["e2e"]]
+    agg = aggregate_ranks(allr, args.steps * args.step_s)
+    S_, LX, E2E = agg['S'], agg['LX'], agg['E2E']
+    lp_rate, kb_rate, ex_rate = agg['lp_rate'], agg['kb_rate'], agg['ex_rate']
+    att, att_ex, att_kb = agg['att'], agg['att_ex'], agg['att_kb']
 
     # roofline of the dominant kernel (LP tcgen05 GEMM, 2*8192^3 per launch), timed alone
     # with CUDA events on its stream (ms_lp_time_full); peak = measured burst bf16.
