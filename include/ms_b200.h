@@ -115,6 +115,12 @@ int ms_lp_run_ex(ms_dev* dev, int id, uint64_t begin, uint64_t end, uint64_t bud
  * first, then fresh tiles), for harvest-budget pacing. */
 uint64_t ms_lp_progress(ms_dev* dev, int id);
 uint64_t ms_lp_total_tiles(ms_dev* dev, int id);
+/* Number of SMs a preemptible LP GEMM grid leaves free (default 0). */
+int ms_set_lp_sm_reserve(ms_dev* dev, int n);
+/* Diagnostics: enable=1 arms per-CTA phase timestamps for subsequent LP runs; enable=0
+ * copies [cta][8] globaltimer stamps (seen, producer done, mma done, epilogue done,
+ * teardown, exit begin, last-exit) into `out` and disarms. */
+int ms_debug_stamps(ms_dev* dev, int enable, unsigned long long* out, size_t n);
 /* Move the running launch's soft end (harvest budget word). */
 int ms_lp_set_budget(ms_dev* dev, int id, uint64_t budget);
 /* Non-blocking: fills *st; returns 1 if the last launch has exited, 0 if running. */
@@ -137,9 +143,13 @@ uint32_t ms_preempt_epoch(ms_dev* dev);
 
 typedef struct ms_hp_op {
   int32_t kind;
-  int32_t block_n;
+  int32_t block_n;   /* GEMM tile N (0: 128) */
   uint64_t a, b, c, bias;
   int64_t m, n, k;
+  int32_t split_k;   /* GEMM k-slices per tile (0: auto — enough units to cover the SMs) */
+  int32_t b_layout;  /* GEMM weights: 0 = row-major [N,K], captured k-block-major at registration
+                        (DRAM-page friendly); 1 = read row-major in place; 2 = b already k-block-major
+                        [K/64][N][64] */
 } ms_hp_op;
 
 typedef struct ms_hp_times {

@@ -6,6 +6,7 @@
 // descriptors.  No CPU fallback: every entry point fails with MS_E_CUDA / MS_E_NODEV when
 // the device or the sm_100a images are unavailable.
 #include <cudaTypedefs.h>
+#include <emmintrin.h>
 #include <time.h>
 
 #include <atomic>
@@ -65,7 +66,25 @@ int encode_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, 
   return 0;
 }
 
+int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  // bf16 [cols/64][rows][64]; box = 64 x box_rows x 1 = box_rows x 128 B contiguous.
+  if (!g_encode) {
+    CUtensorMap dummy;
+    if (int rc = encode_2d(&dummy, base, 128, 64, 64)) return rc;
+  }
+  cuuint64_t dims[3] = {64, rows, cols / 64};
+  cuuint64_t strides[2] = {128, rows * 128};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MS_E_CUDA, "cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
+  return 0;
+}
+
 constexpr int kRedoCap = 8192;
+constexpr int kGateSmem = 40 * 1024;
 
 struct LpSlot {
   bool used = false;
@@ -86,6 +105,11 @@ struct HpOpRt {
   CUtensorMap tma_a{}, tma_b{};
   int tiles_m = 0, tiles_n = 0;
   int ctl_index = 0;
+  int split = 1;
+  float* ws = nullptr;
+  unsigned int* tile_cnt = nullptr;
+  __nv_bfloat16* b_tiled = nullptr;  // k-block-major copy of the weights (captured at registration)
+  int reduce_ctl_index = 0;          // control block of the split-K reduce kernel
 };
 
 struct HpChain {
@@ -111,6 +135,9 @@ struct ms_dev {
   int next_hp_ctl = MS_MAX_LP;
   int stream_memops = 0;
   uint32_t hp_seq = 0;  // monotonic doorbell sequence of this device
+  unsigned long long* dbg = nullptr;  // per-CTA phase stamps of the next LP run (diagnostics)
+  unsigned long long* dbg_buf = nullptr;
+  int lp_sm_reserve = 1;  // SMs an LP GEMM grid leaves free (the HP gate's home)
 };
 
 namespace {
@@ -133,35 +160,50 @@ TileRun base_run(ms_dev* d, int ctl_index) {
   r.ctl = d->ctl + ctl_index;
   r.redo_in = d->dummy_redo;
   r.redo_out = d->dummy_redo + 16;
-  r.host_epoch = &d->page_d->epoch;
-  r.host_budget = &d->page_d->budget[0];
+  r.host_line = reinterpret_cast<const uint64_t*>(&d->page_d->lp_line[0]);
   r.mirror = d->mirror;
   return r;
 }
 
+// `pdl`: launch with programmatic stream serialisation, so the kernel is scheduled as soon
+// as its predecessor triggers griddepcontrol.launch_dependents (HP chains only).
+template <typename K, typename... Args>
+cudaError_t launch_k(K kernel, int grid, int block, int smem, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                cudaStream_t st) {
+                cudaStream_t st, bool pdl = false) {
   switch (block_n) {
     case 256:
-      tc_gemm_kernel<256><<<grid, 256, GemmCfg<256>::kSmemBytes, st>>>(ta, tb, p);
+      MS_CUDA(launch_k(tc_gemm_kernel<256>, grid, 256, GemmCfg<256>::kSmemBytes, st, pdl, ta, tb, p));
       break;
     case 128:
-      tc_gemm_kernel<128><<<grid, 256, GemmCfg<128>::kSmemBytes, st>>>(ta, tb, p);
+      MS_CUDA(launch_k(tc_gemm_kernel<128>, grid, 256, GemmCfg<128>::kSmemBytes, st, pdl, ta, tb, p));
       break;
     case 64:
-      tc_gemm_kernel<64><<<grid, 256, GemmCfg<64>::kSmemBytes, st>>>(ta, tb, p);
+      MS_CUDA(launch_k(tc_gemm_kernel<64>, grid, 256, GemmCfg<64>::kSmemBytes, st, pdl, ta, tb, p));
       break;
     default:
       return fail(MS_E_ARG, "block_n must be 64, 128 or 256");
   }
-  MS_CUDA(cudaGetLastError());
   (void)d;
   return 0;
 }
 
 bool is_copy(const ms_hp_op& op) { return op.kind == MS_HP_H2D || op.kind == MS_HP_D2H; }
 
-int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq) {
+int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq, bool after_gate) {
   const HpOpRt& o = ch.ops[i];
   if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
     MS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(o.op.c), reinterpret_cast<const void*>(o.op.a),
@@ -180,13 +222,22 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   r.hp_ctl = d->hp_ctl + chain_id;
   r.hp_rec = &d->page_d->hp[chain_id];
   r.hp_first = i == first_k;
+  r.dbg = d->dbg;
   r.hp_last = i == last_k && !is_copy(ch.ops.back().op);
   r.hp_seq = seq;
+  // PDL when the stream predecessor is a kernel (the gate, or the previous chain kernel);
+  // the chain's first kernel does not depend on the gate's output, later ones wait.
+  const bool prev_is_kernel = i > 0 ? !is_copy(ch.ops[i - 1].op) : after_gate;
+  r.pdl_wait = i > 0 && prev_is_kernel;
   if (o.op.kind == MS_HP_GEMM) {
     GemmParams p{};
     p.run = r;
     p.run.begin = 0;
-    p.run.end = p.run.budget0 = static_cast<unsigned long long>(o.tiles_m) * o.tiles_n;
+    p.run.end = p.run.budget0 = static_cast<unsigned long long>(o.tiles_m) * o.tiles_n * o.split;
+    p.split_k = o.split;
+    p.ws = o.ws;
+    p.tile_cnt = nullptr;  // split-K partials are reduced by the next (PDL) kernel
+    p.b_kblock_major = o.b_tiled != nullptr || o.op.b_layout == 2;
     p.m = static_cast<int>(o.op.m);
     p.n = static_cast<int>(o.op.n);
     p.k = static_cast<int>(o.op.k);
@@ -195,7 +246,32 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
     p.group_m = 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
     const int grid = static_cast<int>(std::min<uint64_t>(p.run.end, d->prop.multiProcessorCount));
-    return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, p, grid, d->hp);
+    if (o.split == 1) return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, p, grid, d->hp, prev_is_kernel);
+    // split-K: the GEMM streams partials; the reduce kernel carries the chain's last-op role
+    const bool last = p.run.hp_last;
+    p.run.hp_last = 0;
+    if (int rc = launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, p, grid, d->hp, prev_is_kernel)) return rc;
+    SplitReduceParams rp{};
+    rp.run = base_run(d, o.reduce_ctl_index);
+    rp.run.hp_ctl = r.hp_ctl;
+    rp.run.hp_rec = r.hp_rec;
+    rp.run.hp_first = 0;
+    rp.run.hp_last = last;
+    rp.run.hp_seq = seq;
+    rp.run.pdl_wait = 1;
+    rp.run.dbg = d->dbg;
+    rp.ws = reinterpret_cast<const float4*>(o.ws);
+    rp.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+    rp.n = static_cast<int>(o.op.n);
+    rp.tiles_m = o.tiles_m;
+    rp.tiles_n = o.tiles_n;
+    rp.group_m = 16;
+    rp.bn = o.op.block_n;
+    rp.split = o.split;
+    rp.total = static_cast<long long>(o.tiles_m) * o.tiles_n * (o.op.block_n / 4) * kBM;
+    const int rgrid = static_cast<int>(std::min<long long>((rp.total + 255) / 256, 2ll * d->prop.multiProcessorCount));
+    MS_CUDA(launch_k(splitk_reduce_kernel, rgrid, 256, 0, d->hp, true, rp));
+    return 0;
   }
   BiasGeluParams p{};
   p.run = r;
@@ -207,8 +283,7 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   p.rows = static_cast<int>(o.op.m);
   p.cols = static_cast<int>(o.op.n);
   const int grid = static_cast<int>(std::min<int64_t>(o.op.m, d->prop.multiProcessorCount));
-  bias_gelu_kernel<<<grid, 256, 0, d->hp>>>(p);
-  MS_CUDA(cudaGetLastError());
+  MS_CUDA(launch_k(bias_gelu_kernel, grid, 256, 0, d->hp, prev_is_kernel, p));
   return 0;
 }
 
@@ -418,12 +493,13 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   r.redo_out = s.redo[run_id & 1];
   r.preemptible = (flags & MS_RUN_NONPREEMPTIBLE) ? 0 : 1;
   r.host_progress = reinterpret_cast<unsigned long long*>(&d->page_d->progress[id]);
+  r.dbg = d->dbg;
   r.run_epoch = __atomic_load_n(&d->page->epoch, __ATOMIC_ACQUIRE);
-  r.host_budget = &d->page_d->budget[id];
+  r.host_line = reinterpret_cast<const uint64_t*>(&d->page_d->lp_line[id]);
   r.slot = id;
   r.exit_rec = &d->page_d->lp_exit[id];
   r.run_id = run_id;
-  __atomic_store_n(&d->page->budget[id], ((run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
+  __atomic_store_n(&d->page->lp_line[id].budget, ((run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
   __atomic_store_n(&d->page->progress[id], 0ull, __ATOMIC_RELEASE);
   s.last_begin = begin;
   s.last_end = end;
@@ -441,7 +517,7 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.tiles_n = s.tiles_n;
     p.group_m = s.desc.group_m ? s.desc.group_m : 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount)));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount - d->lp_sm_reserve)));
     return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, p, grid, d->lp);
   }
   StreamParams p{};
@@ -455,13 +531,38 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
   const int vpt = s.desc.tile_elems / (kStreamThreads * 8);
   switch (vpt) {
-    case 1: axpy_kernel<1><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
-    case 2: axpy_kernel<2><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
-    case 4: axpy_kernel<4><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
-    case 8: axpy_kernel<8><<<grid, kStreamThreads + 32, 0, d->lp>>>(p); break;
+    case 1: axpy_kernel<1><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
+    case 2: axpy_kernel<2><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
+    case 4: axpy_kernel<4><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
+    case 8: axpy_kernel<8><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
     default: return fail(MS_E_ARG, "tile_elems must be 2048 * {1,2,4,8}");
   }
   MS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int ms_set_lp_sm_reserve(ms_dev* d, int n) {
+  if (n < 0 || n >= d->prop.multiProcessorCount) return fail(MS_E_ARG, "bad SM reserve");
+  d->lp_sm_reserve = n;
+  return 0;
+}
+
+int ms_debug_stamps(ms_dev* d, int enable, unsigned long long* out, size_t n) {
+  // Stream-local operations only: a device-wide sync (cudaFree / legacy-stream memset)
+  // would deadlock against a resident doorbell gate.
+  constexpr size_t kWords = 4096 * 8;
+  if (!d->dbg_buf) MS_CUDA(cudaMalloc(&d->dbg_buf, kWords * sizeof(unsigned long long)));
+  if (enable) {
+    MS_CUDA(cudaMemsetAsync(d->dbg_buf, 0, kWords * sizeof(unsigned long long), d->aux));
+    MS_CUDA(cudaStreamSynchronize(d->aux));
+    d->dbg = d->dbg_buf;
+    return 0;
+  }
+  if (out) {
+    MS_CUDA(cudaMemcpyAsync(out, d->dbg_buf, std::min(n, kWords) * 8, cudaMemcpyDeviceToHost, d->aux));
+    MS_CUDA(cudaStreamSynchronize(d->aux));
+  }
+  d->dbg = nullptr;
   return 0;
 }
 
@@ -476,7 +577,7 @@ uint64_t ms_lp_progress(ms_dev* d, int id) {
 int ms_lp_set_budget(ms_dev* d, int id, uint64_t budget) {
   LpSlot& s = d->lp_slots[id];
   if (budget > s.last_end) budget = s.last_end;
-  __atomic_store_n(&d->page->budget[id], ((s.run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
+  __atomic_store_n(&d->page->lp_line[id].budget, ((s.run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
   return 0;
 }
 
@@ -524,6 +625,7 @@ int ms_lp_reset(ms_dev* d, int id) {
 
 int ms_preempt_raise(ms_dev* d, uint32_t* epoch, int64_t* t_host) {
   const uint32_t e = __atomic_add_fetch(&d->page->epoch, 1u, __ATOMIC_RELEASE);
+  for (int i = 0; i < MS_MAX_LP; ++i) __atomic_store_n(&d->page->lp_line[i].epoch, static_cast<uint64_t>(e), __ATOMIC_RELEASE);
   if (t_host) *t_host = now_ns();
   if (epoch) *epoch = e;
   return 0;
@@ -547,13 +649,43 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
     o.ctl_index = d->next_hp_ctl++;
     if (o.ctl_index >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
     if (o.op.kind == MS_HP_GEMM) {
-      const int bn = o.op.block_n ? o.op.block_n : 64;
+      const int bn = o.op.block_n ? o.op.block_n : 128;
       o.op.block_n = bn;
       if (o.op.m % kBM || o.op.n % bn || o.op.k % kBK) return fail(MS_E_ARG, "HP GEMM shape");
       o.tiles_m = static_cast<int>(o.op.m / kBM);
       o.tiles_n = static_cast<int>(o.op.n / bn);
+      // Skinny HP GEMMs (M = 128) have too few tiles to pull HBM bandwidth from every SM:
+      // split K so (tiles x slices) covers the SMs; slices must divide the k-blocks.
+      const int tiles = o.tiles_m * o.tiles_n;
+      const int kbs = static_cast<int>(o.op.k / kBK);
+      int split = o.op.split_k;
+      if (split <= 0) {
+        split = 1;
+        while (tiles * split * 2 <= d->prop.multiProcessorCount && kbs % (split * 2) == 0 && kbs / (split * 2) >= 4)
+          split *= 2;
+      }
+      if (kbs % split) return fail(MS_E_ARG, "split_k must divide K / 64");
+      o.split = split;
+      if (split > 1) {
+        MS_CUDA(cudaMalloc(&o.ws, sizeof(float) * static_cast<size_t>(split) * o.op.m * o.op.n));
+        o.reduce_ctl_index = d->next_hp_ctl++;
+        if (o.reduce_ctl_index >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
+      }
       if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
-      if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
+      if (o.op.b_layout == 1) {
+        if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
+      } else {
+        const void* wb = reinterpret_cast<const void*>(o.op.b);
+        if (o.op.b_layout == 0) {  // capture a k-block-major copy of the weights now
+          MS_CUDA(cudaMalloc(&o.b_tiled, static_cast<size_t>(o.op.n) * o.op.k * 2));
+          kblock_major_kernel<<<d->prop.multiProcessorCount * 4, 256, 0, d->aux>>>(
+              reinterpret_cast<const __nv_bfloat16*>(o.op.b), o.b_tiled, o.op.n, o.op.k);
+          MS_CUDA(cudaGetLastError());
+          MS_CUDA(cudaStreamSynchronize(d->aux));
+          wb = o.b_tiled;
+        }
+        if (int rc = encode_kblock_major(&o.tma_b, wb, o.op.n, o.op.k, bn)) return rc;
+      }
     } else if (o.op.kind == MS_HP_BIAS_GELU) {
       if (o.op.n % 8) return fail(MS_E_ARG, "bias_gelu cols must be a multiple of 8");
     } else if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
@@ -572,17 +704,20 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
 int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   const HpChain& ch = d->chains[cid];
   if (!ch.used) return fail(MS_E_ARG, "bad chain");
-  gate_kernel<<<1, 32, 0, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid]);
+  // 40 KB of (unused) shared memory keeps a 193 KB LP GEMM CTA off the gate's SM: an LP
+  // CTA co-resident with the spinning gate observed preemptions ~5 us late.
+  gate_kernel<<<1, 32, kGateSmem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
   for (size_t i = 0; i < ch.ops.size(); ++i)
-    if (int rc = launch_hp_op(d, cid, ch, i, seq)) return rc;
+    if (int rc = launch_hp_op(d, cid, ch, i, seq, true)) return rc;
   return 0;
 }
 
 uint32_t ms_hp_next_seq(ms_dev* d) { return ++d->hp_seq; }
 
 int ms_hp_ring(ms_dev* d, uint32_t seq, int64_t* t_host) {
-  __atomic_store_n(&d->page->doorbell, seq, __ATOMIC_RELEASE);
+  const uint64_t e = __atomic_load_n(&d->page->epoch, __ATOMIC_ACQUIRE);
+  __atomic_store_n(&d->page->doorbell, (e << 32) | seq, __ATOMIC_RELEASE);
   if (t_host) *t_host = now_ns();
   return 0;
 }
@@ -591,20 +726,23 @@ int ms_hp_launch_direct(ms_dev* d, int cid, uint32_t seq) {
   const HpChain& ch = d->chains[cid];
   if (!ch.used) return fail(MS_E_ARG, "bad chain");
   for (size_t i = 0; i < ch.ops.size(); ++i)
-    if (int rc = launch_hp_op(d, cid, ch, i, seq)) return rc;
+    if (int rc = launch_hp_op(d, cid, ch, i, seq, false)) return rc;
   return 0;
 }
 
 int ms_hp_poll(ms_dev* d, int cid, uint32_t seq, ms_hp_times* t) {
   const MsHpRecord& r = d->page->hp[cid];
-  const uint32_t done = __atomic_load_n(&r.seq_done, __ATOMIC_ACQUIRE);
+  // 16-byte atomic read of the completion pair (aligned SSE load; written by one PCIe write).
+  const __m128i v = _mm_load_si128(reinterpret_cast<const __m128i*>(&r.done_first));
+  const uint64_t first = static_cast<uint64_t>(_mm_cvtsi128_si64(v));
+  const uint64_t seq_dur = static_cast<uint64_t>(_mm_cvtsi128_si64(_mm_unpackhi_epi64(v, v)));
   std::memset(t, 0, sizeof(*t));
   t->seq = seq;
-  if (static_cast<int32_t>(done - seq) < 0) return 0;
+  if (static_cast<int32_t>(static_cast<uint32_t>(seq_dur >> 32) - seq) < 0) return 0;
   t->done = 1;
   t->t_gate = __atomic_load_n(&r.seq_gate, __ATOMIC_ACQUIRE) == seq ? r.t_gate : 0;
-  t->t_first_cta = r.t_first_cta;
-  t->t_done = r.t_done;
+  t->t_first_cta = first;
+  t->t_done = first + (seq_dur & 0xFFFFFFFFull);
   return 1;
 }
 

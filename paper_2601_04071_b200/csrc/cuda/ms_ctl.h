@@ -16,7 +16,7 @@
 #include <stdint.h>
 
 #define MS_MAX_LP 16
-#define MS_MAX_HP_CHAINS 8
+#define MS_MAX_HP_CHAINS 32
 #define MS_MIRROR_COPIES 8
 #define MS_MIRROR_STRIDE 32  // uint32 elements = 128 B
 
@@ -32,20 +32,30 @@ struct MsLpExit {                 // device -> host, one per LP slot (64 B)
 };
 
 struct MsHpRecord {               // device -> host, one per HP chain slot (64 B)
-  uint32_t seq_done;              // written last (release)
-  uint32_t seq_gate;              // gate released for this seq
+  // Completion: ONE 16-byte store {t_first_cta, (seq << 32) | (t_done - t_first_cta)} —
+  // a single PCIe write, so no system-scope fence (MEMBAR.SYS costs ~8 us) is needed.
+  uint64_t done_first;            // t_first_cta of the completed seq
+  uint64_t done_seq_dur;          // (seq << 32) | duration
   uint64_t t_gate;                // gate kernel observed the doorbell
-  uint64_t t_first_cta;           // first CTA of the first chain kernel started
-  uint64_t t_done;                // last CTA of the last chain kernel finished
+  uint32_t seq_gate;              // gate released for this seq
+  uint32_t pad0;
   uint64_t pad[4];
 };
 
+// One 64 B line per LP slot: the LP run's elected poller fetches {epoch, budget} with a
+// single 16-byte ld.acquire.sys (one PCIe round trip per poll iteration).
+struct MsLpLine {
+  uint64_t epoch;                 // copy of the preempt epoch (host writes every line on raise)
+  uint64_t budget;                // (run tag << 40) | soft end tile id
+  uint64_t pad[6];
+};
+
 struct MsHostPage {
-  uint32_t epoch;                 // preempt epoch (monotonic)
+  uint32_t epoch;                 // preempt epoch (monotonic, canonical host copy)
   uint32_t pad0[31];
-  uint32_t doorbell;              // HP doorbell sequence
-  uint32_t pad1[31];
-  uint64_t budget[MS_MAX_LP];     // soft end (tile id) per LP slot
+  uint64_t doorbell;              // HP doorbell: (epoch << 32) | seq, one release store
+  uint64_t pad1[15];
+  MsLpLine lp_line[MS_MAX_LP];
   uint64_t progress[MS_MAX_LP];   // device -> host: claim counter of the running LP run
   MsLpExit lp_exit[MS_MAX_LP];
   MsHpRecord hp[MS_MAX_HP_CHAINS];

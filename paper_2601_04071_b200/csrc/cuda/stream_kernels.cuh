@@ -27,7 +27,7 @@ struct StreamParams {
   int tile_elems;  // multiple of 256 * 8
 };
 
-constexpr int kStreamThreads = 256;  // streaming warps 0-7; warp 8 = poller
+constexpr int kStreamThreads = 256;  // streaming warps 0-7; warp 8 = mirror poller; warp 9 = host poller (CTA 0)
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 v;
@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t axpy2(float a, uint32_t xv, uint32_t yv) {
 }
 
 template <int VPT>  // 16-byte vectors per thread per tile
-__global__ void __launch_bounds__(kStreamThreads + 32) axpy_kernel(const __grid_constant__ StreamParams p) {
+__global__ void __launch_bounds__(kStreamThreads + 64) axpy_kernel(const __grid_constant__ StreamParams p) {
   __shared__ uint32_t preempt, producer_done, tiles_done;
   __shared__ long long tile_sh[2];
   const int warp = threadIdx.x / 32;
@@ -70,7 +70,9 @@ __global__ void __launch_bounds__(kStreamThreads + 32) axpy_kernel(const __grid_
   }
   __syncthreads();
   if (warp == kStreamThreads / 32) {
-    if ((threadIdx.x & 31) == 0 && p.run.preemptible) run_poller(p.run, &preempt, &producer_done);
+    if ((threadIdx.x & 31) == 0 && p.run.preemptible) poll_mirror(p.run, &preempt, &producer_done);
+  } else if (warp == kStreamThreads / 32 + 1) {
+    if ((threadIdx.x & 31) == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &preempt, &producer_done);
   } else {
     const int tid = threadIdx.x;
     for (int j = 0;; ++j) {
@@ -129,6 +131,10 @@ __global__ void __launch_bounds__(256) bias_gelu_kernel(const __grid_constant__ 
     tiles_done = 0;
     cta_started(p.run);
   }
+  if (p.run.hp_ctl) {  // PDL-launched chain kernel
+    pdl_launch_dependents();
+    if (p.run.pdl_wait) pdl_wait();
+  }
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   for (;;) {
     __syncthreads();
@@ -161,9 +167,23 @@ __global__ void __launch_bounds__(256) bias_gelu_kernel(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- HP doorbell gate
-__global__ void gate_kernel(const uint32_t* doorbell, unsigned int seq, MsHpRecord* rec) {
+// The doorbell word carries (epoch << 32 | seq).  On release the gate (already resident,
+// no launch needed) first pushes the preempt epoch into the device mirror — every LP CTA
+// sees it on its next L2 poll, without waiting for the LP leader's own PCIe round trip —
+// then lets the PDL-launched chain kernel be scheduled.
+__global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpRecord* rec, MsDevMirror* mirror) {
   if (threadIdx.x != 0) return;
-  while (static_cast<int>(ld_acquire_sys(doorbell) - seq) < 0) __nanosleep(20);
+  // Relaxed polling: the doorbell value itself is the only datum consumed.
+  uint64_t v;
+  for (;;) {
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(doorbell) : "memory");
+    if (static_cast<int>(static_cast<uint32_t>(v) - seq) >= 0) break;
+    __nanosleep(64);
+  }
+  const uint32_t epoch = static_cast<uint32_t>(v >> 32);
+#pragma unroll
+  for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&mirror->epoch[c * MS_MIRROR_STRIDE], epoch);
+  pdl_launch_dependents();
   const unsigned long long t = globaltimer();
   st_relaxed_sys_u64(&rec->t_gate, t);
   st_release_sys_u32(&rec->seq_gate, seq);
@@ -172,10 +192,8 @@ __global__ void gate_kernel(const uint32_t* doorbell, unsigned int seq, MsHpReco
 // Completion record of a chain whose last op is a copy (e2e mode): written after the D2H.
 __global__ void hp_notify_kernel(MsHpCtl* ctl, MsHpRecord* rec, unsigned int seq) {
   const unsigned long long t = globaltimer();
-  st_relaxed_sys_u64(&rec->t_first_cta, ctl->t_first_cta);
-  st_relaxed_sys_u64(&rec->t_done, t);
-  fence_sys();
-  st_release_sys_u32(&rec->seq_done, seq);
+  const unsigned long long first = ctl->t_first_cta;
+  st_relaxed_sys_v2(&rec->done_first, first, (static_cast<uint64_t>(seq) << 32) | ((t - first) & 0xFFFFFFFFull));
   ctl->t_first_cta = ~0ull;
 }
 
@@ -209,6 +227,20 @@ __global__ void synth_fill_kernel(__nv_bfloat16* out, unsigned long long n, unsi
     const float u = static_cast<float>(x >> 40) * 5.9604644775390625e-08f;
     const float v = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), scale);
     out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// [N, K] row-major -> [K/64][N][64] (k-block-major), 16 B per thread-iteration.
+__global__ void kblock_major_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, unsigned long long n,
+                                    unsigned long long k) {
+  const unsigned long long vecs = n * k / 8;
+  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < vecs;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long row = i / (k / 8);
+    const unsigned long long k8 = i - row * (k / 8);
+    const unsigned long long kb = k8 / 8;
+    const unsigned long long kin = (k8 & 7) * 8;
+    *reinterpret_cast<uint4*>(dst + (kb * n + row) * 64 + kin) = *reinterpret_cast<const uint4*>(src + row * k + k8 * 8);
   }
 }
 

@@ -34,6 +34,15 @@ struct GemmParams {
   int m, n, k;
   int tiles_m, tiles_n, group_m;
   __nv_bfloat16* c;
+  // split-K (skinny HP GEMMs): a work unit is (tile, k-slice); unit u -> tile u / split_k,
+  // slice u % split_k.  Partials go to ws in fp32; the last unit of a tile to finish
+  // reduces the slices in slice order (deterministic) and writes C.
+  int split_k;
+  float* ws;
+  unsigned int* tile_cnt;
+  // B stored k-block-major ([K/64][N][64], a 3-D tensor map): every B box is one
+  // contiguous BN x 128 B chunk of HBM (DRAM-page friendly streaming of HP weights).
+  int b_kblock_major;
 };
 
 template <int BN>
@@ -60,6 +69,7 @@ struct GemmSmemCtl {
   uint32_t preempt;
   uint32_t producer_done;
   uint32_t tiles_done;
+  uint32_t fix_last;
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -86,6 +96,7 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) dbg_stamp(p.run, 7);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -113,8 +124,16 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // HP chains are PDL-launched: let the next chain kernel get scheduled now, and wait for
+  // the previous one's results before touching them (no-ops for ordinary launches).
+  if (p.run.hp_ctl) {
+    pdl_launch_dependents();
+    if (p.run.pdl_wait) pdl_wait();
+  }
+  if (threadIdx.x == 0) dbg_stamp(p.run, 0);  // prologue done (HP) / overwritten by "seen" (LP)
   const uint32_t tmem_base = s->tmem_base;
-  const int num_kb = p.k / kBK;
+  const int split = p.split_k > 1 ? p.split_k : 1;
+  const int num_kb = p.k / kBK / split;  // k-blocks per work unit
 
   if (warp == 0) {
     // ===================== tile scheduler + TMA producer =====================
@@ -130,19 +149,22 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(&s->tile_full[slot]);
         if (tile < 0) break;
         int mb, nb;
-        tile_coords(tile, p, mb, nb);
+        tile_coords(tile / split, p, mb, nb);
+        const int kb0 = static_cast<int>(tile % split) * num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
           const bool abort = p.run.preemptible && kb > 0 && ld_volatile_smem(&s->preempt);
           mbar_wait(&s->empty[stage], phase ^ 1);
           if (abort) {
-            s->stage_flag[stage] = 2;
+            s->stage_flag[stage] = 2;  // the MMA warp owns the redo push for this tile
             mbar_arrive(&s->full[stage]);
-            push_redo(p.run, static_cast<unsigned long long>(tile));
           } else {
             s->stage_flag[stage] = (kb == num_kb - 1) ? 1u : 0u;
             mbar_arrive_expect_tx(&s->full[stage], Cfg::kStageBytes);
-            tma_load_2d(smem_a + stage * Cfg::kABytes, &tma_a, &s->full[stage], kb * kBK, mb * kBM);
-            tma_load_2d(smem_b + stage * Cfg::kBBytes, &tma_b, &s->full[stage], kb * kBK, nb * BN);
+            tma_load_2d(smem_a + stage * Cfg::kABytes, &tma_a, &s->full[stage], (kb0 + kb) * kBK, mb * kBM);
+            if (p.b_kblock_major)
+              tma_load_3d(smem_b + stage * Cfg::kBBytes, &tma_b, &s->full[stage], 0, nb * BN, kb0 + kb);
+            else
+              tma_load_2d(smem_b + stage * Cfg::kBBytes, &tma_b, &s->full[stage], (kb0 + kb) * kBK, nb * BN);
           }
           if (++stage == S) {
             stage = 0;
@@ -152,11 +174,12 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       st_volatile_smem(&s->producer_done, 1u);
+      dbg_stamp(p.run, 1);
     }
   } else if (warp == 1) {
     // ===================== UMMA issuer =====================
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
+      uint32_t stage = 0, phase = 0, drain_phase = 0;
       for (int j = 0;; ++j) {
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
@@ -169,9 +192,11 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&s->full[stage], phase);
           tc_fence_after();
           const uint32_t flag = s->stage_flag[stage];
-          if (flag == 2) {
+          // Once preempted, stop feeding the tensor core: the tile is abandoned anyway.
+          if (!aborted && p.run.preemptible && ld_volatile_smem(&s->preempt)) aborted = true;
+          if (flag == 2) aborted = true;
+          if (aborted) {
             mbar_arrive(&s->empty[stage]);
-            aborted = true;
           } else {
             const uint64_t a0 = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
             const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + stage * Cfg::kBBytes));
@@ -189,19 +214,24 @@ __global__ void __launch_bounds__(256, 1)
           if (flag != 0) break;
         }
         if (aborted) {
-          // Drain the abandoned tile's MMAs (TMEM must be quiescent before dealloc), then
-          // tell the epilogue to skip it with a plain (release) arrive.  At most once per CTA.
+          // Drain this tile's issued MMAs (TMEM must be quiescent before dealloc), park the
+          // tile on the redo list, and tell the epilogue to skip it with a plain arrive.
           umma_commit(&s->mma_drain);
-          mbar_wait(&s->mma_drain, 0);
+          mbar_wait(&s->mma_drain, drain_phase);
+          drain_phase ^= 1;
+          push_redo(p.run, static_cast<unsigned long long>(s->tile_id[slot]));
           s->tile_abort[slot] = 1;
           mbar_arrive(&s->tmem_full[slot]);
         } else {
           umma_commit(&s->tmem_full[slot]);
         }
       }
+      dbg_stamp(p.run, 2);
     }
   } else if (warp == 2) {
-    if (lane == 0 && p.run.preemptible) run_poller(p.run, &s->preempt, &s->producer_done);
+    if (lane == 0 && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->producer_done);
+  } else if (warp == 3) {
+    if (lane == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &s->preempt, &s->producer_done);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp - 4;  // TMEM lane quarter
@@ -212,25 +242,42 @@ __global__ void __launch_bounds__(256, 1)
       if (tile < 0) break;
       mbar_wait(&s->tmem_full[slot], (j >> 1) & 1);
       tc_fence_after();
-      if (!s->tile_abort[slot]) {
-        int mb, nb;
-        tile_coords(tile, p, mb, nb);
-        const int row = mb * kBM + q * 32 + lane;
+      const bool keep = !s->tile_abort[slot];
+      const long long unit_tile = tile / split;
+      const int unit_slice = static_cast<int>(tile % split);
+      int mb = 0, nb = 0;
+      if (keep) {
+        tile_coords(unit_tile, p, mb, nb);
+        const int row_in_tile = q * 32 + lane;
+        const int row = mb * kBM + row_in_tile;
         __nv_bfloat16* crow = p.c + static_cast<size_t>(row) * p.n + static_cast<size_t>(nb) * BN;
+        // split-K partial layout (per unit, 128 x BN fp32): [BN / 4][128 rows] of float4, so for a
+        // fixed column quad the 32 lanes of a warp touch 512 contiguous bytes (coalesced).
+        float4* wunit = split > 1 ? reinterpret_cast<float4*>(p.ws) +
+                                        (static_cast<size_t>(unit_tile) * split + unit_slice) * (kBM * BN / 4)
+                                  : nullptr;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * BN + c0), r);
           tmem_ld_wait();
-          uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+          if (split > 1) {
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
-            w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
-            w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
-            w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-            dst[v] = w;
+            for (int v = 0; v < 8; ++v)
+              wunit[static_cast<size_t>(c0 / 4 + v) * kBM + row_in_tile] =
+                  make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                              __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 w;
+              w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
+              w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
+              w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
+              w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+              dst[v] = w;
+            }
           }
         }
         if (q == 0 && lane == 0) ++s->tiles_done;
@@ -240,16 +287,97 @@ __global__ void __launch_bounds__(256, 1)
       if (q == 0 && lane == 0) {
         mbar_arrive(&s->tmem_empty[slot]);
         mbar_arrive(&s->tile_empty[slot]);
+        if (keep && split > 1 && p.tile_cnt) {
+          __threadfence();
+          s->fix_last = atomicAdd(&p.tile_cnt[unit_tile], 1u) + 1 == static_cast<unsigned>(split) ? 1u : 0u;
+        }
+      }
+      if (keep && split > 1 && p.tile_cnt) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s->fix_last) {
+          // Last slice of this tile: reduce all slices in slice order, write bf16 C.
+          __threadfence();
+          const int row_in_tile = q * 32 + lane;
+          const float4* base = reinterpret_cast<const float4*>(p.ws) +
+                               static_cast<size_t>(unit_tile) * split * (kBM * BN / 4);
+          __nv_bfloat16* crow = p.c + static_cast<size_t>(mb * kBM + row_in_tile) * p.n + static_cast<size_t>(nb) * BN;
+#pragma unroll 1
+          for (int cq = 0; cq < BN / 4; cq += 2) {
+            float4 x = base[static_cast<size_t>(cq) * kBM + row_in_tile];
+            float4 y = base[static_cast<size_t>(cq + 1) * kBM + row_in_tile];
+            for (int sl = 1; sl < split; ++sl) {  // slice order: deterministic sum
+              const float4* sb = base + static_cast<size_t>(sl) * (kBM * BN / 4);
+              const float4 u = sb[static_cast<size_t>(cq) * kBM + row_in_tile];
+              const float4 w = sb[static_cast<size_t>(cq + 1) * kBM + row_in_tile];
+              x.x += u.x; x.y += u.y; x.z += u.z; x.w += u.w;
+              y.x += w.x; y.y += w.y; y.z += w.z; y.w += w.w;
+            }
+            uint4 o;
+            o.x = pack_bf16x2(x.x, x.y);
+            o.y = pack_bf16x2(x.z, x.w);
+            o.z = pack_bf16x2(y.x, y.y);
+            o.w = pack_bf16x2(y.z, y.w);
+            *reinterpret_cast<uint4*>(crow + cq * 4) = o;
+          }
+          if (q == 0 && lane == 0) p.tile_cnt[unit_tile] = 0;
+        }
       }
     }
+    if (q == 0 && lane == 0) dbg_stamp(p.run, 3);
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if (threadIdx.x == 0) dbg_stamp(p.run, 4);
 
   if (threadIdx.x == 0) cta_exit(p.run, s->tiles_done);
+}
+
+// Split-K reduction (runs as the next PDL-chained kernel): C tile = sum over slices (in
+// slice order: deterministic) of the fp32 partials, written as bf16.  One thread per
+// (tile, column quad, row): coalesced float4 reads, all SMs.
+struct SplitReduceParams {
+  TileRun run;  // HP bookkeeping only (non-preemptible)
+  const float4* ws;
+  __nv_bfloat16* c;
+  int n, tiles_m, tiles_n, group_m, bn, split;
+  long long total;  // tiles * (bn / 4) * 128
+};
+
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ SplitReduceParams p) {
+  if (threadIdx.x == 0) cta_started(p.run);
+  if (p.run.hp_ctl) {
+    pdl_launch_dependents();
+    if (p.run.pdl_wait) pdl_wait();
+  }
+  const int quads = p.bn / 4;
+  GemmParams gp{};
+  gp.tiles_m = p.tiles_m;
+  gp.tiles_n = p.tiles_n;
+  gp.group_m = p.group_m;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int row = static_cast<int>(i % kBM);
+    const long long tq = i / kBM;
+    const int cq = static_cast<int>(tq % quads);
+    const long long tile = tq / quads;
+    const float4* base = p.ws + static_cast<size_t>(tile) * p.split * (kBM * quads) + static_cast<size_t>(cq) * kBM + row;
+    float4 x = base[0];
+    for (int sl = 1; sl < p.split; ++sl) {
+      const float4 u = base[static_cast<size_t>(sl) * (kBM * quads)];
+      x.x += u.x; x.y += u.y; x.z += u.z; x.w += u.w;
+    }
+    int mb, nb;
+    tile_coords(tile, gp, mb, nb);
+    uint2 o;
+    o.x = pack_bf16x2(x.x, x.y);
+    o.y = pack_bf16x2(x.z, x.w);
+    *reinterpret_cast<uint2*>(p.c + static_cast<size_t>(mb * kBM + row) * p.n + static_cast<size_t>(nb) * p.bn + cq * 4) = o;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cta_exit(p.run, 0);
 }
 
 }  // namespace msdev

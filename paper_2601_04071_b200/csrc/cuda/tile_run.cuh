@@ -28,8 +28,7 @@ struct TileRun {
   MsLpCtl* ctl;
   int preemptible;
   unsigned int run_epoch;
-  const uint32_t* host_epoch;
-  const uint64_t* host_budget;
+  const uint64_t* host_line;  // MsLpLine of this slot: {epoch, budget}
   MsDevMirror* mirror;
   int slot;
   MsLpExit* exit_rec;
@@ -40,7 +39,13 @@ struct TileRun {
   MsHpRecord* hp_rec;
   int hp_first, hp_last;
   unsigned int hp_seq;
+  int pdl_wait;  // HP chain kernel whose inputs come from the previous chain kernel
+  unsigned long long* dbg;  // optional per-CTA phase timestamps [gridDim][8] (diagnostics)
 };
+
+__device__ __forceinline__ void dbg_stamp(const TileRun& r, int phase) {
+  if (r.dbg) r.dbg[blockIdx.x * 8 + phase] = globaltimer();
+}
 
 __device__ __forceinline__ unsigned long long current_budget(const TileRun& r) {
   if (!r.preemptible) return r.end;
@@ -72,54 +77,64 @@ __device__ __forceinline__ void cta_started(const TileRun& r) {
   if (r.hp_ctl && r.hp_first) atomicMin(&r.hp_ctl->t_first_cta, now);
 }
 
-// Runs on one thread per CTA.  `preempt` / `producer_done` are the CTA's smem words.
-__device__ __forceinline__ void run_poller(const TileRun& r, uint32_t* preempt, const uint32_t* producer_done) {
-  const bool leader = blockIdx.x == 0;
+// Mirror poller: one thread per CTA, L2 reads of the device mirror only (never PCIe).
+__device__ __forceinline__ void poll_mirror(const TileRun& r, uint32_t* preempt, const uint32_t* producer_done) {
   const uint32_t* mine = &r.mirror->epoch[(blockIdx.x % MS_MIRROR_COPIES) * MS_MIRROR_STRIDE];
-  uint32_t mirrored = 0;
   for (;;) {
-    if (ld_volatile_smem(producer_done)) {
-      if (!leader) break;
-      if (*reinterpret_cast<volatile unsigned int*>(&r.ctl->exited) + 1 >= gridDim.x) break;
-    }
-    uint32_t e;
-    if (leader) {
-      if (r.host_progress)
-        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(r.host_progress), ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&r.ctl->claim)));
-      e = ld_acquire_sys(r.host_epoch);
-      st_relaxed_gpu_u64(&r.mirror->budget[r.slot][0], ld_acquire_sys_u64(r.host_budget));
-      if (e > mirrored) {
-#pragma unroll
-        for (int c = 0; c < MS_MIRROR_COPIES; ++c) st_relaxed_gpu(&r.mirror->epoch[c * MS_MIRROR_STRIDE], e);
-        mirrored = e;
-      }
-    } else {
-      e = ld_relaxed_gpu(mine);
-    }
-    if (e > r.run_epoch) {
+    if (ld_volatile_smem(producer_done)) break;
+    if (ld_relaxed_gpu(mine) > r.run_epoch) {
       st_volatile_smem(preempt, 1u);
+      dbg_stamp(r, 0);
       atomicMin(&r.ctl->t_seen, static_cast<unsigned long long>(globaltimer()));
       r.ctl->preempted = 1u;
       break;
     }
-    __nanosleep(leader ? 32 : 128);
+    __nanosleep(64);
+  }
+}
+
+// Host poller: one thread of CTA 0 (an otherwise idle warp).  Fetches {epoch, budget}
+// from the host-mapped line with one 16-byte ld.acquire.sys per iteration, forwards them
+// to the device mirror, and publishes the claim counter to the host.  Stays alive until
+// every other CTA has exited so scheduler-initiated preemptions keep propagating.
+__device__ __forceinline__ void poll_host(const TileRun& r, const uint32_t* preempt, const uint32_t* producer_done) {
+  uint32_t mirrored = 0;
+  for (;;) {
+    if (ld_volatile_smem(preempt)) break;  // CTA 0 is leaving anyway
+    if (ld_volatile_smem(producer_done) &&
+        *reinterpret_cast<volatile unsigned int*>(&r.ctl->exited) + 1 >= gridDim.x)
+      break;
+    if (r.host_progress)
+      st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(r.host_progress),
+                         ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&r.ctl->claim)));
+    uint64_t ep, bud;
+    ld_acquire_sys_v2(r.host_line, ep, bud);
+    st_relaxed_gpu_u64(&r.mirror->budget[r.slot][0], bud);
+    const uint32_t e = static_cast<uint32_t>(ep);
+    if (e > mirrored) {
+#pragma unroll
+      for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&r.mirror->epoch[c * MS_MIRROR_STRIDE], e);
+      mirrored = e;
+    }
   }
 }
 
 // Called by thread 0 of each CTA after all of the CTA's work (and TMEM traffic) is done.
 __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_done_cta) {
   MsLpCtl* ctl = r.ctl;
+  dbg_stamp(r, 5);
   atomicAdd(&ctl->tiles_done, static_cast<unsigned long long>(tiles_done_cta));
-  __threadfence();
-  const unsigned int prev = atomicAdd(&ctl->exited, 1u);
+  // acq_rel: publishes this CTA's tile / redo accounting (ordered by the CTA barrier before
+  // cta_exit) and, for the last CTA, acquires everyone else's.
+  const unsigned int prev = atom_add_acqrel_gpu(&ctl->exited, 1u);
   if (prev + 1 != gridDim.x) return;
-  __threadfence();
   const unsigned long long claimed = *reinterpret_cast<volatile unsigned long long*>(&ctl->claim);
   // Redo entries nobody claimed carry over to the next run.
   for (unsigned long long idx = claimed; idx < r.nr_in; ++idx) r.redo_out[ctl->redo_out_n++] = r.redo_in[idx];
   unsigned long long cursor = r.begin;
   if (claimed > r.nr_in) cursor = min(r.end, r.begin + (claimed - r.nr_in));
   const unsigned long long t_exit = globaltimer();
+  dbg_stamp(r, 6);
   if (r.exit_rec) {
     MsLpExit* e = r.exit_rec;
     st_relaxed_sys_u64(&e->cursor, cursor);
@@ -129,14 +144,12 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
     st_relaxed_sys_u64(&e->t_seen, ctl->t_seen == ~0ull ? 0ull : ctl->t_seen);
     st_relaxed_sys_u64(&e->t_exit, t_exit);
     st_relaxed_sys_u64(&e->preempted, ctl->preempted);
-    fence_sys();
-    st_relaxed_sys_u64(&e->run_id, r.run_id);
+    st_release_sys_u64(&e->run_id, r.run_id);  // host acquires run_id, then reads the rest
   }
   if (r.hp_ctl && r.hp_last && r.hp_rec) {
-    st_relaxed_sys_u64(&r.hp_rec->t_first_cta, r.hp_ctl->t_first_cta);
-    st_relaxed_sys_u64(&r.hp_rec->t_done, t_exit);
-    fence_sys();
-    st_release_sys_u32(&r.hp_rec->seq_done, r.hp_seq);
+    const unsigned long long first = r.hp_ctl->t_first_cta;
+    st_relaxed_sys_v2(&r.hp_rec->done_first, first,
+                      (static_cast<uint64_t>(r.hp_seq) << 32) | ((t_exit - first) & 0xFFFFFFFFull));
     r.hp_ctl->t_first_cta = ~0ull;
   }
   ctl->claim = 0;

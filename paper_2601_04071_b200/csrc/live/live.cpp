@@ -95,6 +95,7 @@ class LiveRun {
     want_lp_ = policy_ != "exclusive";
     eager_ = opts.value("eager", false);
     direct_hp_ = opts.value("direct_hp", false);  // profiler-safe: no gate kernels
+    debug_runs_ = opts.value("debug_stamps", 0);   // diagnostics: per-CTA exit phases
     calibrate_ = opts.value("calibrate", true);
     record_ = opts.value("timeline", true);
     ms_dev_info info{};
@@ -405,6 +406,7 @@ class LiveRun {
     const bool np = reef_ || policy_ == "exclusive_lp";
     uint64_t budget = lt->total;
     if (harvest_) budget = std::min<uint64_t>(lt->total, lt->cursor + batch_tiles(*lt, harvest_gap_));
+    if (debug_runs_ > 0) ms_debug_stamps(dev_, 1, nullptr, 0);
     check(ms_lp_run_ex(dev_, lt->dev_id, lt->cursor, lt->total, budget, np ? MS_RUN_NONPREEMPTIBLE : 0), "ms_lp_run");
     lp_budget_ = budget;
     lp_running_ = true;
@@ -447,6 +449,15 @@ class LiveRun {
     l.redo = st.redo_count;
     lp_tiles_done_ += st.tiles_done;
     if (st.preempted) lp_preemptions_++;
+    if (debug_runs_ > 0) {
+      std::vector<uint64_t> buf(148 * 8 + 1, 0);
+      ms_debug_stamps(dev_, 0, reinterpret_cast<unsigned long long*>(buf.data()), 148 * 8);
+      if (st.preempted && preempt_raised_) {
+        buf[148 * 8] = static_cast<uint64_t>(t_raise_);
+        debug_.push_back(std::move(buf));
+        --debug_runs_;
+      }
+    }
     lp_samples_.push_back(LpSample{st.preempted && preempt_raised_ ? t_raise_ : -1, st.t_seen, st.t_exit,
                                    static_cast<int>(hp_.size()) + lp_cur_, l.kernel,
                                    "tiles=" + std::to_string(st.tiles_done) + ";cursor=" + std::to_string(st.cursor) +
@@ -486,6 +497,8 @@ class LiveRun {
   json tile_ns_ = json::object();
   bool harvest_ = false, reef_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
   bool direct_hp_ = false, calibrate_ = true;
+  int debug_runs_ = 0;
+  std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
   int n_sm_ = 148;
   int64_t t0_ = 0, off0_ = 0, off1_ = 0, c0_ = 0, c1_ = 0;
   uint32_t last_seq_ = 0;
@@ -687,6 +700,50 @@ json LiveRun::run() {
   for (const Ns x : ring_to_first_) c.push_back(json(static_cast<long long>(x)));
   raw["ring_to_first_hp_cta_all"] = std::move(c);
   out["samples"] = std::move(raw);
+  if (!debug_.empty()) {
+    // phase p of CTA c relative to the raise, converted with the drift-corrected clock
+    json dbg = json::array();
+    for (const auto& buf : debug_) {
+      const Ns raise = static_cast<Ns>(buf[148 * 8]);
+      json run = json::array();
+      for (int ph = 0; ph < 7; ++ph) {
+        std::vector<Ns> v;
+        for (int c = 0; c < 148; ++c)
+          if (buf[c * 8 + ph]) v.push_back(dev_to_host(buf[c * 8 + ph]) - raise);
+        json e = json::array();
+        if (!v.empty()) {
+          std::sort(v.begin(), v.end());
+          e.push_back(json(static_cast<long long>(v.front())));
+          e.push_back(json(static_cast<long long>(v[v.size() / 2])));
+          e.push_back(json(static_cast<long long>(v.back())));
+        }
+        run.push_back(std::move(e));
+      }
+      // the latest observers: [cta, seen, exit_begin]
+      std::vector<std::pair<Ns, int>> seen;
+      for (int c = 0; c < 148; ++c)
+        if (buf[c * 8]) seen.push_back({dev_to_host(buf[c * 8]) - raise, c});
+      std::sort(seen.begin(), seen.end());
+      json late = json::array();
+      for (std::size_t i = seen.size() > 4 ? seen.size() - 4 : 0; i < seen.size(); ++i) {
+        json t = json::array();
+        t.push_back(json(seen[i].second));
+        t.push_back(json(static_cast<long long>(seen[i].first)));
+        t.push_back(json(static_cast<long long>(buf[seen[i].second * 8 + 5] ? dev_to_host(buf[seen[i].second * 8 + 5]) - raise : -1)));
+        late.push_back(std::move(t));
+      }
+      run.push_back(std::move(late));
+      json cnt = json::array();
+      for (int ph = 0; ph < 7; ++ph) {
+        int k = 0;
+        for (int c = 0; c < 148; ++c) k += buf[c * 8 + ph] ? 1 : 0;
+        cnt.push_back(json(k));
+      }
+      run.push_back(std::move(cnt));
+      dbg.push_back(std::move(run));
+    }
+    out["debug_phases"] = std::move(dbg);  // [run][phase] = [min, p50, max] ns
+  }
   out["hp_chains"] = json(static_cast<unsigned long long>(hp_samples_.size()));
   json lp = json::object();
   lp["tiles_done"] = json(static_cast<unsigned long long>(lp_tiles_done_));

@@ -48,7 +48,7 @@ class LpStatus(C.Structure):
 class HpOp(C.Structure):
     _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("a", C.c_uint64), ("b", C.c_uint64),
                 ("c", C.c_uint64), ("bias", C.c_uint64), ("m", C.c_int64), ("n", C.c_int64),
-                ("k", C.c_int64)]
+                ("k", C.c_int64), ("split_k", C.c_int32), ("b_layout", C.c_int32)]
 
 
 class HpTimes(C.Structure):
@@ -86,6 +86,8 @@ def lib() -> C.CDLL:
             "ms_hp_arm": (I, [P, I, U32]), "ms_hp_ring": (I, [P, U32, C.POINTER(I64)]),
             "ms_hp_next_seq": (U32, [P]), "ms_lp_total_tiles": (U64, [P, I]), "ms_lp_progress": (U64, [P, I]),
             "ms_lp_run_ex": (I, [P, I, U64, U64, U64, I]), "ms_lp_unregister": (I, [P, I]),
+            "ms_debug_stamps": (I, [P, I, C.POINTER(C.c_ulonglong), C.c_size_t]),
+            "ms_set_lp_sm_reserve": (I, [P, I]),
             "ms_hp_launch_direct": (I, [P, I, U32]),
             "ms_hp_poll": (I, [P, I, U32, C.POINTER(HpTimes)]),
             "ms_hp_wait": (I, [P, I, U32, I64, C.POINTER(HpTimes)]),
@@ -212,6 +214,17 @@ class Device:
         ms = C.c_float()
         _ck(lib().ms_lp_time_full(self._h, k.id, reps, C.byref(ms)))
         return ms.value
+
+    def set_lp_sm_reserve(self, n: int):
+        _ck(lib().ms_set_lp_sm_reserve(self._h, n))
+
+    def debug_stamps(self, enable: bool, n_cta: int = 148):
+        if enable:
+            _ck(lib().ms_debug_stamps(self._h, 1, None, 0))
+            return None
+        buf = (C.c_ulonglong * (n_cta * 8))()
+        _ck(lib().ms_debug_stamps(self._h, 0, buf, n_cta * 8))
+        return [list(buf[i * 8:(i + 1) * 8]) for i in range(n_cta)]
 
     # ---- preemption
     def preempt_raise(self) -> tuple[int, int]:

@@ -64,7 +64,7 @@ class Config1:
         for i, w in enumerate(self.w):
             dev.fill_synth(w, H * H, seed, 101 + i, 1.0 / math.sqrt(H))
         dev.fill_synth(self.bias, H, seed, 110, 0.1)
-        ops = [dict(kind=1, block_n=64, a=self.act[i], b=self.w[i], c=self.act[i + 1], bias=0, m=M, n=H, k=H)
+        ops = [dict(kind=1, block_n=128, a=self.act[i], b=self.w[i], c=self.act[i + 1], bias=0, m=M, n=H, k=H)
                for i in range(4)]
         ops.append(dict(kind=2, block_n=0, a=self.act[4], b=0, c=self.act[0], bias=self.bias, m=M, n=H, k=0))
         self.chain = dev.hp_register_chain(ops)

@@ -123,3 +123,21 @@ def test_hp_chain_matches_oracle(dev, T):
     want = T.bf16_to_f32(T.bias_gelu(d2h(dev, act[4], M * H), T.synth_bf16(H, SEED, 110, 0.1), M, H))
     got = T.bf16_to_f32(d2h(dev, out, M * H))
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+
+
+@pytest.mark.parametrize("split", [1, 2, 4, 8])
+def test_hp_gemm_split_k_matches_oracle(dev, T, split):
+    """Skinny HP GEMM (M=128) with k-slices reduced in slice order by the last unit."""
+    M, N, K = 128, 2048, 4096
+    a, w, c = dev.alloc(M * K * 2), dev.alloc(N * K * 2), dev.alloc(M * N * 2)
+    s = float(np.float32(1 / math.sqrt(K)))
+    dev.fill_synth(a, M * K, SEED, 31, 1.0)
+    dev.fill_synth(w, N * K, SEED, 32, s)
+    chain = dev.hp_register_chain([dict(kind=1, block_n=128, a=a, b=w, c=c, bias=0, m=M, n=N, k=K, split_k=split)])
+    for _ in range(2):  # second launch reuses the self-resetting tile counters
+        dev.memset(c, 0, M * N * 2)
+        dev.hp_launch_direct(chain, dev.hp_next_seq())
+        dev.sync()
+    want = T.gemm_rows(T.synth_bf16(M * K, SEED, 31, 1.0), T.synth_bf16(N * K, SEED, 32, s), list(range(M)), N, K)
+    got = T.bf16_to_f32(d2h(dev, c, M * N)).reshape(M, N)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL

@@ -45,7 +45,9 @@ def gemm(dev):
 def test_gemm_preempt_resume_bit_exact(dev, gemm):
     n, c, k, ref = gemm
     off, _ = dev.calibrate(100)
-    for delay in (0.0, 50e-6, 150e-6):
+    # A preemption lands ~5 us after the raise; runs shorter than one tile (~30 us here)
+    # complete nothing (abandoned tiles restart), so every run gets at least ~1 tile time.
+    for delay in (40e-6, 120e-6, 400e-6):
         dev.memset(c, 0, n * n * 2)
         dev.lp_reset(k)
         begin, runs, exits = 0, 0, []
@@ -61,7 +63,7 @@ def test_gemm_preempt_resume_bit_exact(dev, gemm):
             begin = st["cursor"]
             if begin >= k.total_tiles and st["redo_count"] == 0:
                 break
-            assert runs < 2000
+            assert runs < 3000
         assert runs > 1
         assert np.array_equal(d2h(dev, c, n * n), ref), delay
         if exits:
