@@ -165,6 +165,15 @@ int ms_hp_register_chain(ms_dev* dev, const ms_hp_op* ops, int n_ops, int* chain
 uint32_t ms_hp_next_seq(ms_dev* dev);
 /* Pre-enqueue gate(seq) + the chain's kernels on the highest-priority stream. */
 int ms_hp_arm(ms_dev* dev, int chain_id, uint32_t seq);
+/* Chain execution mode, applied by later ms_hp_register_chain / arm / launch calls:
+   1 (default): a chain whose kernel ops are contiguous and tile-aligned runs as ONE
+   persistent launch (weights of op i+1 stream during op i; grid phase counters between
+   ops; k-slices of a tile reduced through cluster DSMEM when the split is 2 or 4).
+   2: fused, k-slices reduced through global memory (no clusters).  0: one kernel per op
+   (PDL-linked).  The cluster/no-cluster choice is fixed when the chain is registered. */
+int ms_hp_set_fused(ms_dev* dev, int mode);
+/* Fused plan of a registered chain: grid size and cluster size (0, 0: not fusable). */
+int ms_hp_chain_info(ms_dev* dev, int chain_id, int* fused_grid, int* cluster);
 /* Ring the doorbell: release store doorbell = seq (host ns of the store in *t_host_ns). */
 int ms_hp_ring(ms_dev* dev, uint32_t seq, int64_t* t_host_ns);
 /* Baseline path: launch the chain now with no gate (host launch on the critical path). */

@@ -11,6 +11,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -19,6 +20,7 @@
 #include "ms_b200.h"
 #include "stream_kernels.cuh"
 #include "tc_gemm.cuh"
+#include "hp_fused.cuh"
 
 using namespace msdev;
 
@@ -115,6 +117,16 @@ struct HpOpRt {
 struct HpChain {
   bool used = false;
   std::vector<HpOpRt> ops;
+  // Fused plan (hp_fused.cuh): the chain's kernel ops [fused_first, fused_last] as one launch.
+  bool fusable = false;
+  int fused_first = -1, fused_last = -1;
+  int fused_grid = 0;
+  int fused_ctl = 0;
+  int fused_cs = 1;  // cluster size (k-slices reduced through DSMEM) or 1
+  int n_phases = 0;
+  FusedProgram* prog_d = nullptr;
+  uint32_t* phase_d = nullptr;
+  std::vector<float*> fused_ws;
 };
 
 }  // namespace
@@ -138,6 +150,7 @@ struct ms_dev {
   unsigned long long* dbg = nullptr;  // per-CTA phase stamps of the next LP run (diagnostics)
   unsigned long long* dbg_buf = nullptr;
   int lp_sm_reserve = 1;  // SMs an LP GEMM grid leaves free (the HP gate's home)
+  int hp_fused = 1;       // 0: per-op kernels; 1: fused launch (cluster split-K when it fits); 2: fused, no clusters
 };
 
 namespace {
@@ -151,6 +164,12 @@ int set_smem_attrs() {
                                GemmCfg<128>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                GemmCfg<64>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               FusedCfg<1>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               FusedCfg<2>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               FusedCfg<4>::kSmemBytes));
   done = true;
   return 0;
 }
@@ -168,18 +187,33 @@ TileRun base_run(ms_dev* d, int ctl_index) {
 // `pdl`: launch with programmatic stream serialisation, so the kernel is scheduled as soon
 // as its predecessor triggers griddepcontrol.launch_dependents (HP chains only).
 template <typename K, typename... Args>
-cudaError_t launch_k(K kernel, int grid, int block, int smem, cudaStream_t st, bool pdl, Args... args) {
+cudaError_t launch_kc(K kernel, int grid, int block, int smem, cudaStream_t st, bool pdl, int cluster, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <typename K, typename... Args>
+cudaError_t launch_k(K kernel, int grid, int block, int smem, cudaStream_t st, bool pdl, Args... args) {
+  return launch_kc(kernel, grid, block, smem, st, pdl, 1, args...);
 }
 
 int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
@@ -284,6 +318,173 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   p.cols = static_cast<int>(o.op.n);
   const int grid = static_cast<int>(std::min<int64_t>(o.op.m, d->prop.multiProcessorCount));
   MS_CUDA(launch_k(bias_gelu_kernel, grid, 256, 0, d->hp, prev_is_kernel, p));
+  return 0;
+}
+
+// Build the fused plan of a registered chain (no-op when the chain does not qualify).
+int plan_fused(ms_dev* d, HpChain& ch) {
+  int first = -1, last = -1;
+  for (int i = 0; i < static_cast<int>(ch.ops.size()); ++i)
+    if (!is_copy(ch.ops[i].op)) {
+      if (first < 0) first = i;
+      last = i;
+    }
+  if (first < 0) return 0;
+  for (int i = first; i <= last; ++i) {
+    const ms_hp_op& op = ch.ops[i].op;
+    if (is_copy(op)) return 0;  // copies between kernels: keep per-op launches
+    if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % kFusedBN || op.k % kBK)) return 0;
+    if (op.kind == MS_HP_BIAS_GELU && op.n % 8) return 0;
+  }
+  const int sms = d->prop.multiProcessorCount;
+  FusedProgram prog{};
+  prog.n_ops = last - first + 1;
+  // k-slices per GEMM op: enough units to cover the SMs
+  std::vector<int> splits(prog.n_ops, 1);
+  int max_units = 0, common_split = -1;
+  bool any_gemm = false;
+  for (int i = first; i <= last; ++i) {
+    const HpOpRt& o = ch.ops[i];
+    if (o.op.kind != MS_HP_GEMM) continue;
+    const int tiles = static_cast<int>(o.op.m / kBM) * static_cast<int>(o.op.n / kFusedBN);
+    const int kbs = static_cast<int>(o.op.k / kBK);
+    int split = o.op.split_k > 0 ? o.op.split_k : 1;
+    if (o.op.split_k <= 0)
+      while (tiles * split * 2 <= sms && kbs % (split * 2) == 0 && kbs / (split * 2) >= 4) split *= 2;
+    splits[i - first] = split;
+    max_units = std::max(max_units, tiles * split);
+    common_split = (!any_gemm || common_split == split) ? split : 0;
+    any_gemm = true;
+  }
+  // Cluster split-K: every GEMM op uses the same split CS in {2, 4}, one unit per CTA,
+  // and all CTAs fit as co-resident clusters (the grid phases need co-residency).
+  int cs = 1;
+  if (any_gemm && (common_split == 2 || common_split == 4) && d->hp_fused != 2) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(max_units);
+    cfg.blockDim = dim3(256);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = common_split;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int max_clusters = 0;
+    cudaError_t e;
+    if (common_split == 2) {
+      cfg.dynamicSmemBytes = FusedCfg<2>::kSmemBytes;
+      e = cudaOccupancyMaxActiveClusters(&max_clusters, hp_fused_kernel<2>, &cfg);
+    } else {
+      cfg.dynamicSmemBytes = FusedCfg<4>::kSmemBytes;
+      e = cudaOccupancyMaxActiveClusters(&max_clusters, hp_fused_kernel<4>, &cfg);
+    }
+    if (e != cudaSuccess) cudaGetLastError();
+    if (e == cudaSuccess && max_clusters * common_split >= max_units) cs = common_split;
+  }
+  int np = 0, grid = std::min(std::max(max_units, 1), sms);
+  for (int i = first; i <= last; ++i) {
+    const HpOpRt& o = ch.ops[i];
+    FusedOp& f = prog.ops[i - first];
+    f.m = static_cast<int>(o.op.m);
+    f.n = static_cast<int>(o.op.n);
+    f.k = static_cast<int>(o.op.k);
+    f.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+    f.in_phase = i > first ? prog.ops[i - first - 1].ready_phase : -1;
+    if (o.op.kind == MS_HP_GEMM) {
+      f.kind = kFusedGemm;
+      f.tiles_m = f.m / kBM;
+      f.tiles_n = f.n / kFusedBN;
+      const int split = splits[i - first];
+      f.split = split;
+      f.kb_per_unit = f.k / kBK / split;
+      f.units = f.tiles_m * f.tiles_n * split;
+      if (int rc = encode_2d(&f.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
+      if (o.b_tiled || o.op.b_layout == 2) {
+        f.b_kmajor = 1;
+        const void* wb = o.b_tiled ? static_cast<const void*>(o.b_tiled) : reinterpret_cast<const void*>(o.op.b);
+        if (int rc = encode_kblock_major(&f.tma_b, wb, o.op.n, o.op.k, kFusedBN)) return rc;
+      } else {
+        if (int rc = encode_2d(&f.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, kFusedBN)) return rc;
+      }
+      if (cs > 1) {  // slices reduced inside the cluster: one phase (output ready)
+        f.mma_phase = -1;
+        f.ready_phase = np++;
+      } else {
+        if (split > 1) {
+          MS_CUDA(cudaMalloc(&f.ws, sizeof(float) * static_cast<size_t>(split) * f.m * f.n));
+          ch.fused_ws.push_back(f.ws);
+        }
+        f.mma_phase = np++;
+        f.ready_phase = split > 1 ? np++ : f.mma_phase;
+      }
+    } else {
+      f.kind = kFusedBiasGelu;
+      f.x = reinterpret_cast<const __nv_bfloat16*>(o.op.a);
+      f.bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
+      f.mma_phase = -1;
+      f.ready_phase = np++;
+      if (!any_gemm) {
+        const long long chunks = o.op.m * o.op.n / 8;
+        grid = std::max<int>(grid, static_cast<int>(std::min<long long>((chunks + 127) / 128, sms)));
+      }
+    }
+  }
+  if (cs > 1) grid = max_units;
+  ch.fused_cs = cs;
+  prog.n_phases = np;
+  prog.l2_prefetch = getenv("MS_FUSED_NO_PREFETCH") ? 0 : 1;
+  MS_CUDA(cudaMalloc(&ch.prog_d, sizeof(FusedProgram)));
+  MS_CUDA(cudaMemcpy(ch.prog_d, &prog, sizeof(FusedProgram), cudaMemcpyHostToDevice));
+  MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * std::max(np, 1)));
+  MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * std::max(np, 1)));
+  ch.fused_ctl = d->next_hp_ctl++;
+  if (ch.fused_ctl >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
+  ch.fused_first = first;
+  ch.fused_last = last;
+  ch.fused_grid = grid;
+  ch.n_phases = np;
+  ch.fusable = true;
+  return 0;
+}
+
+int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl) {
+  FusedParams p{};
+  p.run = base_run(d, ch.fused_ctl);
+  p.run.hp_ctl = d->hp_ctl + chain_id;
+  p.run.hp_rec = &d->page_d->hp[chain_id];
+  p.run.hp_first = 1;
+  p.run.hp_last = !is_copy(ch.ops.back().op);
+  p.run.hp_seq = seq;
+  p.run.dbg = d->dbg;
+  p.run.reset_words = ch.phase_d;
+  p.run.n_reset = ch.n_phases;
+  p.prog = ch.prog_d;
+  p.phase_cnt = ch.phase_d;
+  switch (ch.fused_cs) {
+    case 4:
+      MS_CUDA(launch_kc(hp_fused_kernel<4>, ch.fused_grid, 256, FusedCfg<4>::kSmemBytes, d->hp, pdl, 4, p));
+      break;
+    case 2:
+      MS_CUDA(launch_kc(hp_fused_kernel<2>, ch.fused_grid, 256, FusedCfg<2>::kSmemBytes, d->hp, pdl, 2, p));
+      break;
+    default:
+      MS_CUDA(launch_kc(hp_fused_kernel<1>, ch.fused_grid, 256, FusedCfg<1>::kSmemBytes, d->hp, pdl, 1, p));
+  }
+  return 0;
+}
+
+// Enqueue a chain's work on the HP stream (after its gate when `after_gate`).
+int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after_gate) {
+  const bool fused = d->hp_fused && ch.fusable;
+  for (size_t i = 0; i < ch.ops.size(); ++i) {
+    if (fused && static_cast<int>(i) >= ch.fused_first && static_cast<int>(i) <= ch.fused_last) {
+      if (static_cast<int>(i) == ch.fused_first)
+        if (int rc = launch_fused(d, cid, ch, seq, after_gate && i == 0)) return rc;
+      continue;
+    }
+    if (int rc = launch_hp_op(d, cid, ch, i, seq, after_gate)) return rc;
+  }
   return 0;
 }
 
@@ -695,9 +896,24 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
     }
     ch.ops.push_back(o);
   }
+  if (int rc = plan_fused(d, ch)) return rc;
   ch.used = true;
   d->chains[cid] = ch;
   *chain_id = cid;
+  return 0;
+}
+
+int ms_hp_set_fused(ms_dev* d, int mode) {
+  if (mode < 0 || mode > 2) return fail(MS_E_ARG, "fused mode must be 0, 1 or 2");
+  d->hp_fused = mode;
+  return 0;
+}
+
+int ms_hp_chain_info(ms_dev* d, int cid, int* fused_grid, int* cluster) {
+  if (cid < 0 || cid >= MS_MAX_HP_CHAINS || !d->chains[cid].used) return fail(MS_E_ARG, "bad chain");
+  const HpChain& ch = d->chains[cid];
+  if (fused_grid) *fused_grid = ch.fusable ? ch.fused_grid : 0;
+  if (cluster) *cluster = ch.fusable ? ch.fused_cs : 0;
   return 0;
 }
 
@@ -708,9 +924,7 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   // CTA co-resident with the spinning gate observed preemptions ~5 us late.
   gate_kernel<<<1, 32, kGateSmem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
-  for (size_t i = 0; i < ch.ops.size(); ++i)
-    if (int rc = launch_hp_op(d, cid, ch, i, seq, true)) return rc;
-  return 0;
+  return launch_chain(d, cid, ch, seq, true);
 }
 
 uint32_t ms_hp_next_seq(ms_dev* d) { return ++d->hp_seq; }
@@ -725,9 +939,7 @@ int ms_hp_ring(ms_dev* d, uint32_t seq, int64_t* t_host) {
 int ms_hp_launch_direct(ms_dev* d, int cid, uint32_t seq) {
   const HpChain& ch = d->chains[cid];
   if (!ch.used) return fail(MS_E_ARG, "bad chain");
-  for (size_t i = 0; i < ch.ops.size(); ++i)
-    if (int rc = launch_hp_op(d, cid, ch, i, seq, false)) return rc;
-  return 0;
+  return launch_chain(d, cid, ch, seq, false);
 }
 
 int ms_hp_poll(ms_dev* d, int cid, uint32_t seq, ms_hp_times* t) {

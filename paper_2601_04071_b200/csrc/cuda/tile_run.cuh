@@ -41,10 +41,17 @@ struct TileRun {
   unsigned int hp_seq;
   int pdl_wait;  // HP chain kernel whose inputs come from the previous chain kernel
   unsigned long long* dbg;  // optional per-CTA phase timestamps [gridDim][8] (diagnostics)
+  uint32_t* reset_words;    // zeroed by the last CTA to exit (grid-phase counters of a fused chain)
+  int n_reset;
 };
 
 __device__ __forceinline__ void dbg_stamp(const TileRun& r, int phase) {
   if (r.dbg) r.dbg[blockIdx.x * 8 + phase] = globaltimer();
+}
+
+// Extended per-CTA stamps (64 slots per CTA after the [gridDim][8] block).
+__device__ __forceinline__ void dbg_stamp_ext(const TileRun& r, int slot) {
+  if (r.dbg) r.dbg[2048 + blockIdx.x * 64 + slot] = globaltimer();
 }
 
 __device__ __forceinline__ unsigned long long current_budget(const TileRun& r) {
@@ -152,6 +159,7 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
                       (static_cast<uint64_t>(r.hp_seq) << 32) | ((t_exit - first) & 0xFFFFFFFFull));
     r.hp_ctl->t_first_cta = ~0ull;
   }
+  for (int i = 0; i < r.n_reset; ++i) r.reset_words[i] = 0;
   ctl->claim = 0;
   ctl->tiles_done = 0;
   ctl->t_start = ~0ull;

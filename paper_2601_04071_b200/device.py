@@ -88,6 +88,8 @@ def lib() -> C.CDLL:
             "ms_lp_run_ex": (I, [P, I, U64, U64, U64, I]), "ms_lp_unregister": (I, [P, I]),
             "ms_debug_stamps": (I, [P, I, C.POINTER(C.c_ulonglong), C.c_size_t]),
             "ms_set_lp_sm_reserve": (I, [P, I]),
+            "ms_hp_set_fused": (I, [P, I]),
+            "ms_hp_chain_info": (I, [P, I, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "ms_hp_launch_direct": (I, [P, I, U32]),
             "ms_hp_poll": (I, [P, I, U32, C.POINTER(HpTimes)]),
             "ms_hp_wait": (I, [P, I, U32, I64, C.POINTER(HpTimes)]),
@@ -218,6 +220,16 @@ class Device:
     def set_lp_sm_reserve(self, n: int):
         _ck(lib().ms_set_lp_sm_reserve(self._h, n))
 
+    def hp_set_fused(self, mode):
+        """1/True: fused launch per chain (cluster split-K when it fits, default);
+        2: fused, global split-K reduction; 0/False: one kernel per HP op."""
+        _ck(lib().ms_hp_set_fused(self._h, int(mode)))
+
+    def hp_chain_info(self, chain: int) -> dict:
+        g, c = C.c_int(), C.c_int()
+        _ck(lib().ms_hp_chain_info(self._h, chain, C.byref(g), C.byref(c)))
+        return {"fused_grid": g.value, "cluster": c.value}
+
     def debug_stamps(self, enable: bool, n_cta: int = 148):
         if enable:
             _ck(lib().ms_debug_stamps(self._h, 1, None, 0))
@@ -225,6 +237,12 @@ class Device:
         buf = (C.c_ulonglong * (n_cta * 8))()
         _ck(lib().ms_debug_stamps(self._h, 0, buf, n_cta * 8))
         return [list(buf[i * 8:(i + 1) * 8]) for i in range(n_cta)]
+
+    def debug_stamps_ext(self, n_cta: int = 148) -> list[list[int]]:
+        """Read (and disarm) the extended [cta][64] stamp block (fused HP chain kernel)."""
+        buf = (C.c_ulonglong * (2048 + n_cta * 64))()
+        _ck(lib().ms_debug_stamps(self._h, 0, buf, 2048 + n_cta * 64))
+        return [list(buf[2048 + i * 64:2048 + (i + 1) * 64]) for i in range(n_cta)]
 
     # ---- preemption
     def preempt_raise(self) -> tuple[int, int]:

@@ -96,8 +96,11 @@ def test_axpy_bit_exact(dev, T, n, tile):
     dev.free(y)
 
 
-def test_hp_chain_matches_oracle(dev, T):
-    """Config-1 HP chain: 4 chained GEMMs + bias/GELU; fp32-accumulated bf16 ops."""
+@pytest.mark.parametrize("fused", [1, 2, 0])
+def test_hp_chain_matches_oracle(dev, T, fused):
+    """Config-1 HP chain: 4 chained GEMMs + bias/GELU; fp32-accumulated bf16 ops — as one
+    fused launch (cluster/DSMEM split-K, or global split-K) and as one kernel per op."""
+    dev.hp_set_fused(fused)
     M, H = 128, 1024
     act = [dev.alloc(M * H * 2) for _ in range(5)]
     ws = [dev.alloc(H * H * 2) for _ in range(4)]
@@ -123,6 +126,39 @@ def test_hp_chain_matches_oracle(dev, T):
     want = T.bf16_to_f32(T.bias_gelu(d2h(dev, act[4], M * H), T.synth_bf16(H, SEED, 110, 0.1), M, H))
     got = T.bf16_to_f32(d2h(dev, out, M * H))
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+    dev.hp_set_fused(True)
+
+
+def test_hp_chain_fused_equals_per_op(dev, T):
+    """Per-op kernels, the cluster (DSMEM) fused launch and the global-reduction fused
+    launch use the same tiles, k-slices and slice-order sums: config-1-size chains agree
+    bit for bit (and across repeated launches)."""
+    M, H = 128, 4096
+    act = [dev.alloc(M * H * 2) for _ in range(5)]
+    ws = [dev.alloc(H * H * 2) for _ in range(4)]
+    bias, out = dev.alloc(H * 2), dev.alloc(M * H * 2)
+    s = float(np.float32(1 / math.sqrt(H)))
+    for i, w in enumerate(ws):
+        dev.fill_synth(w, H * H, SEED, 201 + i, s)
+    dev.fill_synth(bias, H, SEED, 210, 0.1)
+    ops = [dict(kind=1, block_n=128, a=act[i], b=ws[i], c=act[i + 1], bias=0, m=M, n=H, k=H) for i in range(4)]
+    ops.append(dict(kind=2, block_n=0, a=act[4], b=0, c=out, bias=bias, m=M, n=H, k=0))
+    results = []
+    for fused in (0, 1, 1, 2):
+        dev.hp_set_fused(fused)
+        chain = dev.hp_register_chain(ops)
+        info = dev.hp_chain_info(chain)
+        assert info["fused_grid"] == 128 and (fused == 0 or info["cluster"] == (4 if fused == 1 else 1))
+        dev.fill_synth(act[0], M * H, SEED, 200, 1.0)
+        for a in act[1:] + [out]:
+            dev.memset(a, 0, M * H * 2)
+        dev.hp_launch_direct(chain, dev.hp_next_seq())
+        dev.sync()
+        results.append([d2h(dev, a, M * H) for a in act[1:] + [out]])
+    dev.hp_set_fused(True)
+    for r in results[1:]:
+        for x, y in zip(results[0], r):
+            assert np.array_equal(x, y)
 
 
 @pytest.mark.parametrize("split", [1, 2, 4, 8])
