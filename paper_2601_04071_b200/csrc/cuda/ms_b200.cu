@@ -68,6 +68,23 @@ int encode_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, 
   return 0;
 }
 
+// C (bf16 [rows][cols]) for the TMA-store epilogue: 32 x 32 boxes, 64B swizzle.
+int encode_c(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+  if (!g_encode) {
+    CUtensorMap dummy;
+    if (int rc = encode_2d(&dummy, base, 128, 64, 64)) return rc;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(MS_E_CUDA, "cuTensorMapEncodeTiled(C) failed: " + std::to_string(r));
+  return 0;
+}
+
 int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   // bf16 [cols/64][rows][64]; box = 64 x box_rows x 1 = box_rows x 128 B contiguous.
   if (!g_encode) {
@@ -93,7 +110,7 @@ struct LpSlot {
   ms_lp_desc desc{};
   uint64_t total_tiles = 0;
   int tiles_m = 0, tiles_n = 0;
-  CUtensorMap tma_a{}, tma_b{};
+  CUtensorMap tma_a{}, tma_b{}, tma_c{};
   unsigned long long* redo[2] = {nullptr, nullptr};
   uint64_t run_id = 0;
   uint64_t redo_carry = 0;  // redo entries waiting in redo[run_id % 2] for the next run
@@ -104,7 +121,7 @@ struct LpSlot {
 
 struct HpOpRt {
   ms_hp_op op{};
-  CUtensorMap tma_a{}, tma_b{};
+  CUtensorMap tma_a{}, tma_b{}, tma_c{};
   int tiles_m = 0, tiles_n = 0;
   int ctl_index = 0;
   int split = 1;
@@ -216,17 +233,17 @@ cudaError_t launch_k(K kernel, int grid, int block, int smem, cudaStream_t st, b
   return launch_kc(kernel, grid, block, smem, st, pdl, 1, args...);
 }
 
-int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int grid,
-                cudaStream_t st, bool pdl = false) {
+int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                const GemmParams& p, int grid, cudaStream_t st, bool pdl = false) {
   switch (block_n) {
     case 256:
-      MS_CUDA(launch_k(tc_gemm_kernel<256>, grid, 256, GemmCfg<256>::kSmemBytes, st, pdl, ta, tb, p));
+      MS_CUDA(launch_k(tc_gemm_kernel<256>, grid, 256, GemmCfg<256>::kSmemBytes, st, pdl, ta, tb, tc, p));
       break;
     case 128:
-      MS_CUDA(launch_k(tc_gemm_kernel<128>, grid, 256, GemmCfg<128>::kSmemBytes, st, pdl, ta, tb, p));
+      MS_CUDA(launch_k(tc_gemm_kernel<128>, grid, 256, GemmCfg<128>::kSmemBytes, st, pdl, ta, tb, tc, p));
       break;
     case 64:
-      MS_CUDA(launch_k(tc_gemm_kernel<64>, grid, 256, GemmCfg<64>::kSmemBytes, st, pdl, ta, tb, p));
+      MS_CUDA(launch_k(tc_gemm_kernel<64>, grid, 256, GemmCfg<64>::kSmemBytes, st, pdl, ta, tb, tc, p));
       break;
     default:
       return fail(MS_E_ARG, "block_n must be 64, 128 or 256");
@@ -280,11 +297,11 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
     p.group_m = 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
     const int grid = static_cast<int>(std::min<uint64_t>(p.run.end, d->prop.multiProcessorCount));
-    if (o.split == 1) return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, p, grid, d->hp, prev_is_kernel);
+    if (o.split == 1) return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, o.tma_c, p, grid, d->hp, prev_is_kernel);
     // split-K: the GEMM streams partials; the reduce kernel carries the chain's last-op role
     const bool last = p.run.hp_last;
     p.run.hp_last = 0;
-    if (int rc = launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, p, grid, d->hp, prev_is_kernel)) return rc;
+    if (int rc = launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, o.tma_c, p, grid, d->hp, prev_is_kernel)) return rc;
     SplitReduceParams rp{};
     rp.run = base_run(d, o.reduce_ctl_index);
     rp.run.hp_ctl = r.hp_ctl;
@@ -643,6 +660,7 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n;
     if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
     if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, bn)) return rc;
+    if (int rc = encode_c(&s.tma_c, reinterpret_cast<void*>(desc->c), desc->m, desc->n)) return rc;
   } else if (desc->kind == MS_LP_AXPY) {
     s.desc.tile_elems = desc->tile_elems ? desc->tile_elems : 8192;
     s.desc.ctas_per_sm = desc->ctas_per_sm ? desc->ctas_per_sm : 4;
@@ -719,7 +737,7 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.group_m = s.desc.group_m ? s.desc.group_m : 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount - d->lp_sm_reserve)));
-    return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, p, grid, d->lp);
+    return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, s.tma_c, p, grid, d->lp);
   }
   StreamParams p{};
   p.run = r;
@@ -873,6 +891,7 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
         if (o.reduce_ctl_index >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
       }
       if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
+      if (int rc = encode_c(&o.tma_c, reinterpret_cast<void*>(o.op.c), o.op.m, o.op.n)) return rc;
       if (o.op.b_layout == 1) {
         if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
       } else {

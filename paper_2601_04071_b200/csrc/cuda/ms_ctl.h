@@ -68,15 +68,17 @@ struct MsDevMirror {
   uint64_t budget[MS_MAX_LP][16];
 };
 
-struct MsLpCtl {
+struct alignas(128) MsLpCtl {
   unsigned long long claim;       // virtual claim index: redo_in entries first, then fresh tiles
-  unsigned long long tiles_done;
+  unsigned long long tiles_done;  // (unused by the kernels; kept for layout stability)
   unsigned long long t_start;     // min over CTAs
   unsigned long long t_seen;      // min over CTAs that saw the epoch
-  unsigned int exited;            // CTAs finished
+  unsigned int exited;            // CTAs finished (relaxed; read by CTA 0's host poller)
   unsigned int redo_out_n;
   unsigned int preempted;
-  unsigned int pad[9];
+  unsigned int pad[17];
+  unsigned long long top;  // exit counter: (tiles done << 32) | CTAs exited, own 128 B line
+  unsigned long long pad2[15];
 };
 
 struct MsHpCtl {                  // per HP chain slot, device memory

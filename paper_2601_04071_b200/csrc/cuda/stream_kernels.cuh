@@ -254,6 +254,7 @@ __global__ void init_ctl_kernel(MsLpCtl* ctl, int n, MsHpCtl* hp, int n_hp) {
     ctl[i].exited = 0;
     ctl[i].redo_out_n = 0;
     ctl[i].preempted = 0;
+    ctl[i].top = 0;
   }
   if (i < n_hp) hp[i].t_first_cta = ~0ull;
 }

@@ -52,7 +52,10 @@ struct GemmCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (200 * 1024 / kStageBytes) > 8 ? 8 : (200 * 1024 / kStageBytes);
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 1024 /*barriers etc.*/;
+  // C staging for the TMA-store epilogue: per epilogue warp 2 x [32 rows x 32 cols] bf16
+  // (64 B rows, 64B-swizzled), double-buffered.
+  static constexpr int kCStageBytes = 4 * 2 * 32 * 64;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kCStageBytes + 1024 /*barriers etc.*/;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN);
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN must be a multiple of 32 in [32, 256]");
 };
@@ -85,14 +88,15 @@ __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, in
 template <int BN>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                   const __grid_constant__ GemmParams p) {
+                   const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ GemmParams p) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * Cfg::kABytes;
-  GemmSmemCtl* s = reinterpret_cast<GemmSmemCtl*>(smem + S * Cfg::kStageBytes);
+  uint8_t* smem_c = smem + S * Cfg::kStageBytes;
+  GemmSmemCtl* s = reinterpret_cast<GemmSmemCtl*>(smem_c + Cfg::kCStageBytes);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -119,6 +123,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tma_a);
     prefetch_tmap(&tma_b);
+    if (p.split_k <= 1) prefetch_tmap(&tma_c);
   }
   if (warp == 2) tmem_alloc(&s->tmem_base, Cfg::kTmemCols);
   tc_fence_before();
@@ -180,6 +185,11 @@ __global__ void __launch_bounds__(256, 1)
     // ===================== UMMA issuer =====================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, drain_phase = 0;
+      // Preemptible runs keep at most 2 k-blocks of MMAs queued on the tensor core: an abort
+      // then drains <= 2 k-blocks instead of the whole smem ring (lower preemption latency;
+      // the queue still never runs dry).
+      uint32_t h_stage0 = 0, h_phase0 = 0, h_stage1 = 0, h_phase1 = 0;  // kLag = 2 history
+      int issued = 0;
       for (int j = 0;; ++j) {
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
@@ -198,6 +208,18 @@ __global__ void __launch_bounds__(256, 1)
           if (aborted) {
             mbar_arrive(&s->empty[stage]);
           } else {
+            if (p.run.preemptible) {
+              const bool odd = issued & 1;
+              if (issued >= 2) mbar_wait(&s->empty[odd ? h_stage1 : h_stage0], odd ? h_phase1 : h_phase0);
+              if (odd) {
+                h_stage1 = stage;
+                h_phase1 = phase;
+              } else {
+                h_stage0 = stage;
+                h_phase0 = phase;
+              }
+              ++issued;
+            }
             const uint64_t a0 = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
             const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + stage * Cfg::kBBytes));
 #pragma unroll
@@ -235,6 +257,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp - 4;  // TMEM lane quarter
+    int cbuf_idx = 0;
     for (int j = 0;; ++j) {
       const int slot = j & 1;
       mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
@@ -250,7 +273,6 @@ __global__ void __launch_bounds__(256, 1)
         tile_coords(unit_tile, p, mb, nb);
         const int row_in_tile = q * 32 + lane;
         const int row = mb * kBM + row_in_tile;
-        __nv_bfloat16* crow = p.c + static_cast<size_t>(row) * p.n + static_cast<size_t>(nb) * BN;
         // split-K partial layout (per unit, 128 x BN fp32): [BN / 4][128 rows] of float4, so for a
         // fixed column quad the 32 lanes of a warp touch 512 contiguous bytes (coalesced).
         float4* wunit = split > 1 ? reinterpret_cast<float4*>(p.ws) +
@@ -268,7 +290,11 @@ __global__ void __launch_bounds__(256, 1)
                   make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                               __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
           } else {
-            uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+            // bf16 -> this warp's staging buffer (64B swizzle: chunk ^= (row >> 1) & 3, conflict
+            // free) -> one TMA store of the 32 x 32 box.  The buffer is reused two stores later.
+            uint8_t* cbuf = smem_c + (q * 2 + cbuf_idx) * (32 * 64);
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 w;
@@ -276,8 +302,15 @@ __global__ void __launch_bounds__(256, 1)
               w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
               w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
               w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
-              dst[v] = w;
+              *reinterpret_cast<uint4*>(cbuf + lane * 64 + ((v ^ ((lane >> 1) & 3)) * 16)) = w;
             }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tma_c, cbuf, nb * BN + c0, mb * kBM + q * 32);
+              bulk_commit();
+            }
+            cbuf_idx ^= 1;
           }
         }
         if (q == 0 && lane == 0) ++s->tiles_done;
@@ -323,6 +356,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+    if (lane == 0) bulk_wait_read<0>();  // staging must stay valid until the TMA read it
     if (q == 0 && lane == 0) dbg_stamp(p.run, 3);
   }
 

@@ -127,17 +127,28 @@ __device__ __forceinline__ void poll_host(const TileRun& r, const uint32_t* pree
 }
 
 // Called by thread 0 of each CTA after all of the CTA's work (and TMEM traffic) is done.
+// One acq_rel atomic per CTA on MsLpCtl::top ((tiles << 32) | 1) publishes this CTA's
+// tile / redo accounting (ordered by the CTA barrier before cta_exit) and lets the last
+// CTA acquire everyone else's.  (A two-level tree measured slower: the last CTA then pays
+// two L2 round trips while the preempted CTAs' in-flight loads drain.)
 __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_done_cta) {
   MsLpCtl* ctl = r.ctl;
   dbg_stamp(r, 5);
-  atomicAdd(&ctl->tiles_done, static_cast<unsigned long long>(tiles_done_cta));
-  // acq_rel: publishes this CTA's tile / redo accounting (ordered by the CTA barrier before
-  // cta_exit) and, for the last CTA, acquires everyone else's.
-  const unsigned int prev = atom_add_acqrel_gpu(&ctl->exited, 1u);
-  if (prev + 1 != gridDim.x) return;
-  const unsigned long long claimed = *reinterpret_cast<volatile unsigned long long*>(&ctl->claim);
+  atomicAdd(&ctl->exited, 1u);  // relaxed: only CTA 0's host poller reads it
+  const unsigned long long w =
+      atom_add_acqrel_gpu_u64(&ctl->top, (static_cast<unsigned long long>(tiles_done_cta) << 32) | 1ull);
+  dbg_stamp_ext(r, 1);
+  if (static_cast<unsigned int>(w) + 1 != gridDim.x) return;
+  const unsigned long long tiles_total = (w >> 32) + tiles_done_cta;
+  // Issue every control-block read at once (each is an L2 round trip, slow while the
+  // preempted CTAs' in-flight loads still drain).
+  const unsigned long long claimed = ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->claim));
+  unsigned int redo_n = ld_relaxed_gpu(&ctl->redo_out_n);
+  const unsigned long long t_start = ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->t_start));
+  const unsigned long long t_seen = ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->t_seen));
+  const unsigned int preempted = ld_relaxed_gpu(&ctl->preempted);
   // Redo entries nobody claimed carry over to the next run.
-  for (unsigned long long idx = claimed; idx < r.nr_in; ++idx) r.redo_out[ctl->redo_out_n++] = r.redo_in[idx];
+  for (unsigned long long idx = claimed; idx < r.nr_in; ++idx) r.redo_out[redo_n++] = r.redo_in[idx];
   unsigned long long cursor = r.begin;
   if (claimed > r.nr_in) cursor = min(r.end, r.begin + (claimed - r.nr_in));
   const unsigned long long t_exit = globaltimer();
@@ -145,12 +156,12 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
   if (r.exit_rec) {
     MsLpExit* e = r.exit_rec;
     st_relaxed_sys_u64(&e->cursor, cursor);
-    st_relaxed_sys_u64(&e->redo_count, ctl->redo_out_n);
-    st_relaxed_sys_u64(&e->tiles_done, ctl->tiles_done);
-    st_relaxed_sys_u64(&e->t_start, ctl->t_start);
-    st_relaxed_sys_u64(&e->t_seen, ctl->t_seen == ~0ull ? 0ull : ctl->t_seen);
+    st_relaxed_sys_u64(&e->redo_count, redo_n);
+    st_relaxed_sys_u64(&e->tiles_done, tiles_total);
+    st_relaxed_sys_u64(&e->t_start, t_start);
+    st_relaxed_sys_u64(&e->t_seen, t_seen == ~0ull ? 0ull : t_seen);
     st_relaxed_sys_u64(&e->t_exit, t_exit);
-    st_relaxed_sys_u64(&e->preempted, ctl->preempted);
+    st_relaxed_sys_u64(&e->preempted, preempted);
     st_release_sys_u64(&e->run_id, r.run_id);  // host acquires run_id, then reads the rest
   }
   if (r.hp_ctl && r.hp_last && r.hp_rec) {
@@ -160,8 +171,8 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
     r.hp_ctl->t_first_cta = ~0ull;
   }
   for (int i = 0; i < r.n_reset; ++i) r.reset_words[i] = 0;
+  ctl->top = 0;
   ctl->claim = 0;
-  ctl->tiles_done = 0;
   ctl->t_start = ~0ull;
   ctl->t_seen = ~0ull;
   ctl->redo_out_n = 0;

@@ -8,7 +8,7 @@ from paper_2601_04071_b200.live import Config1
 dev = Device(0)
 w = Config1(dev)
 off, _ = dev.calibrate(200)
-names = ["seen", "prod_done", "mma_done", "epi_done", "teardown", "exit_begin", "last"]
+names = ["seen", "prod_done", "mma_done", "epi_done", "teardown", "exit_begin", "last", "tiles_atom", "exit_atom"]
 for trial in range(6):
     dev.lp_reset(w.lp)
     dev.debug_stamps(True)
@@ -18,7 +18,9 @@ for trial in range(6):
         pass
     _, t_raise = dev.preempt_raise()
     st = dev.lp_wait(w.lp, 30)
+    dx = np.array(dev.debug_stamps_ext(148), dtype=np.float64)[:, :2]
     d = np.array(dev.debug_stamps(False), dtype=np.float64)
+    d = np.concatenate([d[:, :7], dx], axis=1)
     raise_dev = t_raise + off
     rel = (d - raise_dev) / 1e3
     rel[d == 0] = np.nan

@@ -14,5 +14,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_g
   -o gpurun_out/prof_gemm -f python tools/ncu_target.py > gpurun_out/ncu_gemm.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:axpy_kernel -s 1 -c 1 \
   -o gpurun_out/prof_axpy -f python tools/ncu_target.py > gpurun_out/ncu_axpy.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:hp_fused -s 1 -c 1 \
+  -o gpurun_out/prof_fused -f python tools/ncu_fused.py > gpurun_out/ncu_fused.log 2>&1
 fi
 tail -2 gpurun_out/smoke.log gpurun_out/pytest_gpu.log; tail -c 3000 gpurun_out/bench.log; tail -c 1500 gpurun_out/bench_ref.log
