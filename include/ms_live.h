@@ -7,9 +7,12 @@
  * events in the Timeline — but kernels execute on the GPU and every timestamp is real.
  *
  * scenario_json : reference scenario schema (scenario_io.hpp)
- * policy        : "splitkernel" | "exclusive" | "exclusive_lp" | "reef" (kernel-boundary
- *                 temporal sharing: unsplit, non-preemptible LP kernels, LP only between
- *                 HP requests, HP waits for the running LP kernel)
+ * policy        : "splitkernel" | "exclusive" | "exclusive_lp" | "reef" | "reef_req"
+ *                 reef = kernel-boundary temporal sharing as the reference's Reef policy
+ *                 models it (engine.hpp:949-997, 1129-1143): unsplit, non-preemptible LP
+ *                 kernels relaunched whenever HP drains (after the scheduler sync); an HP
+ *                 segment arriving meanwhile waits for the running LP kernel.
+ *                 reef_req = the same with LP only between HP requests.
  * binding_json  : {"lp": {"<kernel name>": <ms_lp id>, ...},
  *                  "hp": {"<task name>": [<chain id of segment 0>, ...], ...}}
  * options_json  : {"eager": bool, "slo": {"ttft_ns": .., "tpot_ns": ..},

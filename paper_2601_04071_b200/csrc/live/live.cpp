@@ -43,7 +43,7 @@ struct Timer {
   long b;
   bool operator>(const Timer& o) const { return t != o.t ? t > o.t : seq > o.seq; }
 };
-enum TimerKind { kArrival, kBubbleOver, kLargeBubble };
+enum TimerKind { kArrival, kBubbleOver, kLargeBubble, kReefRefill };
 
 struct HpTask {
   const TaskSpec* spec = nullptr;
@@ -90,7 +90,12 @@ class LiveRun {
       : dev_(dev), sc_(std::move(sc)), policy_(std::move(policy)), opts_(opts),
         predictor_(sc_.sched.ema_alpha, sc_.sched.ema_k, sc_.sched.large_bubble_threshold) {
     harvest_ = policy_ == "splitkernel";
-    reef_ = policy_ == "reef";
+    // Kernel-boundary temporal sharing (the reference's Reef policy, engine.hpp:949-997,
+    // 1129-1143): non-preemptible LP kernels are (re)launched whenever HP drains; an HP
+    // segment that arrives meanwhile waits for the running LP kernel to finish.
+    // "reef_req": the same, but LP only between HP requests (request-level boundary).
+    reef_ = policy_ == "reef" || policy_ == "reef_req";
+    reef_req_ = policy_ == "reef_req";
     want_hp_ = policy_ != "exclusive_lp";
     want_lp_ = policy_ != "exclusive";
     eager_ = opts.value("eager", false);
@@ -280,6 +285,11 @@ class LiveRun {
   void hp_drained() {
     if (policy_ == "exclusive") return;
     p_flag_ = false;
+    if (reef_ && !reef_req_) {  // refill after the scheduler's sync (engine.hpp:986-990)
+      art_.sync_cost_total += sc_.gpu.sync_overhead;
+      push_timer(now_ + sc_.gpu.sync_overhead, kReefRefill, 0);
+      return;
+    }
     if (!harvest_ || open_hint_ >= 0) return;
     if (eager_) {
       start_harvest(predictor_.predict());
@@ -350,7 +360,7 @@ class LiveRun {
     rs.completed = true;
     if (!h.backlog.empty()) return begin_request(h);
     h.busy = false;
-    if (reef_) relaunch_if_allowed();  // kernel-boundary sharing: LP only between HP requests
+    if (reef_req_) relaunch_if_allowed();  // request-level boundary: LP only between HP requests
   }
 
   void large_bubble_check(long gen) {
@@ -482,7 +492,7 @@ class LiveRun {
     if (lp_.empty() || lp_running_ || p_flag_) return;
     if (policy_ == "exclusive_lp") return launch_lp();
     if (reef_) {
-      if (!any_hp_busy()) launch_lp();
+      if (!reef_req_ || !any_hp_busy()) launch_lp();
       return;
     }
     if (harvest_ && harvest_open_) launch_lp();
@@ -495,7 +505,7 @@ class LiveRun {
   json opts_;
   json lp_bind_ = json::object();
   json tile_ns_ = json::object();
-  bool harvest_ = false, reef_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
+  bool harvest_ = false, reef_ = false, reef_req_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
   bool direct_hp_ = false, calibrate_ = true;
   int debug_runs_ = 0;
   std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
@@ -589,6 +599,7 @@ json LiveRun::run() {
         case kArrival: request_arrival(t.a, static_cast<std::size_t>(t.b)); break;
         case kBubbleOver: bubble_over(t.a); break;
         case kLargeBubble: large_bubble_check(t.b); break;
+        case kReefRefill: relaunch_if_allowed(); break;  // flag checked before the first wave
       }
     }
     for (HpTask& h : hp_) {
@@ -786,7 +797,10 @@ extern "C" int ms_live_run(ms_dev* dev, const char* scenario_json, const char* p
     const ScenarioSpec sc = scenario_from_json(json::parse(scenario_json));
     const json binding = json::parse(binding_json ? binding_json : "{}");
     const json opts = json::parse(options_json ? options_json : "{}");
-    LiveRun run(dev, sc, policy ? policy : "splitkernel", binding, opts);
+    const std::string pol = policy ? policy : "splitkernel";
+    if (pol != "splitkernel" && pol != "exclusive" && pol != "exclusive_lp" && pol != "reef" && pol != "reef_req")
+      throw ValidationError("policy", "unknown live policy '" + pol + "'");
+    LiveRun run(dev, sc, pol, binding, opts);
     const std::string s = run.run().dump();
     *result_json = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(*result_json, s.c_str(), s.size() + 1);

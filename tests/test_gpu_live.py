@@ -15,6 +15,7 @@ def test_live_config1_short():
     ex = live_run(dev, sc, "exclusive", w.binding(), w.options())
     sk = live_run(dev, sc, "splitkernel", w.binding(), w.options())
     kb = live_run(dev, sc, "reef", w.binding(), w.options())
+    kbr = live_run(dev, sc, "reef_req", w.binding(), w.options())
     lp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options())
     assert ex["requests"]["n"] == sk["requests"]["n"] > 5
     assert sk["requests"]["completed"] >= sk["requests"]["n"] - 1
@@ -22,7 +23,8 @@ def test_live_config1_short():
     assert sk["preempt_ring_to_first_hp_cta"]["n"] >= sk["hp_chains"] - 1
     assert 0 < sk["preempt_ring_to_first_hp_cta"]["p50_ns"] < 200_000
     assert lp["lp"]["tiles_done"] > sk["lp"]["tiles_done"] > 0
-    assert kb["lp"]["tiles_done"] > 0
+    assert kb["lp"]["tiles_done"] > 0 and kbr["lp"]["tiles_done"] > 0
+    assert kb["requests"]["completed"] >= kb["requests"]["n"] - 1
     e2e = live_run(dev, sc, "splitkernel", w.binding(e2e=True), w.options())
     assert e2e["hp_chains"] > 0 and e2e["requests"]["completed"] > 0
     dev.close()

@@ -40,7 +40,7 @@ def main():
     exlp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options())
     print("exclusive_lp", json.dumps(brief(exlp)), flush=True)
     res["exclusive_lp"] = brief(exlp)
-    for pol, kw in [("splitkernel", {}), ("splitkernel", {"eager": True}), ("reef", {})]:
+    for pol, kw in [("splitkernel", {}), ("splitkernel", {"eager": True}), ("reef", {}), ("reef_req", {})]:
         t = time.time()
         r = live_run(dev, sc, pol, w.binding(), w.options(slo=slo, **kw,
                      ndjson_path=str(ROOT / "gpurun_out" / f"live_{pol}{'_eager' if kw else ''}.ndjson")))
