@@ -138,6 +138,7 @@ uint32_t ms_preempt_epoch(ms_dev* dev);
 /* ---- HP chains --------------------------------------------------------------------- */
 #define MS_HP_GEMM 1      /* C = A * B^T (non-preemptible tcgen05 GEMM) */
 #define MS_HP_BIAS_GELU 2 /* c = gelu(a + bias) over m x n */
+#define MS_HP_SILU_MUL 5  /* c[m, n] = silu(a[m, j]) * a[m, n + j]: a is [m x 2n] = [gate | up] */
 #define MS_HP_H2D 3       /* copy m bytes: pinned host a -> device c (e2e request input) */
 #define MS_HP_D2H 4       /* copy m bytes: device a -> pinned host c (e2e request output) */
 
@@ -150,6 +151,8 @@ typedef struct ms_hp_op {
   int32_t b_layout;  /* GEMM weights: 0 = row-major [N,K], captured k-block-major at registration
                         (DRAM-page friendly); 1 = read row-major in place; 2 = b already k-block-major
                         [K/64][N][64] */
+  int64_t lda;       /* GEMM: row stride of a in elements (0: k) — e.g. a column slice of a wider
+                        activation */
 } ms_hp_op;
 
 typedef struct ms_hp_times {
@@ -163,6 +166,8 @@ typedef struct ms_hp_times {
 int ms_hp_register_chain(ms_dev* dev, const ms_hp_op* ops, int n_ops, int* chain_id);
 /* Next value of the device's monotonic doorbell sequence (never reused on this ms_dev). */
 uint32_t ms_hp_next_seq(ms_dev* dev);
+/* Release a chain's device buffers (its slot becomes reusable).  The chain must be idle. */
+int ms_hp_unregister_chain(ms_dev* dev, int chain_id);
 /* Pre-enqueue gate(seq) + the chain's kernels on the highest-priority stream. */
 int ms_hp_arm(ms_dev* dev, int chain_id, uint32_t seq);
 /* Chain execution mode, applied by later ms_hp_register_chain / arm / launch calls:

@@ -24,6 +24,7 @@ def lib():
         L.tr_gemm_rows.argtypes = [P, P, P, I, I, I, P, I]
         L.tr_axpy_bf16.argtypes = [P, P, F, S, S]
         L.tr_bias_gelu.argtypes = [P, P, P, I, I]
+        L.tr_silu_mul.argtypes = [P, P, I, I]
         _lib = L
     return _lib
 
@@ -58,4 +59,11 @@ def axpy(y: np.ndarray, x: np.ndarray, alpha: float, begin: int = 0, end: int | 
 def bias_gelu(x: np.ndarray, bias: np.ndarray, M: int, N: int) -> np.ndarray:
     out = np.empty(M * N, dtype=np.uint16)
     lib().tr_bias_gelu(_p(x), _p(bias), _p(out), M, N)
+    return out
+
+
+def silu_mul(x: np.ndarray, M: int, N: int) -> np.ndarray:
+    """out[m, n] = silu(x[m, n]) * x[m, N + n] for x = [M x 2N] bf16 (oracle/tenant_ref.c)."""
+    out = np.empty(M * N, dtype=np.uint16)
+    lib().tr_silu_mul(_p(x), _p(out), M, N)
     return out

@@ -75,6 +75,17 @@ void tr_axpy_bf16(uint16_t* y, const uint16_t* x, float a, size_t begin, size_t 
   for (size_t i = begin; i < end; ++i) y[i] = f32_to_bf16(fmaf(a, bf16_to_f32(x[i]), bf16_to_f32(y[i])));
 }
 
+/* SwiGLU of a decode layer: out[m, n] = silu(x[m, n]) * x[m, N + n], x = [M x 2N] bf16,
+   fp32 math (the device uses __expf; agreement is within the bf16 tolerance). */
+void tr_silu_mul(const uint16_t* x, uint16_t* out, int M, int N) {
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < N; ++n) {
+      const float g = bf16_to_f32(x[(size_t)m * 2 * N + n]);
+      const float u = bf16_to_f32(x[(size_t)m * 2 * N + N + n]);
+      out[(size_t)m * N + n] = f32_to_bf16(g / (1.0f + expf(-g)) * u);
+    }
+}
+
 /* tanh-approximated GELU of (x + bias[col]) over an M x N bf16 matrix, fp32 math. */
 void tr_bias_gelu(const uint16_t* x, const uint16_t* bias, uint16_t* out, int M, int N) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;

@@ -22,10 +22,11 @@
 
 namespace msdev {
 
-constexpr int kFusedMaxOps = 16;
+constexpr int kFusedMaxOps = 96;
 constexpr int kFusedBN = 128;
 constexpr int kFusedGemm = 1;
 constexpr int kFusedBiasGelu = 2;
+constexpr int kFusedSiluMul = 5;
 
 struct alignas(64) FusedOp {
   CUtensorMap tma_a;
@@ -300,6 +301,30 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOp& o, int u, uint32
   }
 }
 
+// SILU_MUL: out[r, j] = silu(x[r, j]) * x[r, n + j] (x = [m x 2n]); same arithmetic as
+// silu_mul_kernel and oracle tr_silu_mul.
+__device__ __forceinline__ void silu_mul_phase(const FusedOp& o, int t, int G) {
+  const long long chunks = static_cast<long long>(o.m) * o.n / 8;
+  const int cpr = o.n / 8;  // chunks per output row
+  for (long long i = static_cast<long long>(blockIdx.x) * 128 + t; i < chunks; i += static_cast<long long>(G) * 128) {
+    const long long row = i / cpr;
+    const int c = static_cast<int>(i % cpr) * 8;
+    const uint4 gv = *reinterpret_cast<const uint4*>(o.x + row * 2 * o.n + c);
+    const uint4 uv = *reinterpret_cast<const uint4*>(o.x + row * 2 * o.n + o.n + c);
+    const uint32_t* gs = &gv.x;
+    const uint32_t* us = &uv.x;
+    uint4 out;
+    uint32_t* os = &out.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(&gs[e]);
+      const __nv_bfloat162 u2 = *reinterpret_cast<const __nv_bfloat162*>(&us[e]);
+      os[e] = pack_bf16x2(silu_mul(__low2float(g2), __low2float(u2)), silu_mul(__high2float(g2), __high2float(u2)));
+    }
+    *reinterpret_cast<uint4*>(o.c + row * o.n + c) = out;
+  }
+}
+
 template <int CS>
 __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant__ FusedParams p) {
   using Cfg = FusedCfg<CS>;
@@ -332,10 +357,12 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
     fence_mbar_init();
     cta_started(p.run);
   }
-  if (warp == 0 && lane < n_ops && prog.ops[lane].kind == kFusedGemm) {
-    prefetch_tmap(&prog.ops[lane].tma_a);
-    prefetch_tmap(&prog.ops[lane].tma_b);
-  }
+  if (warp == 0)
+    for (int i = lane; i < n_ops; i += 32)
+      if (prog.ops[i].kind == kFusedGemm) {
+        prefetch_tmap(&prog.ops[i].tma_a);
+        prefetch_tmap(&prog.ops[i].tma_b);
+      }
   if (warp == 2) tmem_alloc(&s->tmem_base, Cfg::kTmemCols);
   tc_fence_before();
   if constexpr (CS > 1) cluster_sync_all();  // peers' barriers initialised before any st.async
@@ -541,7 +568,10 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
       } else {
         // BIAS_GELU (tanh form, same arithmetic as bias_gelu_kernel / oracle tr_bias_gelu)
         if (o.in_phase >= 0) group_wait(p.phase_cnt + o.in_phase, static_cast<uint32_t>(G), leader);
-        bias_gelu_phase(o, t, G);
+        if (o.kind == kFusedSiluMul)
+          silu_mul_phase(o, t, G);
+        else
+          bias_gelu_phase(o, t, G);
         group_arrive(p.phase_cnt + o.ready_phase, leader);
       }
     }

@@ -48,8 +48,10 @@ int64_t now_ns() {
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int encode_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  // bf16 [rows, cols] row-major, box = 64 cols (128 B, swizzle 128B) x box_rows.
+int encode_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+              uint64_t row_stride = 0) {
+  // bf16 [rows, cols] row-major (row stride `row_stride` elements, 0 = cols), box = 64 cols
+  // (128 B, swizzle 128B) x box_rows.
   if (!g_encode) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -58,7 +60,7 @@ int encode_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, 
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
+  cuuint64_t strides[1] = {(row_stride ? row_stride : cols) * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -156,7 +158,7 @@ struct ms_dev {
   MsHostPage* page = nullptr;    // host view
   MsHostPage* page_d = nullptr;  // device view of the same page
   MsDevMirror* mirror = nullptr;
-  MsLpCtl* ctl = nullptr;        // [MS_MAX_LP + MS_MAX_HP_CHAINS * 16]
+  MsLpCtl* ctl = nullptr;        // [MS_N_CTL]
   MsHpCtl* hp_ctl = nullptr;     // [MS_MAX_HP_CHAINS]
   unsigned long long* dummy_redo = nullptr;
   LpSlot lp_slots[MS_MAX_LP];
@@ -334,7 +336,10 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   p.rows = static_cast<int>(o.op.m);
   p.cols = static_cast<int>(o.op.n);
   const int grid = static_cast<int>(std::min<int64_t>(o.op.m, d->prop.multiProcessorCount));
-  MS_CUDA(launch_k(bias_gelu_kernel, grid, 256, 0, d->hp, prev_is_kernel, p));
+  if (o.op.kind == MS_HP_SILU_MUL)
+    MS_CUDA(launch_k(silu_mul_kernel, grid, 256, 0, d->hp, prev_is_kernel, p));
+  else
+    MS_CUDA(launch_k(bias_gelu_kernel, grid, 256, 0, d->hp, prev_is_kernel, p));
   return 0;
 }
 
@@ -351,7 +356,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
     const ms_hp_op& op = ch.ops[i].op;
     if (is_copy(op)) return 0;  // copies between kernels: keep per-op launches
     if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % kFusedBN || op.k % kBK)) return 0;
-    if (op.kind == MS_HP_BIAS_GELU && op.n % 8) return 0;
+    if ((op.kind == MS_HP_BIAS_GELU || op.kind == MS_HP_SILU_MUL) && op.n % 8) return 0;
   }
   const int sms = d->prop.multiProcessorCount;
   FusedProgram prog{};
@@ -416,7 +421,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
       f.split = split;
       f.kb_per_unit = f.k / kBK / split;
       f.units = f.tiles_m * f.tiles_n * split;
-      if (int rc = encode_2d(&f.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
+      if (int rc = encode_2d(&f.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM, o.op.lda)) return rc;
       if (o.b_tiled || o.op.b_layout == 2) {
         f.b_kmajor = 1;
         const void* wb = o.b_tiled ? static_cast<const void*>(o.b_tiled) : reinterpret_cast<const void*>(o.op.b);
@@ -436,7 +441,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
         f.ready_phase = split > 1 ? np++ : f.mma_phase;
       }
     } else {
-      f.kind = kFusedBiasGelu;
+      f.kind = o.op.kind == MS_HP_SILU_MUL ? kFusedSiluMul : kFusedBiasGelu;
       f.x = reinterpret_cast<const __nv_bfloat16*>(o.op.a);
       f.bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
       f.mma_phase = -1;
@@ -456,7 +461,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * std::max(np, 1)));
   MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * std::max(np, 1)));
   ch.fused_ctl = d->next_hp_ctl++;
-  if (ch.fused_ctl >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
+  if (ch.fused_ctl >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
   ch.fused_first = first;
   ch.fused_last = last;
   ch.fused_grid = grid;
@@ -533,7 +538,7 @@ int ms_dev_open(int ordinal, ms_dev** out) {
   MS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d->page_d), d->page, 0));
   MS_CUDA(cudaMalloc(&d->mirror, sizeof(MsDevMirror)));
   MS_CUDA(cudaMemset(d->mirror, 0, sizeof(MsDevMirror)));
-  const int n_ctl = MS_MAX_LP + MS_MAX_HP_CHAINS * 16;
+  const int n_ctl = MS_N_CTL;
   MS_CUDA(cudaMalloc(&d->ctl, sizeof(MsLpCtl) * n_ctl));
   MS_CUDA(cudaMalloc(&d->hp_ctl, sizeof(MsHpCtl) * MS_MAX_HP_CHAINS));
   MS_CUDA(cudaMemset(d->hp_ctl, 0, sizeof(MsHpCtl) * MS_MAX_HP_CHAINS));
@@ -860,13 +865,13 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       cid = i;
       break;
     }
-  if (cid < 0 || n_ops < 1 || n_ops > 16) return fail(MS_E_ARG, "bad HP chain");
+  if (cid < 0 || n_ops < 1 || n_ops > kFusedMaxOps) return fail(MS_E_ARG, "bad HP chain");
   HpChain ch;
   for (int i = 0; i < n_ops; ++i) {
     HpOpRt o;
     o.op = ops[i];
     o.ctl_index = d->next_hp_ctl++;
-    if (o.ctl_index >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
+    if (o.ctl_index >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
     if (o.op.kind == MS_HP_GEMM) {
       const int bn = o.op.block_n ? o.op.block_n : 128;
       o.op.block_n = bn;
@@ -888,9 +893,10 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       if (split > 1) {
         MS_CUDA(cudaMalloc(&o.ws, sizeof(float) * static_cast<size_t>(split) * o.op.m * o.op.n));
         o.reduce_ctl_index = d->next_hp_ctl++;
-        if (o.reduce_ctl_index >= MS_MAX_LP + MS_MAX_HP_CHAINS * 16) return fail(MS_E_ARG, "out of HP control blocks");
+        if (o.reduce_ctl_index >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
       }
-      if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM)) return rc;
+      if (o.op.lda && (o.op.lda < o.op.k || o.op.lda % 8)) return fail(MS_E_ARG, "lda must be >= k and a multiple of 8");
+      if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM, o.op.lda)) return rc;
       if (int rc = encode_c(&o.tma_c, reinterpret_cast<void*>(o.op.c), o.op.m, o.op.n)) return rc;
       if (o.op.b_layout == 1) {
         if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
@@ -906,8 +912,8 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
         }
         if (int rc = encode_kblock_major(&o.tma_b, wb, o.op.n, o.op.k, bn)) return rc;
       }
-    } else if (o.op.kind == MS_HP_BIAS_GELU) {
-      if (o.op.n % 8) return fail(MS_E_ARG, "bias_gelu cols must be a multiple of 8");
+    } else if (o.op.kind == MS_HP_BIAS_GELU || o.op.kind == MS_HP_SILU_MUL) {
+      if (o.op.n % 8) return fail(MS_E_ARG, "elementwise cols must be a multiple of 8");
     } else if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
       if (o.op.m <= 0) return fail(MS_E_ARG, "copy size must be > 0");
     } else {
@@ -919,6 +925,22 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
   ch.used = true;
   d->chains[cid] = ch;
   *chain_id = cid;
+  return 0;
+}
+
+int ms_hp_unregister_chain(ms_dev* d, int cid) {
+  if (cid < 0 || cid >= MS_MAX_HP_CHAINS || !d->chains[cid].used) return fail(MS_E_ARG, "bad chain");
+  MS_CUDA(cudaStreamSynchronize(d->hp));
+  HpChain& ch = d->chains[cid];
+  for (HpOpRt& o : ch.ops) {
+    if (o.ws) cudaFree(o.ws);
+    if (o.tile_cnt) cudaFree(o.tile_cnt);
+    if (o.b_tiled) cudaFree(o.b_tiled);
+  }
+  for (float* w : ch.fused_ws) cudaFree(w);
+  if (ch.prog_d) cudaFree(ch.prog_d);
+  if (ch.phase_d) cudaFree(ch.phase_d);
+  ch = HpChain{};
   return 0;
 }
 

@@ -16,7 +16,8 @@
 #include <stdint.h>
 
 #define MS_MAX_LP 16
-#define MS_MAX_HP_CHAINS 32
+#define MS_MAX_HP_CHAINS 64
+#define MS_N_CTL (MS_MAX_LP + 8192)  // control blocks: LP slots, then HP chain kernels
 #define MS_MIRROR_COPIES 8
 #define MS_MIRROR_STRIDE 32  // uint32 elements = 128 B
 

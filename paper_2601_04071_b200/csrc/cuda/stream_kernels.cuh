@@ -166,6 +166,46 @@ __global__ void __launch_bounds__(256) bias_gelu_kernel(const __grid_constant__ 
   if (threadIdx.x == 0) cta_exit(p.run, tiles_done);
 }
 
+// SwiGLU activation of a decode layer: out[r, j] = silu(x[r, j]) * x[r, cols + j], x = [rows x 2 cols].
+__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
+
+__global__ void __launch_bounds__(256) silu_mul_kernel(const __grid_constant__ BiasGeluParams p) {
+  __shared__ long long tile_sh;
+  __shared__ uint32_t tiles_done;
+  if (threadIdx.x == 0) {
+    tiles_done = 0;
+    cta_started(p.run);
+  }
+  if (p.run.hp_ctl) {
+    pdl_launch_dependents();
+    if (p.run.pdl_wait) pdl_wait();
+  }
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) tile_sh = claim_tile(p.run);
+    __syncthreads();
+    const long long r = tile_sh;
+    if (r < 0) break;
+    for (int c = threadIdx.x * 8; c < p.cols; c += blockDim.x * 8) {
+      const uint4 gv = *reinterpret_cast<const uint4*>(p.x + static_cast<size_t>(r) * 2 * p.cols + c);
+      const uint4 uv = *reinterpret_cast<const uint4*>(p.x + static_cast<size_t>(r) * 2 * p.cols + p.cols + c);
+      const uint32_t* gs = &gv.x;
+      const uint32_t* us = &uv.x;
+      uint4 o;
+      uint32_t* os = &o.x;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(&gs[i]);
+        const __nv_bfloat162 u2 = *reinterpret_cast<const __nv_bfloat162*>(&us[i]);
+        os[i] = pack_bf16x2(silu_mul(__low2float(g2), __low2float(u2)), silu_mul(__high2float(g2), __high2float(u2)));
+      }
+      *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(r) * p.cols + c) = o;
+    }
+    if (threadIdx.x == 0) ++tiles_done;
+  }
+  if (threadIdx.x == 0) cta_exit(p.run, tiles_done);
+}
+
 // ---------------------------------------------------------------- HP doorbell gate
 // The doorbell word carries (epoch << 32 | seq).  On release the gate (already resident,
 // no launch needed) first pushes the preempt epoch into the device mirror — every LP CTA
@@ -244,7 +284,7 @@ __global__ void kblock_major_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst
   }
 }
 
-__global__ void init_ctl_kernel(MsLpCtl* ctl, int n, MsHpCtl* hp, int n_hp) {
+__global__ void init_ctl_kernel(MsLpCtl* ctl, int n, MsHpCtl* hp, int n_hp) {  // n = MS_N_CTL
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     ctl[i].claim = 0;

@@ -48,7 +48,7 @@ class LpStatus(C.Structure):
 class HpOp(C.Structure):
     _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("a", C.c_uint64), ("b", C.c_uint64),
                 ("c", C.c_uint64), ("bias", C.c_uint64), ("m", C.c_int64), ("n", C.c_int64),
-                ("k", C.c_int64), ("split_k", C.c_int32), ("b_layout", C.c_int32)]
+                ("k", C.c_int64), ("split_k", C.c_int32), ("b_layout", C.c_int32), ("lda", C.c_int64)]
 
 
 class HpTimes(C.Structure):
@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
             "ms_debug_stamps": (I, [P, I, C.POINTER(C.c_ulonglong), C.c_size_t]),
             "ms_set_lp_sm_reserve": (I, [P, I]),
             "ms_hp_set_fused": (I, [P, I]),
+            "ms_hp_unregister_chain": (I, [P, I]),
             "ms_hp_chain_info": (I, [P, I, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
             "ms_hp_launch_direct": (I, [P, I, U32]),
             "ms_hp_poll": (I, [P, I, U32, C.POINTER(HpTimes)]),
@@ -259,6 +260,9 @@ class Device:
         cid = C.c_int()
         _ck(lib().ms_hp_register_chain(self._h, arr, len(ops), C.byref(cid)))
         return cid.value
+
+    def hp_unregister_chain(self, chain: int):
+        _ck(lib().ms_hp_unregister_chain(self._h, chain))
 
     def hp_next_seq(self) -> int:
         return lib().ms_hp_next_seq(self._h)

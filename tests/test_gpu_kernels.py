@@ -177,3 +177,68 @@ def test_hp_gemm_split_k_matches_oracle(dev, T, split):
     want = T.gemm_rows(T.synth_bf16(M * K, SEED, 31, 1.0), T.synth_bf16(N * K, SEED, 32, s), list(range(M)), N, K)
     got = T.bf16_to_f32(d2h(dev, c, M * N)).reshape(M, N)
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+
+
+def decode_chain_ops(M, H, Q, F, V, layers, bufs, ws, lm):
+    """Synthetic Llama-style decode step (config 4): per layer qkv = h Wqkv^T, o = qkv[:, :H] Wo^T
+    (strided A), gu = o Wgu^T, act = silu(gu[:, :F]) * gu[:, F:], h = act Wd^T; then logits = h Wlm^T."""
+    h, qkv, o, gu, act, logits = bufs
+    ops = []
+    for l in range(layers):
+        wq, wo, wg, wd = ws[l]
+        src = h
+        ops += [dict(kind=1, block_n=128, a=src, b=wq, c=qkv, bias=0, m=M, n=Q, k=H),
+                dict(kind=1, block_n=128, a=qkv, b=wo, c=o, bias=0, m=M, n=H, k=H, lda=Q),
+                dict(kind=1, block_n=128, a=o, b=wg, c=gu, bias=0, m=M, n=2 * F, k=H),
+                dict(kind=5, block_n=0, a=gu, b=0, c=act, bias=0, m=M, n=F, k=0),
+                dict(kind=1, block_n=128, a=act, b=wd, c=h, bias=0, m=M, n=H, k=F)]
+    ops.append(dict(kind=1, block_n=128, a=h, b=lm, c=logits, bias=0, m=M, n=V, k=H))
+    return ops
+
+
+@pytest.mark.parametrize("fused", [1, 2, 0])
+def test_hp_decode_chain_matches_oracle(dev, T, fused):
+    """Config-4 HP step (2 layers + LM head, small geometry) incl. strided A and SILU_MUL,
+    against the oracle chain with bf16 rounding between ops."""
+    dev.hp_set_fused(fused)
+    M, H, Q, F, V, L = 128, 256, 384, 512, 1024, 2
+    bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
+    s = lambda k: float(np.float32(1 / math.sqrt(k)))
+    ws, host_w = [], []
+    for l in range(L):
+        shapes = [(Q, H), (H, H), (2 * F, H), (H, F)]
+        ptrs = []
+        hw = []
+        for j, (n, k) in enumerate(shapes):
+            p = dev.alloc(n * k * 2)
+            dev.fill_synth(p, n * k, SEED, 300 + 10 * l + j, s(k))
+            ptrs.append(p)
+            hw.append(T.synth_bf16(n * k, SEED, 300 + 10 * l + j, s(k)))
+        ws.append(ptrs)
+        host_w.append(hw)
+    lm = dev.alloc(V * H * 2)
+    dev.fill_synth(lm, V * H, SEED, 399, s(H))
+    dev.fill_synth(bufs[0], M * H, SEED, 298, 1.0)
+    chain = dev.hp_register_chain(decode_chain_ops(M, H, Q, F, V, L, bufs, ws, lm))
+    dev.hp_launch_direct(chain, dev.hp_next_seq())
+    dev.sync()
+
+    def rnd(y):  # fp32 -> bf16 bits (RNE), like the device epilogue
+        u = y.astype(np.float32).view(np.uint32)
+        return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+    rows = list(range(M))
+    h = T.synth_bf16(M * H, SEED, 298, 1.0)
+    for l in range(L):
+        wq, wo, wg, wd = host_w[l]
+        qkv = rnd(T.gemm_rows(h, wq, rows, Q, H).reshape(-1))
+        qh = np.ascontiguousarray(qkv.reshape(M, Q)[:, :H]).reshape(-1)
+        o = rnd(T.gemm_rows(qh, wo, rows, H, H).reshape(-1))
+        gu = rnd(T.gemm_rows(o, wg, rows, 2 * F, H).reshape(-1))
+        act = T.silu_mul(gu, M, F)
+        h = rnd(T.gemm_rows(act, wd, rows, H, F).reshape(-1))
+    want = T.gemm_rows(h, T.synth_bf16(V * H, SEED, 399, s(H)), rows, V, H)
+    got = T.bf16_to_f32(d2h(dev, bufs[5], M * V)).reshape(M, V)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+    dev.hp_unregister_chain(chain)
+    dev.hp_set_fused(1)
