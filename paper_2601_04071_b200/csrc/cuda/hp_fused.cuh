@@ -28,9 +28,9 @@ constexpr int kFusedGemm = 1;
 constexpr int kFusedBiasGelu = 2;
 constexpr int kFusedSiluMul = 5;
 
-struct alignas(64) FusedOp {
-  CUtensorMap tma_a;
-  CUtensorMap tma_b;
+// Scalar description of one op; copied into shared memory at kernel start (the grid-phase
+// acquires invalidate L1, so re-reading these from global on every use costs L2 trips).
+struct FusedOpDesc {
   int kind;
   int m, n, k;
   int tiles_m, tiles_n, split, kb_per_unit, units;
@@ -42,6 +42,12 @@ struct alignas(64) FusedOp {
   float* ws;
   const __nv_bfloat16* x;  // BIAS_GELU input
   const __nv_bfloat16* bias;
+};
+
+struct alignas(64) FusedOp {
+  CUtensorMap tma_a;
+  CUtensorMap tma_b;
+  FusedOpDesc d;
 };
 
 // Shared-memory plan.  CS > 1: the k-slices of a tile run on the CS CTAs of one thread-
@@ -71,13 +77,19 @@ struct FusedProgram {
   int l2_prefetch;  // warm the L2 with the next op's weights (1) or not (0)
 };
 
+// Kernel parameters (constant bank): the op descriptors live here rather than in global or
+// shared memory — reads go through the constant cache, which the grid-phase acquires do not
+// invalidate, and the compiler may re-load them freely instead of pinning registers.
 struct FusedParams {
   TileRun run;  // HP bookkeeping (first-CTA stamp, completion record, phase-counter reset)
-  const FusedProgram* prog;
+  const FusedProgram* prog;  // tensor maps (global memory, 64 B aligned)
   uint32_t* phase_cnt;
+  int n_ops;
+  int l2_prefetch;
+  FusedOpDesc ops[kFusedMaxOps];
 };
 
-__device__ __forceinline__ void fused_unit_coords(const FusedOp& o, int u, int& mb, int& nb, int& kb0) {
+__device__ __forceinline__ void fused_unit_coords(const FusedOpDesc& o, int u, int& mb, int& nb, int& kb0) {
   const int tile = u / o.split;
   mb = tile % o.tiles_m;
   nb = tile / o.tiles_m;
@@ -108,7 +120,7 @@ __device__ __forceinline__ void group_wait(const uint32_t* cnt, uint32_t target,
 // ---- grid phases (epilogue warps, 128 threads per CTA).  Each thread owns items
 // blockIdx.x * 128 + t + b * G * 128; all loads of a batch are issued before the first
 // add so one L2 latency covers the batch (the phases are latency-, not bandwidth-bound).
-__device__ __forceinline__ void reduce_store(const FusedOp& o, int i, const float4& x) {
+__device__ __forceinline__ void reduce_store(const FusedOpDesc& o, int i, const float4& x) {
   constexpr int quads = kFusedBN / 4;
   const int row = i % kBM;
   const int tq = i / kBM;
@@ -120,7 +132,7 @@ __device__ __forceinline__ void reduce_store(const FusedOp& o, int i, const floa
   out.y = pack_bf16x2(x.z, x.w);
   *reinterpret_cast<uint2*>(o.c + static_cast<size_t>(mb * kBM + row) * o.n + static_cast<size_t>(nb) * kFusedBN + cq * 4) = out;
 }
-__device__ __forceinline__ const float4* reduce_src(const FusedOp& o, int i) {
+__device__ __forceinline__ const float4* reduce_src(const FusedOpDesc& o, int i) {
   constexpr int quads = kFusedBN / 4;
   const int row = i % kBM;
   const int tq = i / kBM;
@@ -131,7 +143,7 @@ __device__ __forceinline__ const float4* reduce_src(const FusedOp& o, int i) {
 }
 
 template <int SPLIT, int B>
-__device__ __forceinline__ void reduce_slices(const FusedOp& o, int t, int G) {
+__device__ __forceinline__ void reduce_slices(const FusedOpDesc& o, int t, int G) {
   constexpr size_t slice_stride = kBM * kFusedBN / 4;
   const int total = o.tiles_m * o.tiles_n * (kFusedBN / 4) * kBM;
   const int step = G * 128;
@@ -161,7 +173,7 @@ __device__ __forceinline__ void reduce_slices(const FusedOp& o, int t, int G) {
   }
 }
 
-__device__ __forceinline__ void reduce_slices_any(const FusedOp& o, int t, int G) {
+__device__ __forceinline__ void reduce_slices_any(const FusedOpDesc& o, int t, int G) {
   constexpr size_t slice_stride = kBM * kFusedBN / 4;
   const int total = o.tiles_m * o.tiles_n * (kFusedBN / 4) * kBM;
   for (int i = blockIdx.x * 128 + t; i < total; i += G * 128) {
@@ -176,7 +188,7 @@ __device__ __forceinline__ void reduce_slices_any(const FusedOp& o, int t, int G
 }
 
 // BIAS_GELU (tanh form; same arithmetic as bias_gelu_kernel and oracle tr_bias_gelu).
-__device__ __forceinline__ void bias_gelu_phase(const FusedOp& o, int t, int G) {
+__device__ __forceinline__ void bias_gelu_phase(const FusedOpDesc& o, int t, int G) {
   constexpr int B = 4;
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   const long long chunks = static_cast<long long>(o.m) * o.n / 8;
@@ -217,7 +229,7 @@ __device__ __forceinline__ void bias_gelu_phase(const FusedOp& o, int t, int G) 
 // Cluster-mode epilogue of one unit (CS > 1): send the other ranks' strips of this CTA's
 // fp32 partial, sum the received slices with its own strip in slice order, store bf16.
 template <int CS>
-__device__ __forceinline__ void cluster_epilogue(const FusedOp& o, int u, uint32_t tmem_row, uint8_t* recv,
+__device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, uint32_t tmem_row, uint8_t* recv,
                                                  uint64_t* recv_full, uint32_t recv_parity, int q, int lane,
                                                  bool leader, const TileRun& run, int oi) {
   using Cfg = FusedCfg<CS>;
@@ -303,25 +315,39 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOp& o, int u, uint32
 
 // SILU_MUL: out[r, j] = silu(x[r, j]) * x[r, n + j] (x = [m x 2n]); same arithmetic as
 // silu_mul_kernel and oracle tr_silu_mul.
-__device__ __forceinline__ void silu_mul_phase(const FusedOp& o, int t, int G) {
-  const long long chunks = static_cast<long long>(o.m) * o.n / 8;
+__device__ __forceinline__ void silu_mul_phase(const FusedOpDesc& o, int t, int G) {
+  constexpr int B = 4;  // chunks in flight per thread
+  const int chunks = o.m * o.n / 8;
   const int cpr = o.n / 8;  // chunks per output row
-  for (long long i = static_cast<long long>(blockIdx.x) * 128 + t; i < chunks; i += static_cast<long long>(G) * 128) {
-    const long long row = i / cpr;
-    const int c = static_cast<int>(i % cpr) * 8;
-    const uint4 gv = *reinterpret_cast<const uint4*>(o.x + row * 2 * o.n + c);
-    const uint4 uv = *reinterpret_cast<const uint4*>(o.x + row * 2 * o.n + o.n + c);
-    const uint32_t* gs = &gv.x;
-    const uint32_t* us = &uv.x;
-    uint4 out;
-    uint32_t* os = &out.x;
+  const int step = G * 128;
+  for (int i0 = blockIdx.x * 128 + t; i0 < chunks; i0 += step * B) {
+    uint4 gv[B], uv[B];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(&gs[e]);
-      const __nv_bfloat162 u2 = *reinterpret_cast<const __nv_bfloat162*>(&us[e]);
-      os[e] = pack_bf16x2(silu_mul(__low2float(g2), __low2float(u2)), silu_mul(__high2float(g2), __high2float(u2)));
+    for (int b = 0; b < B; ++b) {
+      const int i = i0 + b * step;
+      if (i < chunks) {
+        const int row = i / cpr, c = (i - row * cpr) * 8;
+        gv[b] = *reinterpret_cast<const uint4*>(o.x + static_cast<size_t>(row) * 2 * o.n + c);
+        uv[b] = *reinterpret_cast<const uint4*>(o.x + static_cast<size_t>(row) * 2 * o.n + o.n + c);
+      }
     }
-    *reinterpret_cast<uint4*>(o.c + row * o.n + c) = out;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int i = i0 + b * step;
+      if (i >= chunks) continue;
+      const int row = i / cpr, c = (i - row * cpr) * 8;
+      const uint32_t* gs = &gv[b].x;
+      const uint32_t* us = &uv[b].x;
+      uint4 out;
+      uint32_t* os = &out.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(&gs[e]);
+        const __nv_bfloat162 u2 = *reinterpret_cast<const __nv_bfloat162*>(&us[e]);
+        os[e] = pack_bf16x2(silu_mul(__low2float(g2), __low2float(u2)), silu_mul(__high2float(g2), __high2float(u2)));
+      }
+      *reinterpret_cast<uint4*>(o.c + static_cast<size_t>(row) * o.n + c) = out;
+    }
   }
 }
 
@@ -338,7 +364,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
   GemmSmemCtl* s = reinterpret_cast<GemmSmemCtl*>(recv + Cfg::kRecvBytes);
   uint64_t* recv_full = &s->mma_drain;  // (no drain in the HP chain) cluster receive barrier
   const FusedProgram& prog = *p.prog;
-  const int n_ops = prog.n_ops;
+  const int n_ops = p.n_ops;
   const int G = static_cast<int>(gridDim.x);
 
   const int warp = threadIdx.x / 32;
@@ -357,12 +383,11 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
     fence_mbar_init();
     cta_started(p.run);
   }
-  if (warp == 0)
-    for (int i = lane; i < n_ops; i += 32)
-      if (prog.ops[i].kind == kFusedGemm) {
-        prefetch_tmap(&prog.ops[i].tma_a);
-        prefetch_tmap(&prog.ops[i].tma_b);
-      }
+  for (int i = threadIdx.x; i < n_ops; i += blockDim.x)
+    if (p.ops[i].kind == kFusedGemm) {
+      prefetch_tmap(&prog.ops[i].tma_a);
+      prefetch_tmap(&prog.ops[i].tma_b);
+    }
   if (warp == 2) tmem_alloc(&s->tmem_base, Cfg::kTmemCols);
   tc_fence_before();
   if constexpr (CS > 1) cluster_sync_all();  // peers' barriers initialised before any st.async
@@ -376,8 +401,10 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       for (int oi = 0; oi < n_ops; ++oi) {
-        const FusedOp& o = prog.ops[oi];
+        const FusedOpDesc& o = p.ops[oi];
         if (o.kind != kFusedGemm) continue;
+        const CUtensorMap* tma_a = &prog.ops[oi].tma_a;
+        const CUtensorMap* tma_b = &prog.ops[oi].tma_b;
         bool a_ready = o.in_phase < 0;
         const int dslot = oi * 8;
         dbg_stamp_ext(p.run, dslot + 0);
@@ -393,7 +420,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
               dbg_stamp_ext(p.run, dslot + 1);
               fence_proxy_async_global();
               for (int i = 0; i < deferred; ++i) {
-                tma_load_2d(smem_a + d_stage * Cfg::kABytes, &o.tma_a, &s->full[d_stage], (kb0 + d_kb + i) * kBK,
+                tma_load_2d(smem_a + d_stage * Cfg::kABytes, tma_a, &s->full[d_stage], (kb0 + d_kb + i) * kBK,
                             mb * kBM);
                 if (++d_stage == S) d_stage = 0;
               }
@@ -402,11 +429,11 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
             mbar_wait(&s->empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&s->full[stage], Cfg::kStageBytes);
             if (o.b_kmajor)
-              tma_load_3d(smem_b + stage * Cfg::kBBytes, &o.tma_b, &s->full[stage], 0, nb * BN, kb0 + kb);
+              tma_load_3d(smem_b + stage * Cfg::kBBytes, tma_b, &s->full[stage], 0, nb * BN, kb0 + kb);
             else
-              tma_load_2d(smem_b + stage * Cfg::kBBytes, &o.tma_b, &s->full[stage], (kb0 + kb) * kBK, nb * BN);
+              tma_load_2d(smem_b + stage * Cfg::kBBytes, tma_b, &s->full[stage], (kb0 + kb) * kBK, nb * BN);
             if (a_ready)
-              tma_load_2d(smem_a + stage * Cfg::kABytes, &o.tma_a, &s->full[stage], (kb0 + kb) * kBK, mb * kBM);
+              tma_load_2d(smem_a + stage * Cfg::kABytes, tma_a, &s->full[stage], (kb0 + kb) * kBK, mb * kBM);
             else
               ++deferred;
             if (++stage == S) {
@@ -418,7 +445,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
             phase_wait(p.phase_cnt + o.in_phase, static_cast<uint32_t>(G));
             fence_proxy_async_global();
             for (int i = 0; i < deferred; ++i) {
-              tma_load_2d(smem_a + d_stage * Cfg::kABytes, &o.tma_a, &s->full[d_stage], (kb0 + d_kb + i) * kBK,
+              tma_load_2d(smem_a + d_stage * Cfg::kABytes, tma_a, &s->full[d_stage], (kb0 + d_kb + i) * kBK,
                           mb * kBM);
               if (++d_stage == S) d_stage = 0;
             }
@@ -428,17 +455,18 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
         dbg_stamp_ext(p.run, dslot + 2);
         // This CTA's loads of op oi are all issued: warm the L2 with the weights of its
         // units in the next GEMM op (their HBM latency overlaps op oi's tail + phases).
-        for (int oj = oi + 1; oj < n_ops && prog.l2_prefetch; ++oj) {
-          const FusedOp& q = prog.ops[oj];
+        for (int oj = oi + 1; oj < n_ops && p.l2_prefetch; ++oj) {
+          const FusedOpDesc& q = p.ops[oj];
           if (q.kind != kFusedGemm) continue;
+          const CUtensorMap* qtma_b = &prog.ops[oj].tma_b;
           for (int u = blockIdx.x; u < q.units; u += G) {
             int mb, nb, kb0;
             fused_unit_coords(q, u, mb, nb, kb0);
             for (int kb = S; kb < q.kb_per_unit; ++kb) {  // the first S go straight to smem
               if (q.b_kmajor)
-                tma_prefetch_l2_3d(&q.tma_b, 0, nb * BN, kb0 + kb);
+                tma_prefetch_l2_3d(qtma_b, 0, nb * BN, kb0 + kb);
               else
-                tma_prefetch_l2_2d(&q.tma_b, (kb0 + kb) * kBK, nb * BN);
+                tma_prefetch_l2_2d(qtma_b, (kb0 + kb) * kBK, nb * BN);
             }
           }
           break;
@@ -451,7 +479,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
       uint32_t stage = 0, phase = 0;
       int j = 0;
       for (int oi = 0; oi < n_ops; ++oi) {
-        const FusedOp& o = prog.ops[oi];
+        const FusedOpDesc& o = p.ops[oi];
         if (o.kind != kFusedGemm) continue;
         for (int u = blockIdx.x; u < o.units; u += G, ++j) {
           const int slot = j & 1;
@@ -486,9 +514,9 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
     int j = 0;
     uint32_t recv_parity = 0;
     for (int oi = 0; oi < n_ops; ++oi) {
-      const FusedOp& o = prog.ops[oi];
+      const FusedOpDesc& o = p.ops[oi];
       if constexpr (CS > 1) {
-        if (o.kind == kFusedGemm) {
+        if (o.kind == kFusedGemm && o.split > 1) {
           // one unit per CTA per op (host plan), slices of a tile = the CTAs of a cluster
           const int u = blockIdx.x;
           if (u < o.units) {
@@ -526,7 +554,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
             uint32_t r[32];
             tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * BN + c0), r);
             tmem_ld_wait();
-            if (o.split > 1) {
+            if (CS == 1 && o.split > 1) {  // (cluster launches reduce k-slices in DSMEM)
 #pragma unroll
               for (int v = 0; v < 8; ++v)
                 wunit[static_cast<size_t>(c0 / 4 + v) * kBM + row_in_tile] =
@@ -552,14 +580,14 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 6);
         group_arrive(p.phase_cnt + o.mma_phase, leader);
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 7);
-        if (o.split > 1) {
+        if (CS == 1 && o.split > 1) {
           // Reduce the k-slices (slice order) into bf16 C across the whole grid.
           group_wait(p.phase_cnt + o.mma_phase, static_cast<uint32_t>(G), leader);
           if (leader) dbg_stamp_ext(p.run, 40 + oi * 2);
           switch (o.split) {
-            case 2: reduce_slices<2, 8>(o, t, G); break;
-            case 4: reduce_slices<4, 4>(o, t, G); break;
-            case 8: reduce_slices<8, 2>(o, t, G); break;
+            case 2: reduce_slices<2, 6>(o, t, G); break;
+            case 4: reduce_slices<4, 3>(o, t, G); break;
+            case 8: reduce_slices<8, 1>(o, t, G); break;
             default: reduce_slices_any(o, t, G); break;
           }
           if (leader) dbg_stamp_ext(p.run, 41 + oi * 2);
@@ -567,12 +595,16 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
         }
       } else {
         // BIAS_GELU (tanh form, same arithmetic as bias_gelu_kernel / oracle tr_bias_gelu)
+        if (leader) dbg_stamp_ext(p.run, oi * 8 + 4);
         if (o.in_phase >= 0) group_wait(p.phase_cnt + o.in_phase, static_cast<uint32_t>(G), leader);
+        if (leader) dbg_stamp_ext(p.run, oi * 8 + 5);
         if (o.kind == kFusedSiluMul)
           silu_mul_phase(o, t, G);
         else
           bias_gelu_phase(o, t, G);
+        if (leader) dbg_stamp_ext(p.run, oi * 8 + 6);
         group_arrive(p.phase_cnt + o.ready_phase, leader);
+        if (leader) dbg_stamp_ext(p.run, oi * 8 + 7);
       }
     }
     if (leader) dbg_stamp(p.run, 6);

@@ -145,6 +145,8 @@ struct HpChain {
   int n_phases = 0;
   FusedProgram* prog_d = nullptr;
   uint32_t* phase_d = nullptr;
+  std::vector<FusedOpDesc> descs;  // copied into the launch parameters
+  int l2_prefetch = 1;
   std::vector<float*> fused_ws;
 };
 
@@ -361,107 +363,164 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   const int sms = d->prop.multiProcessorCount;
   FusedProgram prog{};
   prog.n_ops = last - first + 1;
-  // k-slices per GEMM op: enough units to cover the SMs
-  std::vector<int> splits(prog.n_ops, 1);
-  int max_units = 0, common_split = -1;
-  bool any_gemm = false;
+  // Grid <= SMs - 1: a preemptible LP kernel's CTA 0 (its host poller) may hold one SM
+  // until its not-yet-resident CTAs have run; a fused chain that needed every SM could then
+  // wait at its first grid phase for an SM that only frees after the LP stragglers run.
+  const int max_grid = sms - 1;
+  struct GemmShape {
+    int idx, tiles, kbs, req;
+  };
+  std::vector<GemmShape> gemms;
   for (int i = first; i <= last; ++i) {
-    const HpOpRt& o = ch.ops[i];
-    if (o.op.kind != MS_HP_GEMM) continue;
-    const int tiles = static_cast<int>(o.op.m / kBM) * static_cast<int>(o.op.n / kFusedBN);
-    const int kbs = static_cast<int>(o.op.k / kBK);
-    int split = o.op.split_k > 0 ? o.op.split_k : 1;
-    if (o.op.split_k <= 0)
-      while (tiles * split * 2 <= sms && kbs % (split * 2) == 0 && kbs / (split * 2) >= 4) split *= 2;
-    splits[i - first] = split;
-    max_units = std::max(max_units, tiles * split);
-    common_split = (!any_gemm || common_split == split) ? split : 0;
-    any_gemm = true;
+    const ms_hp_op& op = ch.ops[i].op;
+    if (op.kind != MS_HP_GEMM) continue;
+    gemms.push_back({i - first, static_cast<int>(op.m / kBM) * static_cast<int>(op.n / kFusedBN),
+                     static_cast<int>(op.k / kBK), op.split_k});
   }
-  // Cluster split-K: every GEMM op uses the same split CS in {2, 4}, one unit per CTA,
-  // and all CTAs fit as co-resident clusters (the grid phases need co-residency).
-  int cs = 1;
-  if (any_gemm && (common_split == 2 || common_split == 4) && d->hp_fused != 2) {
+  std::vector<int> splits(prog.n_ops, 1);
+  int cs = 1, max_units = 0;
+  // (1) Cluster split-K (k-slices reduced through DSMEM): each GEMM op gets split CS when its
+  // tiles x CS fit one unit per CTA (else split 1, tiles spread over the grid); all CTAs
+  // must be co-resident as clusters (the grid phases need co-residency).
+  for (int c : {4, 2}) {
+    if (d->hp_fused == 2 || gemms.empty()) break;
+    std::vector<int> sp(prog.n_ops, 1);
+    int mu = 0, n_split = 0;
+    bool ok = true;
+    for (const GemmShape& g : gemms) {
+      int split = 1;
+      if (g.req > 0) {
+        if (g.req != 1 && g.req != c) ok = false;
+        split = g.req;
+      } else if (g.tiles * c <= max_grid && g.kbs % c == 0 && g.kbs / c >= 2) {
+        split = c;
+      }
+      if (split > 1 && g.kbs % split) ok = false;
+      sp[g.idx] = split;
+      n_split += split > 1;
+      mu = std::max(mu, g.tiles * split);
+    }
+    if (!ok || n_split == 0) continue;
+    const int grid_c = std::min(mu, max_grid) / c * c;
+    for (const GemmShape& g : gemms)
+      if (sp[g.idx] > 1 && g.tiles * sp[g.idx] > grid_c) ok = false;
+    if (!ok || grid_c < c) continue;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(max_units);
+    cfg.gridDim = dim3(grid_c);
     cfg.blockDim = dim3(256);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = common_split;
+    attr[0].val.clusterDim.x = c;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int max_clusters = 0;
     cudaError_t e;
-    if (common_split == 2) {
+    if (c == 2) {
       cfg.dynamicSmemBytes = FusedCfg<2>::kSmemBytes;
       e = cudaOccupancyMaxActiveClusters(&max_clusters, hp_fused_kernel<2>, &cfg);
     } else {
       cfg.dynamicSmemBytes = FusedCfg<4>::kSmemBytes;
       e = cudaOccupancyMaxActiveClusters(&max_clusters, hp_fused_kernel<4>, &cfg);
     }
-    if (e != cudaSuccess) cudaGetLastError();
-    if (e == cudaSuccess && max_clusters * common_split >= max_units) cs = common_split;
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (max_clusters * c < grid_c) continue;
+    // Only worth it when no GEMM op loses parallelism against the no-cluster plan (k-slices
+    // doubled while the units fit the SMs): e.g. a [128 x 2048] x [2048 x 8192]^T op keeps
+    // 128 units with 8 global k-slices but only 32 with cluster pairs.
+    bool keeps = true;
+    for (const GemmShape& g : gemms) {
+      int gs = g.req > 0 ? g.req : 1;
+      if (g.req <= 0)
+        while (g.tiles * gs * 2 <= sms && g.kbs % (gs * 2) == 0 && g.kbs / (gs * 2) >= 4) gs *= 2;
+      const int u_global = std::min(g.tiles * gs, max_grid), u_cluster = std::min(g.tiles * sp[g.idx], grid_c);
+      if (10 * u_cluster < 9 * u_global) keeps = false;
+    }
+    if (!keeps) continue;
+    cs = c;
+    splits = sp;
+    max_units = grid_c;  // grid of the cluster launch
+    break;
   }
-  int np = 0, grid = std::min(std::max(max_units, 1), sms);
+  // (2) No clusters: k-slices reduced through global partials + a grid phase; split doubles
+  // while the units still fit the SMs.
+  if (cs == 1)
+    for (const GemmShape& g : gemms) {
+      int split = g.req > 0 ? g.req : 1;
+      if (g.req <= 0)
+        while (g.tiles * split * 2 <= sms && g.kbs % (split * 2) == 0 && g.kbs / (split * 2) >= 4) split *= 2;
+      splits[g.idx] = split;
+      max_units = std::max(max_units, g.tiles * split);
+    }
+  const bool any_gemm = !gemms.empty();
+  int np = 0, grid = std::min(std::max(max_units, 1), max_grid);
   for (int i = first; i <= last; ++i) {
     const HpOpRt& o = ch.ops[i];
     FusedOp& f = prog.ops[i - first];
-    f.m = static_cast<int>(o.op.m);
-    f.n = static_cast<int>(o.op.n);
-    f.k = static_cast<int>(o.op.k);
-    f.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
-    f.in_phase = i > first ? prog.ops[i - first - 1].ready_phase : -1;
+    f.d.m = static_cast<int>(o.op.m);
+    f.d.n = static_cast<int>(o.op.n);
+    f.d.k = static_cast<int>(o.op.k);
+    f.d.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+    f.d.in_phase = i > first ? prog.ops[i - first - 1].d.ready_phase : -1;
     if (o.op.kind == MS_HP_GEMM) {
-      f.kind = kFusedGemm;
-      f.tiles_m = f.m / kBM;
-      f.tiles_n = f.n / kFusedBN;
+      f.d.kind = kFusedGemm;
+      f.d.tiles_m = f.d.m / kBM;
+      f.d.tiles_n = f.d.n / kFusedBN;
       const int split = splits[i - first];
-      f.split = split;
-      f.kb_per_unit = f.k / kBK / split;
-      f.units = f.tiles_m * f.tiles_n * split;
+      f.d.split = split;
+      f.d.kb_per_unit = f.d.k / kBK / split;
+      f.d.units = f.d.tiles_m * f.d.tiles_n * split;
       if (int rc = encode_2d(&f.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM, o.op.lda)) return rc;
       if (o.b_tiled || o.op.b_layout == 2) {
-        f.b_kmajor = 1;
+        f.d.b_kmajor = 1;
         const void* wb = o.b_tiled ? static_cast<const void*>(o.b_tiled) : reinterpret_cast<const void*>(o.op.b);
         if (int rc = encode_kblock_major(&f.tma_b, wb, o.op.n, o.op.k, kFusedBN)) return rc;
       } else {
         if (int rc = encode_2d(&f.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, kFusedBN)) return rc;
       }
-      if (cs > 1) {  // slices reduced inside the cluster: one phase (output ready)
-        f.mma_phase = -1;
-        f.ready_phase = np++;
+      if (cs > 1 && split > 1) {  // slices reduced inside the cluster: one phase (output ready)
+        f.d.mma_phase = -1;
+        f.d.ready_phase = np++;
       } else {
         if (split > 1) {
-          MS_CUDA(cudaMalloc(&f.ws, sizeof(float) * static_cast<size_t>(split) * f.m * f.n));
-          ch.fused_ws.push_back(f.ws);
+          MS_CUDA(cudaMalloc(&f.d.ws, sizeof(float) * static_cast<size_t>(split) * f.d.m * f.d.n));
+          ch.fused_ws.push_back(f.d.ws);
         }
-        f.mma_phase = np++;
-        f.ready_phase = split > 1 ? np++ : f.mma_phase;
+        f.d.mma_phase = np++;
+        f.d.ready_phase = split > 1 ? np++ : f.d.mma_phase;
       }
     } else {
-      f.kind = o.op.kind == MS_HP_SILU_MUL ? kFusedSiluMul : kFusedBiasGelu;
-      f.x = reinterpret_cast<const __nv_bfloat16*>(o.op.a);
-      f.bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
-      f.mma_phase = -1;
-      f.ready_phase = np++;
+      f.d.kind = o.op.kind == MS_HP_SILU_MUL ? kFusedSiluMul : kFusedBiasGelu;
+      f.d.x = reinterpret_cast<const __nv_bfloat16*>(o.op.a);
+      f.d.bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
+      f.d.mma_phase = -1;
+      f.d.ready_phase = np++;
       if (!any_gemm) {
         const long long chunks = o.op.m * o.op.n / 8;
-        grid = std::max<int>(grid, static_cast<int>(std::min<long long>((chunks + 127) / 128, sms)));
+        grid = std::max<int>(grid, static_cast<int>(std::min<long long>((chunks + 127) / 128, max_grid)));
       }
     }
   }
-  if (cs > 1) grid = max_units;
+  if (cs > 1) grid = max_units;  // a multiple of the cluster size
   ch.fused_cs = cs;
   prog.n_phases = np;
-  prog.l2_prefetch = getenv("MS_FUSED_NO_PREFETCH") ? 0 : 1;
+  // L2 prefetch of the next op's weights: measured +2% on cluster launches (config-1 chain
+  // 59.7 vs 60.9 us) but -11% on long non-cluster chains (config-4 step 1.03 vs 0.92 ms: the
+  // prefetch backlog delays the grid phases' own loads and fences).
+  prog.l2_prefetch = cs > 1 && !getenv("MS_FUSED_NO_PREFETCH");
   MS_CUDA(cudaMalloc(&ch.prog_d, sizeof(FusedProgram)));
   MS_CUDA(cudaMemcpy(ch.prog_d, &prog, sizeof(FusedProgram), cudaMemcpyHostToDevice));
   MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * std::max(np, 1)));
   MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * std::max(np, 1)));
   ch.fused_ctl = d->next_hp_ctl++;
   if (ch.fused_ctl >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
+  ch.descs.clear();
+  for (int i = 0; i < prog.n_ops; ++i) ch.descs.push_back(prog.ops[i].d);
+  ch.l2_prefetch = prog.l2_prefetch;
   ch.fused_first = first;
   ch.fused_last = last;
   ch.fused_grid = grid;
@@ -483,6 +542,9 @@ int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool 
   p.run.n_reset = ch.n_phases;
   p.prog = ch.prog_d;
   p.phase_cnt = ch.phase_d;
+  p.n_ops = static_cast<int>(ch.descs.size());
+  p.l2_prefetch = ch.l2_prefetch;
+  for (size_t i = 0; i < ch.descs.size(); ++i) p.ops[i] = ch.descs[i];
   switch (ch.fused_cs) {
     case 4:
       MS_CUDA(launch_kc(hp_fused_kernel<4>, ch.fused_grid, 256, FusedCfg<4>::kSmemBytes, d->hp, pdl, 4, p));

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) bias_gelu_kernel(const __grid_constant__ 
 }
 
 // SwiGLU activation of a decode layer: out[r, j] = silu(x[r, j]) * x[r, cols + j], x = [rows x 2 cols].
-__device__ __forceinline__ float silu_mul(float g, float u) { return g / (1.0f + __expf(-g)) * u; }
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
 
 __global__ void __launch_bounds__(256) silu_mul_kernel(const __grid_constant__ BiasGeluParams p) {
   __shared__ long long tile_sh;

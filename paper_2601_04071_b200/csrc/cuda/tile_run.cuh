@@ -51,7 +51,7 @@ __device__ __forceinline__ void dbg_stamp(const TileRun& r, int phase) {
 
 // Extended per-CTA stamps (64 slots per CTA after the [gridDim][8] block).
 __device__ __forceinline__ void dbg_stamp_ext(const TileRun& r, int slot) {
-  if (r.dbg) r.dbg[2048 + blockIdx.x * 64 + slot] = globaltimer();
+  if (r.dbg && slot < 64) r.dbg[2048 + blockIdx.x * 64 + slot] = globaltimer();
 }
 
 __device__ __forceinline__ unsigned long long current_budget(const TileRun& r) {

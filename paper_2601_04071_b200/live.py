@@ -3,8 +3,8 @@
 Python only allocates the tenants' synthetic tensors, registers the sm_100a kernels,
 and hands the scenario + bindings to ms_live_run, which runs Algorithm 1 in C++ on
 this thread in real time.  Policies: splitkernel (this system), exclusive (HP alone ->
-SLO), exclusive_lp (LP alone -> LP throughput reference), reef (kernel-boundary
-temporal sharing baseline).
+SLO), exclusive_lp (LP alone -> LP throughput reference), reef / reef_req
+(kernel-boundary temporal sharing baselines).
 """
 from __future__ import annotations
 
@@ -106,5 +106,100 @@ class Config1:
 
     def options(self, **kw) -> dict:
         o = {"tile_ns": {"lp_gemm_8192": (self.calib or {}).get("lp_gemm_tile_ns", 57000)}, "timeline": True}
+        o.update(kw)
+        return o
+
+
+def decode_step_ops(M: int, H: int, Q: int, F: int, V: int, layers: int, bufs, weights, lm) -> list[dict]:
+    """HP chain of one synthetic Llama-style decode step (config 4): per layer
+    qkv = h Wqkv^T, o = qkv[:, :H] Wo^T (strided A: the attention core is not modelled),
+    gu = o Wgu^T, act = silu(gu[:, :F]) * gu[:, F:], h = act Wd^T; then logits = h Wlm^T.
+    `bufs` = (h, qkv, o, gu, act, logits) device pointers; `weights[l]` = (Wqkv, Wo, Wgu, Wd)."""
+    h, qkv, o, gu, act, logits = bufs
+    ops = []
+    for l in range(layers):
+        wq, wo, wg, wd = weights[l]
+        ops += [dict(kind=1, block_n=128, a=h, b=wq, c=qkv, bias=0, m=M, n=Q, k=H),
+                dict(kind=1, block_n=128, a=qkv, b=wo, c=o, bias=0, m=M, n=H, k=H, lda=Q),
+                dict(kind=1, block_n=128, a=o, b=wg, c=gu, bias=0, m=M, n=2 * F, k=H),
+                dict(kind=5, block_n=0, a=gu, b=0, c=act, bias=0, m=M, n=F, k=0),
+                dict(kind=1, block_n=128, a=act, b=wd, c=h, bias=0, m=M, n=H, k=F)]
+    ops.append(dict(kind=1, block_n=128, a=h, b=lm, c=logits, bias=0, m=M, n=V, k=H))
+    return ops
+
+
+class Config4:
+    """Config 4 tenants on one B200.  HP = one decode step of a Llama-3.2-1B-geometry model
+    (hidden 2048, qkv 3072, FFN 8192, 16 layers, vocab 128256: 1.24 B parameters = 2.47 GB of
+    bf16 weights streamed per token); the bs=1 token rides in row 0 of the 128-row UMMA
+    tile (weights dominate the bytes; compute stays under the HBM time).  LP1 = bf16
+    8192^3 GEMM loop, LP2 = bf16 axpy over 2^30 elements (6 GiB of HBM traffic per pass)."""
+
+    M, H, Q, F, V, LAYERS = 128, 2048, 3072, 8192, 128256, 16
+    N_LP = 8192
+    N_EW = 1 << 30
+
+    def __init__(self, dev: Device, seed: int = SEED):
+        self.dev = dev
+        M, H, Q, F, V = self.M, self.H, self.Q, self.F, self.V
+        self.bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
+        dev.fill_synth(self.bufs[0], M * H, seed, 400, 1.0)
+        self.weights = []
+        for l in range(self.LAYERS):
+            ws = []
+            for j, (n, k) in enumerate([(Q, H), (H, H), (2 * F, H), (H, F)]):
+                p = dev.alloc(n * k * 2)
+                dev.fill_synth(p, n * k, seed, 401 + 4 * l + j, 1.0 / math.sqrt(k))
+                ws.append(p)
+            self.weights.append(ws)
+        self.lm = dev.alloc(V * H * 2)
+        dev.fill_synth(self.lm, V * H, seed, 499, 1.0 / math.sqrt(H))
+        self.chain = dev.hp_register_chain(decode_step_ops(M, H, Q, F, V, self.LAYERS, self.bufs,
+                                                           self.weights, self.lm))
+        n = self.N_LP
+        self.a, self.b, self.c = dev.alloc(n * n * 2), dev.alloc(n * n * 2), dev.alloc(n * n * 2)
+        dev.fill_synth(self.a, n * n, seed, 1, 1.0)
+        dev.fill_synth(self.b, n * n, seed, 2, 1.0 / math.sqrt(n))
+        self.lp_gemm = dev.lp_register_gemm(self.a, self.b, self.c, n, n, n, block_n=256)
+        self.x, self.y = dev.alloc(self.N_EW * 2), dev.alloc(self.N_EW * 2)
+        dev.fill_synth(self.x, self.N_EW, seed, 21, 1.0)
+        dev.fill_synth(self.y, self.N_EW, seed, 22, 1.0)
+        self.lp_axpy = dev.lp_register_axpy(self.x, self.y, self.N_EW, 0.5)
+        self.calib = None
+
+    @property
+    def weight_bytes(self) -> int:
+        H, Q, F, V = self.H, self.Q, self.F, self.V
+        return 2 * (self.LAYERS * (Q * H + H * H + 2 * F * H + H * F) + V * H)
+
+    def binding(self) -> dict:
+        return {"lp": {"lp_gemm_8192": self.lp_gemm.id, "lp_axpy_1g": self.lp_axpy.id},
+                "hp": {"hp_decode": [self.chain]}}
+
+    def calibrate(self, reps: int = 3) -> dict:
+        sm = self.dev.info["sm_count"]
+        ms_gemm = self.dev.lp_time_full(self.lp_gemm, reps)
+        ms_axpy = self.dev.lp_time_full(self.lp_axpy, reps)
+        ms_chain = self.dev.hp_time_chain(self.chain, 5)
+        self.calib = {
+            "lp_gemm_ms": ms_gemm, "lp_axpy_ms": ms_axpy, "hp_step_ms": ms_chain,
+            "hp_weight_gbs": self.weight_bytes / (ms_chain * 1e-3) / 1e9,
+            "lp_gemm_tile_ns": int(ms_gemm * 1e6 / math.ceil(self.lp_gemm.total_tiles / sm)),
+            # one "tile" of the pacing model = one tile per SM per wave
+            "lp_ew_tile_ns": int(ms_axpy * 1e6 / math.ceil(self.lp_axpy.total_tiles / sm)),
+            "lp_ew_tiles": int(self.lp_axpy.total_tiles),
+            "lp_ew_tile_bytes": 6 * 8192,
+            "hp_layer_ns": int(ms_chain * 1e6 * 0.79 / self.LAYERS),
+            "hp_lm_head_ns": int(ms_chain * 1e6 * 0.21),
+        }
+        return self.calib
+
+    def scenario(self, seed: int, horizon_s: float) -> dict:
+        return scenarios.config4(seed=seed, horizon_s=horizon_s, calib=self.calib or {})
+
+    def options(self, **kw) -> dict:
+        c = self.calib or {}
+        o = {"tile_ns": {"lp_gemm_8192": c.get("lp_gemm_tile_ns", 57000),
+                         "lp_axpy_1g": c.get("lp_ew_tile_ns", 4000)}, "timeline": True}
         o.update(kw)
         return o

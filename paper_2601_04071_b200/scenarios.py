@@ -88,10 +88,10 @@ def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None) -
         "horizon": _dur(int(horizon_s * 1e9)),
         "gpu": gpu_b200(c),
         "kernels": [
-            _kernel("hp_decode_layer", 148, 20_000, 148 * 1024 * 1024 // 148, False),
-            _kernel("hp_lm_head", 148, 40_000, 2048 * 128256 * 2 // 148, False),
+            _kernel("hp_decode_layer", 148, c.get("hp_layer_ns", 20_000), 148 * 1024 * 1024 // 148, False),
+            _kernel("hp_lm_head", 148, c.get("hp_lm_head_ns", 40_000), 2048 * 128256 * 2 // 148, False),
             _kernel("lp_gemm_8192", 2048, c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"]),
-            _kernel("lp_axpy_1g", 16384, c["lp_ew_tile_ns"], c["lp_ew_tile_bytes"], per_sm=4),
+            _kernel("lp_axpy_1g", c.get("lp_ew_tiles", 16384), c["lp_ew_tile_ns"], c["lp_ew_tile_bytes"], per_sm=4),
         ],
         "tasks": [
             {"name": "hp_decode", "priority": "high", "kind": "serving", "trace": "hp_trace",

@@ -179,23 +179,6 @@ def test_hp_gemm_split_k_matches_oracle(dev, T, split):
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
 
 
-def decode_chain_ops(M, H, Q, F, V, layers, bufs, ws, lm):
-    """Synthetic Llama-style decode step (config 4): per layer qkv = h Wqkv^T, o = qkv[:, :H] Wo^T
-    (strided A), gu = o Wgu^T, act = silu(gu[:, :F]) * gu[:, F:], h = act Wd^T; then logits = h Wlm^T."""
-    h, qkv, o, gu, act, logits = bufs
-    ops = []
-    for l in range(layers):
-        wq, wo, wg, wd = ws[l]
-        src = h
-        ops += [dict(kind=1, block_n=128, a=src, b=wq, c=qkv, bias=0, m=M, n=Q, k=H),
-                dict(kind=1, block_n=128, a=qkv, b=wo, c=o, bias=0, m=M, n=H, k=H, lda=Q),
-                dict(kind=1, block_n=128, a=o, b=wg, c=gu, bias=0, m=M, n=2 * F, k=H),
-                dict(kind=5, block_n=0, a=gu, b=0, c=act, bias=0, m=M, n=F, k=0),
-                dict(kind=1, block_n=128, a=act, b=wd, c=h, bias=0, m=M, n=H, k=F)]
-    ops.append(dict(kind=1, block_n=128, a=h, b=lm, c=logits, bias=0, m=M, n=V, k=H))
-    return ops
-
-
 @pytest.mark.parametrize("fused", [1, 2, 0])
 def test_hp_decode_chain_matches_oracle(dev, T, fused):
     """Config-4 HP step (2 layers + LM head, small geometry) incl. strided A and SILU_MUL,
@@ -219,7 +202,8 @@ def test_hp_decode_chain_matches_oracle(dev, T, fused):
     lm = dev.alloc(V * H * 2)
     dev.fill_synth(lm, V * H, SEED, 399, s(H))
     dev.fill_synth(bufs[0], M * H, SEED, 298, 1.0)
-    chain = dev.hp_register_chain(decode_chain_ops(M, H, Q, F, V, L, bufs, ws, lm))
+    from paper_2601_04071_b200.live import decode_step_ops
+    chain = dev.hp_register_chain(decode_step_ops(M, H, Q, F, V, L, bufs, ws, lm))
     dev.hp_launch_direct(chain, dev.hp_next_seq())
     dev.sync()
 

@@ -28,3 +28,20 @@ def test_live_config1_short():
     e2e = live_run(dev, sc, "splitkernel", w.binding(e2e=True), w.options())
     assert e2e["hp_chains"] > 0 and e2e["requests"]["completed"] > 0
     dev.close()
+
+
+def test_live_config4_short():
+    """Config 4 live: Llama-geometry decode HP (81-op fused chain) + two LP tenants (GEMM loop
+    and HBM streamer) round-robined into the HP gaps."""
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config4, live_run
+    dev = Device(0)
+    w = Config4(dev)
+    c = w.calibrate(reps=1)
+    assert c["hp_weight_gbs"] > 1000  # 2.47 GB of weights per step streamed from HBM
+    sc = w.scenario(seed=5, horizon_s=0.5)
+    sk = live_run(dev, sc, "splitkernel", w.binding(), w.options())
+    assert sk["requests"]["n"] >= 1 and sk["hp_chains"] > 10
+    assert sk["lp"]["tiles_done"] > 0 and sk["lp"]["preemptions"] > 0
+    assert 0 < sk["preempt_ring_to_first_hp_cta"]["p50_ns"] < 200_000
+    dev.close()
