@@ -139,6 +139,8 @@ uint32_t ms_preempt_epoch(ms_dev* dev);
 #define MS_HP_GEMM 1      /* C = A * B^T (non-preemptible tcgen05 GEMM) */
 #define MS_HP_BIAS_GELU 2 /* c = gelu(a + bias) over m x n */
 #define MS_HP_SILU_MUL 5  /* c[m, n] = silu(a[m, j]) * a[m, n + j]: a is [m x 2n] = [gate | up] */
+#define MS_HP_GEMM_SWIGLU 6 /* c[m, n] = silu(a b_gate^T) * (a b_up^T); b = [2n x k] = [gate rows; up
+                               rows] (row-major); the SwiGLU is applied to the fp32 accumulators */
 #define MS_HP_H2D 3       /* copy m bytes: pinned host a -> device c (e2e request input) */
 #define MS_HP_D2H 4       /* copy m bytes: device a -> pinned host c (e2e request output) */
 

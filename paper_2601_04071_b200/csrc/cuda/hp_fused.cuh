@@ -35,6 +35,7 @@ struct FusedOpDesc {
   int m, n, k;
   int tiles_m, tiles_n, split, kb_per_unit, units;
   int b_kmajor;
+  int swiglu;       // GEMM whose 128-column tiles hold [64 gate | 64 up] features (n = output cols)
   int in_phase;     // phase whose completion makes this op's input readable (-1: chain input)
   int mma_phase;    // GEMM: every unit's epilogue done (C or partials written)
   int ready_phase;  // output complete
@@ -547,12 +548,34 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
           int mb, nb, kb0;
           fused_unit_coords(o, u, mb, nb, kb0);
           const int row_in_tile = q * 32 + lane;
+          const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * BN);
+          if (o.swiglu) {
+            // columns [0, 64) = gate, [64, 128) = up of output features [64 nb, 64 nb + 64)
+            __nv_bfloat16* crow = o.c + static_cast<size_t>(mb * kBM + row_in_tile) * o.n + static_cast<size_t>(nb) * 64;
+#pragma unroll 1
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+              uint32_t g[32], u[32];
+              tmem_ld_32x32b_x32(trow + c0, g);
+              tmem_ld_32x32b_x32(trow + 64 + c0, u);
+              tmem_ld_wait();
+              uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  w[e] = pack_bf16x2(silu_mul(__uint_as_float(g[8 * v + 2 * e]), __uint_as_float(u[8 * v + 2 * e])),
+                                     silu_mul(__uint_as_float(g[8 * v + 2 * e + 1]), __uint_as_float(u[8 * v + 2 * e + 1])));
+                dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+              }
+            }
+          } else {
           __nv_bfloat16* crow = o.c + static_cast<size_t>(mb * kBM + row_in_tile) * o.n + static_cast<size_t>(nb) * BN;
           float4* wunit = o.split > 1 ? reinterpret_cast<float4*>(o.ws) + static_cast<size_t>(u) * (kBM * BN / 4) : nullptr;
 #pragma unroll 1
           for (int c0 = 0; c0 < BN; c0 += 32) {
             uint32_t r[32];
-            tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * BN + c0), r);
+            tmem_ld_32x32b_x32(trow + c0, r);
             tmem_ld_wait();
             if (CS == 1 && o.split > 1) {  // (cluster launches reduce k-slices in DSMEM)
 #pragma unroll
@@ -572,6 +595,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
                 dst[v] = w;
               }
             }
+          }
           }
           tc_fence_before();
           asm volatile("bar.sync 1, 128;" ::: "memory");

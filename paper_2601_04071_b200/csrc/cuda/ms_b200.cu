@@ -131,6 +131,8 @@ struct HpOpRt {
   unsigned int* tile_cnt = nullptr;
   __nv_bfloat16* b_tiled = nullptr;  // k-block-major copy of the weights (captured at registration)
   int reduce_ctl_index = 0;          // control block of the split-K reduce kernel
+  __nv_bfloat16* tmp = nullptr;      // GEMM_SWIGLU per-op path: [m x 2n] gate|up before the SwiGLU
+  int act_ctl_index = 0;             // GEMM_SWIGLU per-op path: control block of the SwiGLU kernel
 };
 
 struct HpChain {
@@ -284,6 +286,42 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   // the chain's first kernel does not depend on the gate's output, later ones wait.
   const bool prev_is_kernel = i > 0 ? !is_copy(ch.ops[i - 1].op) : after_gate;
   r.pdl_wait = i > 0 && prev_is_kernel;
+  if (o.op.kind == MS_HP_GEMM_SWIGLU) {
+    // GEMM into tmp ([gate | up] halves), then the SwiGLU kernel (PDL) writes c.
+    const bool last = r.hp_last;
+    GemmParams p{};
+    p.run = r;
+    p.run.hp_last = 0;
+    p.run.begin = 0;
+    p.run.end = p.run.budget0 = static_cast<unsigned long long>(o.tiles_m) * o.tiles_n;
+    p.split_k = 1;
+    p.m = static_cast<int>(o.op.m);
+    p.n = static_cast<int>(2 * o.op.n);
+    p.k = static_cast<int>(o.op.k);
+    p.tiles_m = o.tiles_m;
+    p.tiles_n = o.tiles_n;
+    p.group_m = 16;
+    p.c = o.tmp;
+    const int grid = static_cast<int>(std::min<uint64_t>(p.run.end, d->prop.multiProcessorCount));
+    if (int rc = launch_gemm(d, 128, o.tma_a, o.tma_b, o.tma_c, p, grid, d->hp, prev_is_kernel)) return rc;
+    BiasGeluParams q{};
+    q.run = base_run(d, o.act_ctl_index);
+    q.run.hp_ctl = r.hp_ctl;
+    q.run.hp_rec = r.hp_rec;
+    q.run.hp_last = last;
+    q.run.hp_seq = seq;
+    q.run.pdl_wait = 1;
+    q.run.dbg = d->dbg;
+    q.run.begin = 0;
+    q.run.end = q.run.budget0 = static_cast<unsigned long long>(o.op.m);
+    q.x = o.tmp;
+    q.out = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+    q.rows = static_cast<int>(o.op.m);
+    q.cols = static_cast<int>(o.op.n);
+    const int qgrid = static_cast<int>(std::min<int64_t>(o.op.m, d->prop.multiProcessorCount));
+    MS_CUDA(launch_k(silu_mul_kernel, qgrid, 256, 0, d->hp, true, q));
+    return 0;
+  }
   if (o.op.kind == MS_HP_GEMM) {
     GemmParams p{};
     p.run = r;
@@ -358,6 +396,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
     const ms_hp_op& op = ch.ops[i].op;
     if (is_copy(op)) return 0;  // copies between kernels: keep per-op launches
     if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % kFusedBN || op.k % kBK)) return 0;
+    if (op.kind == MS_HP_GEMM_SWIGLU && (op.m % kBM || op.n % 64 || op.k % kBK)) return 0;
     if ((op.kind == MS_HP_BIAS_GELU || op.kind == MS_HP_SILU_MUL) && op.n % 8) return 0;
   }
   const int sms = d->prop.multiProcessorCount;
@@ -373,6 +412,9 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   std::vector<GemmShape> gemms;
   for (int i = first; i <= last; ++i) {
     const ms_hp_op& op = ch.ops[i].op;
+    if (op.kind == MS_HP_GEMM_SWIGLU)  // SwiGLU epilogue needs whole k: split 1
+      gemms.push_back({i - first, static_cast<int>(op.m / kBM) * static_cast<int>(2 * op.n / kFusedBN),
+                       static_cast<int>(op.k / kBK), 1});
     if (op.kind != MS_HP_GEMM) continue;
     gemms.push_back({i - first, static_cast<int>(op.m / kBM) * static_cast<int>(op.n / kFusedBN),
                      static_cast<int>(op.k / kBK), op.split_k});
@@ -466,10 +508,11 @@ int plan_fused(ms_dev* d, HpChain& ch) {
     f.d.k = static_cast<int>(o.op.k);
     f.d.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
     f.d.in_phase = i > first ? prog.ops[i - first - 1].d.ready_phase : -1;
-    if (o.op.kind == MS_HP_GEMM) {
+    if (o.op.kind == MS_HP_GEMM || o.op.kind == MS_HP_GEMM_SWIGLU) {
       f.d.kind = kFusedGemm;
+      f.d.swiglu = o.op.kind == MS_HP_GEMM_SWIGLU;
       f.d.tiles_m = f.d.m / kBM;
-      f.d.tiles_n = f.d.n / kFusedBN;
+      f.d.tiles_n = (f.d.swiglu ? 2 * f.d.n : f.d.n) / kFusedBN;
       const int split = splits[i - first];
       f.d.split = split;
       f.d.kb_per_unit = f.d.k / kBK / split;
@@ -478,7 +521,8 @@ int plan_fused(ms_dev* d, HpChain& ch) {
       if (o.b_tiled || o.op.b_layout == 2) {
         f.d.b_kmajor = 1;
         const void* wb = o.b_tiled ? static_cast<const void*>(o.b_tiled) : reinterpret_cast<const void*>(o.op.b);
-        if (int rc = encode_kblock_major(&f.tma_b, wb, o.op.n, o.op.k, kFusedBN)) return rc;
+        const uint64_t bn_rows = f.d.swiglu ? 2 * o.op.n : o.op.n;
+        if (int rc = encode_kblock_major(&f.tma_b, wb, bn_rows, o.op.k, kFusedBN)) return rc;
       } else {
         if (int rc = encode_2d(&f.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, kFusedBN)) return rc;
       }
@@ -974,6 +1018,26 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
         }
         if (int rc = encode_kblock_major(&o.tma_b, wb, o.op.n, o.op.k, bn)) return rc;
       }
+    } else if (o.op.kind == MS_HP_GEMM_SWIGLU) {
+      // per-op path: GEMM over the row-major [gate; up] weights into tmp, then SwiGLU kernel;
+      // fused path: interleaved k-block-major copy, SwiGLU in the GEMM epilogue.
+      if (o.op.m % kBM || o.op.n % 64 || o.op.k % kBK) return fail(MS_E_ARG, "HP GEMM_SWIGLU shape");
+      if (o.op.lda && (o.op.lda < o.op.k || o.op.lda % 8)) return fail(MS_E_ARG, "lda must be >= k and a multiple of 8");
+      o.op.block_n = 128;
+      o.tiles_m = static_cast<int>(o.op.m / kBM);
+      o.tiles_n = static_cast<int>(2 * o.op.n / 128);
+      o.split = 1;
+      o.act_ctl_index = d->next_hp_ctl++;
+      if (o.act_ctl_index >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
+      MS_CUDA(cudaMalloc(&o.tmp, static_cast<size_t>(o.op.m) * 2 * o.op.n * 2));
+      if (int rc = encode_2d(&o.tma_a, reinterpret_cast<void*>(o.op.a), o.op.m, o.op.k, kBM, o.op.lda)) return rc;
+      if (int rc = encode_c(&o.tma_c, o.tmp, o.op.m, 2 * o.op.n)) return rc;
+      if (int rc = encode_2d(&o.tma_b, reinterpret_cast<void*>(o.op.b), 2 * o.op.n, o.op.k, 128)) return rc;
+      MS_CUDA(cudaMalloc(&o.b_tiled, static_cast<size_t>(2 * o.op.n) * o.op.k * 2));
+      kblock_major_swiglu_kernel<<<d->prop.multiProcessorCount * 4, 256, 0, d->aux>>>(
+          reinterpret_cast<const __nv_bfloat16*>(o.op.b), o.b_tiled, o.op.n, o.op.k);
+      MS_CUDA(cudaGetLastError());
+      MS_CUDA(cudaStreamSynchronize(d->aux));
     } else if (o.op.kind == MS_HP_BIAS_GELU || o.op.kind == MS_HP_SILU_MUL) {
       if (o.op.n % 8) return fail(MS_E_ARG, "elementwise cols must be a multiple of 8");
     } else if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
@@ -998,6 +1062,7 @@ int ms_hp_unregister_chain(ms_dev* d, int cid) {
     if (o.ws) cudaFree(o.ws);
     if (o.tile_cnt) cudaFree(o.tile_cnt);
     if (o.b_tiled) cudaFree(o.b_tiled);
+    if (o.tmp) cudaFree(o.tmp);
   }
   for (float* w : ch.fused_ws) cudaFree(w);
   if (ch.prog_d) cudaFree(ch.prog_d);
@@ -1025,7 +1090,7 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   if (!ch.used) return fail(MS_E_ARG, "bad chain");
   // 40 KB of (unused) shared memory keeps a 193 KB LP GEMM CTA off the gate's SM: an LP
   // CTA co-resident with the spinning gate observed preemptions ~5 us late.
-  gate_kernel<<<1, 32, kGateSmem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
+  gate_kernel<<<1, 32 * kGateWarps, kGateSmem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
   return launch_chain(d, cid, ch, seq, true);
 }

@@ -211,22 +211,39 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(const __grid_constant__ B
 // no launch needed) first pushes the preempt epoch into the device mirror — every LP CTA
 // sees it on its next L2 poll, without waiting for the LP leader's own PCIe round trip —
 // then lets the PDL-launched chain kernel be scheduled.
+// Four pollers (lane 0 of warps 0-3), started ~150 ns apart, so a PCIe read reaches the
+// host page every ~RTT/4 instead of every RTT: the doorbell is seen sooner after it lands.
+constexpr int kGateWarps = 4;
+
 __global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpRecord* rec, MsDevMirror* mirror) {
-  if (threadIdx.x != 0) return;
-  // Relaxed polling: the doorbell value itself is the only datum consumed.
-  uint64_t v;
-  for (;;) {
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(doorbell) : "memory");
-    if (static_cast<int>(static_cast<uint32_t>(v) - seq) >= 0) break;
-    __nanosleep(64);
-  }
-  const uint32_t epoch = static_cast<uint32_t>(v >> 32);
+  __shared__ uint32_t rung;
+  __shared__ uint64_t word;
+  if (threadIdx.x == 0) rung = 0;
+  __syncthreads();
+  const int warp = threadIdx.x / 32;
+  if ((threadIdx.x & 31) == 0) {
+    __nanosleep(150 * warp);
+    // Relaxed polling: the doorbell value itself is the only datum consumed.
+    for (;;) {
+      if (ld_volatile_smem(&rung)) break;
+      uint64_t v;
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(doorbell) : "memory");
+      if (static_cast<int>(static_cast<uint32_t>(v) - seq) >= 0) {
+        if (atomicExch(&rung, 1u) == 0) {
+          word = v;
+          const uint32_t epoch = static_cast<uint32_t>(v >> 32);
 #pragma unroll
-  for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&mirror->epoch[c * MS_MIRROR_STRIDE], epoch);
-  pdl_launch_dependents();
-  const unsigned long long t = globaltimer();
-  st_relaxed_sys_u64(&rec->t_gate, t);
-  st_release_sys_u32(&rec->seq_gate, seq);
+          for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&mirror->epoch[c * MS_MIRROR_STRIDE], epoch);
+          pdl_launch_dependents();
+          const unsigned long long t = globaltimer();
+          st_relaxed_sys_u64(&rec->t_gate, t);
+          st_release_sys_u32(&rec->seq_gate, seq);
+        }
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
 }
 
 // Completion record of a chain whose last op is a copy (e2e mode): written after the D2H.
@@ -281,6 +298,25 @@ __global__ void kblock_major_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst
     const unsigned long long kb = k8 / 8;
     const unsigned long long kin = (k8 & 7) * 8;
     *reinterpret_cast<uint4*>(dst + (kb * n + row) * 64 + kin) = *reinterpret_cast<const uint4*>(src + row * k + k8 * 8);
+  }
+}
+
+// SwiGLU weights [2F][K] (gate rows, then up rows) -> k-block-major [K/64][2F][64] with the
+// rows interleaved in 64-row blocks: block t = gate rows [64t, 64t + 64) then up rows
+// [64t, 64t + 64), so one 128-column GEMM tile holds the gate and up halves of 64 features.
+__global__ void kblock_major_swiglu_kernel(const __nv_bfloat16* src, __nv_bfloat16* dst, unsigned long long f,
+                                           unsigned long long k) {
+  const unsigned long long n = 2 * f;
+  const unsigned long long vecs = n * k / 8;
+  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < vecs;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long row = i / (k / 8);  // interleaved row
+    const unsigned long long k8 = i - row * (k / 8);
+    const unsigned long long t = row / 128, w = row % 128;
+    const unsigned long long srow = w < 64 ? 64 * t + w : f + 64 * t + (w - 64);
+    const unsigned long long kb = k8 / 8;
+    const unsigned long long kin = (k8 & 7) * 8;
+    *reinterpret_cast<uint4*>(dst + (kb * n + row) * 64 + kin) = *reinterpret_cast<const uint4*>(src + srow * k + k8 * 8);
   }
 }
 

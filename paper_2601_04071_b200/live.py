@@ -113,16 +113,16 @@ class Config1:
 def decode_step_ops(M: int, H: int, Q: int, F: int, V: int, layers: int, bufs, weights, lm) -> list[dict]:
     """HP chain of one synthetic Llama-style decode step (config 4): per layer
     qkv = h Wqkv^T, o = qkv[:, :H] Wo^T (strided A: the attention core is not modelled),
-    gu = o Wgu^T, act = silu(gu[:, :F]) * gu[:, F:], h = act Wd^T; then logits = h Wlm^T.
-    `bufs` = (h, qkv, o, gu, act, logits) device pointers; `weights[l]` = (Wqkv, Wo, Wgu, Wd)."""
+    act = silu(o Wg^T) * (o Wu^T) (one GEMM_SWIGLU op, Wgu = [Wg; Wu]), h = act Wd^T; then
+    logits = h Wlm^T.  `bufs` = (h, qkv, o, gu, act, logits) device pointers (gu unused by
+    the fused SwiGLU); `weights[l]` = (Wqkv, Wo, Wgu, Wd)."""
     h, qkv, o, gu, act, logits = bufs
     ops = []
     for l in range(layers):
         wq, wo, wg, wd = weights[l]
         ops += [dict(kind=1, block_n=128, a=h, b=wq, c=qkv, bias=0, m=M, n=Q, k=H),
                 dict(kind=1, block_n=128, a=qkv, b=wo, c=o, bias=0, m=M, n=H, k=H, lda=Q),
-                dict(kind=1, block_n=128, a=o, b=wg, c=gu, bias=0, m=M, n=2 * F, k=H),
-                dict(kind=5, block_n=0, a=gu, b=0, c=act, bias=0, m=M, n=F, k=0),
+                dict(kind=6, block_n=128, a=o, b=wg, c=act, bias=0, m=M, n=F, k=H),
                 dict(kind=1, block_n=128, a=act, b=wd, c=h, bias=0, m=M, n=H, k=F)]
     ops.append(dict(kind=1, block_n=128, a=h, b=lm, c=logits, bias=0, m=M, n=V, k=H))
     return ops
@@ -194,8 +194,16 @@ class Config4:
         }
         return self.calib
 
-    def scenario(self, seed: int, horizon_s: float) -> dict:
-        return scenarios.config4(seed=seed, horizon_s=horizon_s, calib=self.calib or {})
+    def hp_rate(self, utilisation: float = 0.5) -> float:
+        """Request rate giving the HP tenant `utilisation` of the GPU on its own.  At the
+        specified 20 req/s the HP tenant alone is overloaded on B200 (2.47 GB of weights per
+        token, 80 tokens per request on average, plus 0.3 ms of CPU gap per token)."""
+        step_s = (self.calib or {}).get("hp_step_ms", 1.0) * 1e-3
+        return utilisation / (80.0 * (step_s + 300e-6))
+
+    def scenario(self, seed: int, horizon_s: float, rate: float | None = None) -> dict:
+        return scenarios.config4(seed=seed, horizon_s=horizon_s, calib=self.calib or {},
+                                 rate=rate if rate is not None else self.hp_rate())
 
     def options(self, **kw) -> dict:
         c = self.calib or {}

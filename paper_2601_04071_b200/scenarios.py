@@ -79,7 +79,7 @@ def config1(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
     }
 
 
-def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None) -> dict:
+def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, rate: float = 20.0) -> dict:
     """Config 4: Llama-style 1B decode HP (bs=1) + LP GEMM training + LP HBM streamer."""
     c = dict(DEFAULT_CALIB, **(calib or {}))
     sc = {
@@ -102,7 +102,7 @@ def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None) -
             {"name": "lp_gemm", "priority": "low", "kind": "batch", "kernels": [{"kernel": "lp_gemm_8192"}]},
             {"name": "lp_stream", "priority": "low", "kind": "batch", "kernels": [{"kernel": "lp_axpy_1g"}]},
         ],
-        "traces": [{"name": "hp_trace", "bursty": {"rate": 20.0, "burstiness": 1.0},
+        "traces": [{"name": "hp_trace", "bursty": {"rate": rate, "burstiness": 1.0},
                     "iterations": {"dist": "uniform", "lo": 32, "hi": 128}}],
     }
     return sc

@@ -129,6 +129,24 @@ def test_hp_chain_matches_oracle(dev, T, fused):
     dev.hp_set_fused(True)
 
 
+def test_hp_silu_mul_matches_oracle(dev, T):
+    """Standalone SILU_MUL op (fused and per-op): out = silu(gate) * up over [M x 2N]."""
+    M, N = 256, 1024
+    x, out = dev.alloc(M * 2 * N * 2), dev.alloc(M * N * 2)
+    dev.fill_synth(x, M * 2 * N, SEED, 41, 2.0)
+    want = T.bf16_to_f32(T.silu_mul(T.synth_bf16(M * 2 * N, SEED, 41, 2.0), M, N))
+    for fused in (1, 0):
+        dev.hp_set_fused(fused)
+        dev.memset(out, 0, M * N * 2)
+        ch = dev.hp_register_chain([dict(kind=5, block_n=0, a=x, b=0, c=out, bias=0, m=M, n=N, k=0)])
+        dev.hp_launch_direct(ch, dev.hp_next_seq())
+        dev.sync()
+        got = T.bf16_to_f32(d2h(dev, out, M * N))
+        assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+        dev.hp_unregister_chain(ch)
+    dev.hp_set_fused(1)
+
+
 def test_hp_chain_fused_equals_per_op(dev, T):
     """Per-op kernels, the cluster (DSMEM) fused launch and the global-reduction fused
     launch use the same tiles, k-slices and slice-order sums: config-1-size chains agree
@@ -181,8 +199,8 @@ def test_hp_gemm_split_k_matches_oracle(dev, T, split):
 
 @pytest.mark.parametrize("fused", [1, 2, 0])
 def test_hp_decode_chain_matches_oracle(dev, T, fused):
-    """Config-4 HP step (2 layers + LM head, small geometry) incl. strided A and SILU_MUL,
-    against the oracle chain with bf16 rounding between ops."""
+    """Config-4 HP step (2 layers + LM head, small geometry) incl. strided A and the fused
+    GEMM+SwiGLU op, against the oracle chain with bf16 rounding between ops."""
     dev.hp_set_fused(fused)
     M, H, Q, F, V, L = 128, 256, 384, 512, 1024, 2
     bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
@@ -218,8 +236,9 @@ def test_hp_decode_chain_matches_oracle(dev, T, fused):
         qkv = rnd(T.gemm_rows(h, wq, rows, Q, H).reshape(-1))
         qh = np.ascontiguousarray(qkv.reshape(M, Q)[:, :H]).reshape(-1)
         o = rnd(T.gemm_rows(qh, wo, rows, H, H).reshape(-1))
-        gu = rnd(T.gemm_rows(o, wg, rows, 2 * F, H).reshape(-1))
-        act = T.silu_mul(gu, M, F)
+        gu = T.gemm_rows(o, wg, rows, 2 * F, H)  # fp32 gate|up: the SwiGLU acts on the accumulators
+        g, u = gu[:, :F], gu[:, F:]
+        act = rnd((g / (1.0 + np.exp(-g)) * u).reshape(-1))
         h = rnd(T.gemm_rows(act, wd, rows, H, F).reshape(-1))
     want = T.gemm_rows(h, T.synth_bf16(V * H, SEED, 399, s(H)), rows, V, H)
     got = T.bf16_to_f32(d2h(dev, bufs[5], M * V)).reshape(M, V)

@@ -17,4 +17,11 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:axpy
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:hp_fused -s 1 -c 1 \
   -o gpurun_out/prof_fused -f python tools/ncu_fused.py > gpurun_out/ncu_fused.log 2>&1
 fi
+if [ "${LIVE:-1}" = "1" ]; then
+timeout 600 python tools/live_check.py 2.0 > gpurun_out/live_check.log 2>&1
+timeout 600 python tools/live_check4.py 2.0 > gpurun_out/live_check4.log 2>&1
+timeout 200 python tools/exit_probe.py > gpurun_out/exit_probe.log 2>&1
+timeout 200 python tools/fused_stamps.py 1 > gpurun_out/fused_timeline.log 2>&1
+timeout 300 python tools/decode_stamps.py 1 > gpurun_out/decode_timeline.log 2>&1
+fi
 tail -2 gpurun_out/smoke.log gpurun_out/pytest_gpu.log; tail -c 3000 gpurun_out/bench.log; tail -c 1500 gpurun_out/bench_ref.log
