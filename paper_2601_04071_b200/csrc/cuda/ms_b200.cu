@@ -21,6 +21,7 @@
 #include "stream_kernels.cuh"
 #include "tc_gemm.cuh"
 #include "hp_fused.cuh"
+#include "hp_gemv.cuh"
 
 using namespace msdev;
 
@@ -133,6 +134,7 @@ struct HpOpRt {
   int reduce_ctl_index = 0;          // control block of the split-K reduce kernel
   __nv_bfloat16* tmp = nullptr;      // GEMM_SWIGLU per-op path: [m x 2n] gate|up before the SwiGLU
   int act_ctl_index = 0;             // GEMM_SWIGLU per-op path: control block of the SwiGLU kernel
+  bool gemv = false;                 // m == 1 GEMM / GEMM_SWIGLU: runs in the HBM-streaming GEMV chain
 };
 
 struct HpChain {
@@ -150,6 +152,11 @@ struct HpChain {
   std::vector<FusedOpDesc> descs;  // copied into the launch parameters
   int l2_prefetch = 1;
   std::vector<float*> fused_ws;
+  // Batch-1 chain (every kernel op has m == 1): one hp_gemv_kernel launch (hp_gemv.cuh).
+  bool gemv = false;
+  std::vector<GemvOpDesc> gemv_descs;
+  uint32_t* wire_d = nullptr;       // tagged op->op handoff words
+  mutable uint32_t launches = 0;    // wire tag source (one tag per launch, stream-ordered)
 };
 
 }  // namespace
@@ -193,6 +200,7 @@ int set_smem_attrs() {
                                FusedCfg<2>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                FusedCfg<4>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   done = true;
   return 0;
 }
@@ -573,6 +581,128 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   return 0;
 }
 
+// Plan of a batch-1 chain (hp_gemv.cuh): per op, the unit size (whole rows, <= one 16 KB
+// stage) and the chain-wide unit counter at its first unit, so units are dealt to CTAs
+// round-robin across op boundaries.  Grid = SMs - 1 (same co-residency rule as plan_fused).
+int plan_gemv(ms_dev* d, HpChain& ch) {
+  int first = -1, last = -1;
+  for (int i = 0; i < static_cast<int>(ch.ops.size()); ++i)
+    if (!is_copy(ch.ops[i].op)) {
+      if (first < 0) first = i;
+      last = i;
+    }
+  for (int i = first; i <= last; ++i)
+    if (is_copy(ch.ops[i].op)) return fail(MS_E_ARG, "batch-1 chains: copies only before/after the kernel ops");
+  if (last - first + 1 > kGemvMaxOps) return fail(MS_E_ARG, "batch-1 chain too long");
+  ch.gemv_descs.clear();
+  const int grid = d->prop.multiProcessorCount - 1;
+  int64_t unit_ctr = 0;
+  for (int i = first; i <= last; ++i) {
+    const ms_hp_op& op = ch.ops[i].op;
+    GemvOpDesc g{};
+    g.n = static_cast<int>(op.n);
+    g.k = static_cast<int>(op.k);
+    g.x = reinterpret_cast<const __nv_bfloat16*>(op.a);
+    g.w = reinterpret_cast<const __nv_bfloat16*>(op.b);
+    g.bias = reinterpret_cast<const __nv_bfloat16*>(op.bias);
+    g.y = reinterpret_cast<__nv_bfloat16*>(op.c);
+    if (op.kind == MS_HP_GEMM || op.kind == MS_HP_GEMM_SWIGLU) {
+      const bool sw = op.kind == MS_HP_GEMM_SWIGLU;
+      g.kind = sw ? kGemvSwiglu : kGemvMatvec;
+      g.rows = std::min(32, kGemvStageBytes / (static_cast<int>(op.k) * 2 * (sw ? 2 : 1)));  // <= one output per lane
+      g.units = (g.n + g.rows - 1) / g.rows;
+      g.unit_base = static_cast<int>(unit_ctr % grid);
+      unit_ctr += g.units;
+    } else {
+      g.kind = op.kind == MS_HP_SILU_MUL ? kGemvSiluMul : kGemvBiasGelu;
+      g.k = 0;
+    }
+    ch.gemv_descs.push_back(g);
+  }
+  // Wires: op j whose input lies inside the output of the latest earlier op i reads it
+  // from op i's tagged wire (no grid phase); any other input orders op j behind op j-1's
+  // phase counter.  Wire offsets are 4-word aligned (16-byte vector polls).
+  const int n = static_cast<int>(ch.gemv_descs.size());
+  std::vector<int64_t> wire_off(n, -1);
+  std::vector<std::pair<int, int64_t>> src(n, {-1, 0});  // (producer op, word offset in its output)
+  int64_t words = 0;
+  for (int j = 1; j < n; ++j) {
+    GemvOpDesc& g = ch.gemv_descs[j];
+    const uint64_t a = reinterpret_cast<uint64_t>(g.x);
+    const uint64_t in_bytes = 2ull * (g.kind == kGemvMatvec || g.kind == kGemvSwiglu ? g.k
+                                      : g.kind == kGemvSiluMul ? 2 * g.n : g.n);
+    for (int i = j - 1; i >= 0; --i) {
+      const uint64_t c = reinterpret_cast<uint64_t>(ch.gemv_descs[i].y);
+      const uint64_t c_bytes = 2ull * ch.gemv_descs[i].n;
+      if (a + in_bytes <= c || a >= c + c_bytes) continue;  // no overlap: look further back
+      if (a >= c && a + in_bytes <= c + c_bytes && (a - c) % 8 == 0) src[j] = {i, static_cast<int64_t>((a - c) / 2)};
+      break;  // latest producer overlapping the input decides
+    }
+    if (src[j].first >= 0 && wire_off[src[j].first] < 0) {
+      wire_off[src[j].first] = words;
+      words += (ch.gemv_descs[src[j].first].n + 3) / 4 * 4;
+    }
+  }
+  if (words > 0) {
+    MS_CUDA(cudaMalloc(&ch.wire_d, sizeof(uint32_t) * words));
+    MS_CUDA(cudaMemset(ch.wire_d, 0, sizeof(uint32_t) * words));
+  }
+  for (int i = 0; i < n; ++i)
+    if (wire_off[i] >= 0) ch.gemv_descs[i].y_wire = ch.wire_d + wire_off[i];
+  for (int j = 1; j < n; ++j) {
+    GemvOpDesc& g = ch.gemv_descs[j];
+    if (src[j].first >= 0) {
+      g.x_wire = ch.gemv_descs[src[j].first].y_wire + src[j].second;
+    } else {
+      g.wait_phase = 1;
+      ch.gemv_descs[j - 1].arrive = 1;
+    }
+  }
+  const int np = n;
+  MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * np));
+  MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * np));
+  ch.fused_ctl = d->next_hp_ctl++;
+  if (ch.fused_ctl >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
+  ch.fused_first = first;
+  ch.fused_last = last;
+  ch.fused_grid = grid;
+  ch.fused_cs = 1;
+  ch.n_phases = np;
+  ch.gemv = true;
+  ch.fusable = true;
+  return 0;
+}
+
+int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl) {
+  GemvParams p{};
+  p.run = base_run(d, ch.fused_ctl);
+  p.run.hp_ctl = d->hp_ctl + chain_id;
+  p.run.hp_rec = &d->page_d->hp[chain_id];
+  p.run.hp_first = 1;
+  p.run.hp_last = !is_copy(ch.ops.back().op);
+  p.run.hp_seq = seq;
+  p.run.dbg = d->dbg;
+  p.run.reset_words = ch.phase_d;
+  p.run.n_reset = ch.n_phases;
+  p.phase_cnt = ch.phase_d;
+  p.n_ops = static_cast<int>(ch.gemv_descs.size());
+  p.tag = (++ch.launches) & 0xFFFFu;
+  static const int inflight = [] {
+    const char* e = getenv("MS_GEMV_INFLIGHT");
+    const int v = e ? atoi(e) : kGemvStages;
+    return v < 1 ? 1 : v > kGemvStages ? kGemvStages : v;
+  }();
+  p.inflight = inflight;
+  static const int prefetch = [] {
+    const char* e = getenv("MS_GEMV_PREFETCH");
+    return e ? std::max(0, atoi(e)) : 16;
+  }();
+  p.prefetch = prefetch;
+  for (size_t i = 0; i < ch.gemv_descs.size(); ++i) p.ops[i] = ch.gemv_descs[i];
+  MS_CUDA(launch_kc(hp_gemv_kernel, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
+  return 0;
+}
+
 int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl) {
   FusedParams p{};
   p.run = base_run(d, ch.fused_ctl);
@@ -604,11 +734,14 @@ int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool 
 
 // Enqueue a chain's work on the HP stream (after its gate when `after_gate`).
 int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after_gate) {
-  const bool fused = d->hp_fused && ch.fusable;
+  // batch-1 chains have no per-op kernels: the GEMV chain is their only implementation
+  const bool fused = (d->hp_fused && ch.fusable) || ch.gemv;
   for (size_t i = 0; i < ch.ops.size(); ++i) {
     if (fused && static_cast<int>(i) >= ch.fused_first && static_cast<int>(i) <= ch.fused_last) {
-      if (static_cast<int>(i) == ch.fused_first)
-        if (int rc = launch_fused(d, cid, ch, seq, after_gate && i == 0)) return rc;
+      if (static_cast<int>(i) == ch.fused_first) {
+        const bool pdl = after_gate && i == 0;
+        if (int rc = ch.gemv ? launch_gemv(d, cid, ch, seq, pdl) : launch_fused(d, cid, ch, seq, pdl)) return rc;
+      }
       continue;
     }
     if (int rc = launch_hp_op(d, cid, ch, i, seq, after_gate)) return rc;
@@ -972,13 +1105,33 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       break;
     }
   if (cid < 0 || n_ops < 1 || n_ops > kFusedMaxOps) return fail(MS_E_ARG, "bad HP chain");
+  // Batch-1 (m == 1) GEMM ops run as one HBM-streaming GEMV chain; they cannot share a
+  // chain with tcgen05 (m >= 128) GEMMs.  Checked before anything is allocated.
+  bool any_gemv = false, any_mat = false;
+  for (int i = 0; i < n_ops; ++i) {
+    const bool mm = ops[i].kind == MS_HP_GEMM || ops[i].kind == MS_HP_GEMM_SWIGLU;
+    any_gemv |= mm && ops[i].m == 1;
+    any_mat |= mm && ops[i].m != 1;
+  }
+  if (any_gemv && any_mat) return fail(MS_E_ARG, "an HP chain cannot mix m == 1 and m >= 128 GEMM ops");
+  for (int i = 0; i < n_ops && any_gemv; ++i)
+    if ((ops[i].kind == MS_HP_BIAS_GELU || ops[i].kind == MS_HP_SILU_MUL) && ops[i].m != 1)
+      return fail(MS_E_ARG, "batch-1 chain: elementwise ops must have m == 1");
   HpChain ch;
   for (int i = 0; i < n_ops; ++i) {
     HpOpRt o;
     o.op = ops[i];
     o.ctl_index = d->next_hp_ctl++;
     if (o.ctl_index >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
-    if (o.op.kind == MS_HP_GEMM) {
+    if ((o.op.kind == MS_HP_GEMM || o.op.kind == MS_HP_GEMM_SWIGLU) && o.op.m == 1) {
+      // Batch-1 op: HBM-streaming matrix-vector product over the row-major weights in place
+      // (hp_gemv.cuh).  A whole row (gate + up row for SWIGLU) must fit one 16 KB stage.
+      const int64_t row_cap = kGemvStageBytes / 2 / (o.op.kind == MS_HP_GEMM_SWIGLU ? 2 : 1);
+      if (o.op.n < 1 || o.op.k < 8 || o.op.k % 8 || o.op.k > row_cap) return fail(MS_E_ARG, "HP batch-1 GEMM shape");
+      if ((o.op.a | o.op.b) % 16) return fail(MS_E_ARG, "HP batch-1 GEMM operands must be 16-byte aligned");
+      o.gemv = true;
+      o.split = 1;
+    } else if (o.op.kind == MS_HP_GEMM) {
       const int bn = o.op.block_n ? o.op.block_n : 128;
       o.op.block_n = bn;
       if (o.op.m % kBM || o.op.n % bn || o.op.k % kBK) return fail(MS_E_ARG, "HP GEMM shape");
@@ -1047,7 +1200,11 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
     }
     ch.ops.push_back(o);
   }
-  if (int rc = plan_fused(d, ch)) return rc;
+  if (any_gemv) {
+    if (int rc = plan_gemv(d, ch)) return rc;
+  } else if (int rc = plan_fused(d, ch)) {
+    return rc;
+  }
   ch.used = true;
   d->chains[cid] = ch;
   *chain_id = cid;
@@ -1067,6 +1224,7 @@ int ms_hp_unregister_chain(ms_dev* d, int cid) {
   for (float* w : ch.fused_ws) cudaFree(w);
   if (ch.prog_d) cudaFree(ch.prog_d);
   if (ch.phase_d) cudaFree(ch.phase_d);
+  if (ch.wire_d) cudaFree(ch.wire_d);
   ch = HpChain{};
   return 0;
 }

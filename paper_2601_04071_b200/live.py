@@ -129,18 +129,21 @@ def decode_step_ops(M: int, H: int, Q: int, F: int, V: int, layers: int, bufs, w
 
 
 class Config4:
-    """Config 4 tenants on one B200.  HP = one decode step of a Llama-3.2-1B-geometry model
-    (hidden 2048, qkv 3072, FFN 8192, 16 layers, vocab 128256: 1.24 B parameters = 2.47 GB of
-    bf16 weights streamed per token); the bs=1 token rides in row 0 of the 128-row UMMA
-    tile (weights dominate the bytes; compute stays under the HBM time).  LP1 = bf16
-    8192^3 GEMM loop, LP2 = bf16 axpy over 2^30 elements (6 GiB of HBM traffic per pass)."""
+    """Config 4 tenants on one B200.  HP = one bs=1 decode step of a Llama-3.2-1B-geometry
+    model (hidden 2048, qkv 3072, FFN 8192, 16 layers, vocab 128256: 1.24 B parameters =
+    2.47 GB of bf16 weights streamed per token) as an m = 1 chain, i.e. the HBM-streaming
+    GEMV chain (hp_gemv.cuh).  LP1 = bf16 8192^3 GEMM loop, LP2 = bf16 axpy over 2^30
+    elements (6 GiB of HBM traffic per pass).  m = 128 gives the tcgen05 chain with the token
+    in row 0 of the UMMA tile (round-1 layout, kept for comparison)."""
 
-    M, H, Q, F, V, LAYERS = 128, 2048, 3072, 8192, 128256, 16
+    M, H, Q, F, V, LAYERS = 1, 2048, 3072, 8192, 128256, 16
     N_LP = 8192
     N_EW = 1 << 30
 
-    def __init__(self, dev: Device, seed: int = SEED):
+    def __init__(self, dev: Device, seed: int = SEED, m: int | None = None):
         self.dev = dev
+        if m is not None:
+            self.M = m
         M, H, Q, F, V = self.M, self.H, self.Q, self.F, self.V
         self.bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
         dev.fill_synth(self.bufs[0], M * H, seed, 400, 1.0)

@@ -197,12 +197,18 @@ def test_hp_gemm_split_k_matches_oracle(dev, T, split):
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
 
 
-@pytest.mark.parametrize("fused", [1, 2, 0])
-def test_hp_decode_chain_matches_oracle(dev, T, fused):
-    """Config-4 HP step (2 layers + LM head, small geometry) incl. strided A and the fused
-    GEMM+SwiGLU op, against the oracle chain with bf16 rounding between ops."""
+DECODE_SMALL = (256, 384, 512, 1024, 2)          # H, Q, F, V, layers
+DECODE_LLAMA = (2048, 3072, 8192, 4096, 1)       # Llama-3.2-1B layer geometry, short vocab
+
+
+@pytest.mark.parametrize("M,fused,geom", [(128, 1, DECODE_SMALL), (128, 2, DECODE_SMALL), (128, 0, DECODE_SMALL),
+                                          (1, 1, DECODE_SMALL), (1, 1, DECODE_LLAMA)])
+def test_hp_decode_chain_matches_oracle(dev, T, M, fused, geom):
+    """Config-4 HP step (layers + LM head) incl. strided A and the fused GEMM+SwiGLU op,
+    against the oracle chain with bf16 rounding between ops.  M = 128: tcgen05 chain;
+    M = 1 (bs=1 decode): the HBM-streaming GEMV chain (hp_gemv.cuh)."""
     dev.hp_set_fused(fused)
-    M, H, Q, F, V, L = 128, 256, 384, 512, 1024, 2
+    H, Q, F, V, L = geom
     bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
     s = lambda k: float(np.float32(1 / math.sqrt(k)))
     ws, host_w = [], []
@@ -222,7 +228,13 @@ def test_hp_decode_chain_matches_oracle(dev, T, fused):
     dev.fill_synth(bufs[0], M * H, SEED, 298, 1.0)
     from paper_2601_04071_b200.live import decode_step_ops
     chain = dev.hp_register_chain(decode_step_ops(M, H, Q, F, V, L, bufs, ws, lm))
-    dev.hp_launch_direct(chain, dev.hp_next_seq())
+    if M == 1:
+        ci = dev.hp_chain_info(chain)
+        assert ci["fused_grid"] == dev.info["sm_count"] - 1 and ci["cluster"] == 1
+    for _ in range(2):  # a second launch must reproduce the first (phase counters reset)
+        dev.sync()
+        dev.fill_synth(bufs[0], M * H, SEED, 298, 1.0)  # the chain overwrites h
+        dev.hp_launch_direct(chain, dev.hp_next_seq())
     dev.sync()
 
     def rnd(y):  # fp32 -> bf16 bits (RNE), like the device epilogue
@@ -245,3 +257,40 @@ def test_hp_decode_chain_matches_oracle(dev, T, fused):
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
     dev.hp_unregister_chain(chain)
     dev.hp_set_fused(1)
+
+
+def test_hp_gemv_chain_elementwise_and_errors(dev, T):
+    """Batch-1 chain with elementwise ops (GEMV -> BIAS_GELU -> GEMV -> SILU_MUL input), and
+    the registration errors of the batch-1 path."""
+    K, N = 512, 1000  # N not a multiple of the unit size: ragged last unit
+    x, y0, y1, y2 = dev.alloc(K * 2), dev.alloc(N * 2), dev.alloc(N * 2), dev.alloc(2 * N * 2)
+    w0, w1, bias = dev.alloc(N * K * 2), dev.alloc(2 * N * N * 2), dev.alloc(N * 2)
+    s = lambda k: float(np.float32(1 / math.sqrt(k)))
+    dev.fill_synth(x, K, SEED, 500, 1.0)
+    dev.fill_synth(w0, N * K, SEED, 501, s(K))
+    dev.fill_synth(w1, 2 * N * N, SEED, 502, s(N))
+    dev.fill_synth(bias, N, SEED, 503, 0.1)
+    ops = [dict(kind=1, block_n=0, a=x, b=w0, c=y0, bias=0, m=1, n=N, k=K),
+           dict(kind=2, block_n=0, a=y0, b=0, c=y1, bias=bias, m=1, n=N, k=0),
+           dict(kind=1, block_n=0, a=y1, b=w1, c=y2, bias=0, m=1, n=2 * N, k=N)]
+    chain = dev.hp_register_chain(ops)
+    dev.hp_launch_direct(chain, dev.hp_next_seq())
+    dev.sync()
+    h0 = T.gemm_rows(T.synth_bf16(K, SEED, 500, 1.0), T.synth_bf16(N * K, SEED, 501, s(K)), [0], N, K)
+    u = h0.astype(np.float32).view(np.uint32)
+    h0b = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16).reshape(-1)
+    h1 = T.bias_gelu(h0b, T.synth_bf16(N, SEED, 503, 0.1), 1, N)
+    got1 = d2h(dev, y1, N)
+    assert np.max(np.abs(T.bf16_to_f32(got1) - T.bf16_to_f32(h1))) <= 2 * 2.0 ** -8 * np.max(np.abs(T.bf16_to_f32(h1)))
+    want = T.gemm_rows(got1, T.synth_bf16(2 * N * N, SEED, 502, s(N)), [0], 2 * N, N)
+    got = T.bf16_to_f32(d2h(dev, y2, 2 * N)).reshape(1, -1)
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= BF16_TOL
+    dev.hp_unregister_chain(chain)
+    from paper_2601_04071_b200.device import DeviceError
+    with pytest.raises(DeviceError):  # rows longer than one 16 KB stage
+        dev.hp_register_chain([dict(kind=1, block_n=0, a=x, b=w0, c=y0, bias=0, m=1, n=8, k=16384)])
+    with pytest.raises(DeviceError):  # m == 1 and m == 128 GEMMs in one chain
+        dev.hp_register_chain([dict(kind=1, block_n=0, a=x, b=w0, c=y0, bias=0, m=1, n=128, k=512),
+                               dict(kind=1, block_n=128, a=x, b=w0, c=y0, bias=0, m=128, n=128, k=512)])
+    for p in (x, y0, y1, y2, w0, w1, bias):
+        dev.free(p)

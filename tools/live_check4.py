@@ -25,6 +25,9 @@ def main():
     res["exclusive"] = brief(ex)
     print("exclusive", json.dumps(res["exclusive"]), flush=True)
     slo = {"ttft_ns": ex["own_p99"]["ttft_ns"], "tpot_ns": ex["own_p99"]["tpot_ns"]}
+    ex2 = live_run(dev, sc, "exclusive", w.binding(), w.options(slo=slo))
+    res["exclusive_att"] = ex2.get("slo_attainment")
+    print("exclusive attainment vs own slo", res["exclusive_att"], "rate", sc["traces"][0]["bursty"]["rate"], flush=True)
     exlp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options())
     res["exclusive_lp"] = brief(exlp)
     for pol, kw in [("splitkernel", {}), ("splitkernel", {"eager": True}), ("reef", {}), ("reef_req", {})]:
