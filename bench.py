@@ -194,6 +194,8 @@ def aggregate_ranks(allr, horizon_total):
             "kb_rate": sum(r["kb_tiles"] for r in allr) / horizon_total,
             "kbr_rate": sum(r.get("kbr_tiles", 0) for r in allr) / horizon_total,
             "ex_rate": sum(r["exlp_rate"] for r in allr),
+            "pb_rate": sum(r.get("pb_tiles", 0) for r in allr) / horizon_total,
+            "att_pb": att("pb_rows") if all("pb_rows" in r for r in allr) else None,
             "att": att("rows"), "att_ex": att("ex_rows"), "att_kb": att("kb_rows"),
             "att_kbr": att("kbr_rows") if all("kbr_rows" in r for r in allr) else None}
 
@@ -205,7 +207,7 @@ def main():
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--step-s", type=float, default=1.0)
+    ap.add_argument("--step-s", type=float, default=2.5)
     ap.add_argument("--warmup-s", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -293,6 +295,19 @@ def main():
         kbr_tiles += r["lp"]["tiles_done"]
         kbr_samples += r["samples"]["ring_to_first_hp_cta_all"]
 
+    # --- power-governed variant: the same policy with the NVML clock-feedback governor
+    # sizing LP's SM footprint so the GPU stays off its 1 kW cap and the HP chain keeps max
+    # clocks (power; live.cpp PowerGovernor)
+    pb_rows, pb_tiles, pb_samples, pb_gov = [], 0, [], []
+    with ClockSampler(local) as pclk:
+        for i in range(args.steps):
+            r = live_run(dev, sc(i, args.step_s), "splitkernel", w.binding(),
+                         w.options(timeline=False, power_governor=True))
+            pb_gov.append(r.get("power_governor", {}).get("mean_lp_sms"))
+            pb_rows += r["requests"]["rows"]
+            pb_tiles += r["lp"]["tiles_done"]
+            pb_samples += r["samples"]["preempt_ring_to_first_hp_cta"]
+
     # --- e2e: same metric through the C-ABI with the HP request buffers in pinned host
     # memory (H2D of the input after the doorbell, D2H of the output before completion)
     e2e = live_run(dev, sc(0, args.step_s), "splitkernel", w.binding(e2e=True), w.options(timeline=False))
@@ -303,7 +318,8 @@ def main():
             "kbr_samples": kbr_samples, "exlp_rate": exlp_rate, "ex_rows": ex_rows,
             "step_ms": step_ms, "wall": wall, "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"],
             "launches": launches, "chains": chains, "clocks": clk.summary(), "calib": calib,
-            "slo": slo}
+            "slo": slo, "pb_rows": pb_rows, "pb_tiles": pb_tiles, "pb_samples": pb_samples,
+            "pb_clocks": pclk.summary(), "pb_gov": pb_gov}
     allr = gather(mine, ws)
     if rank != 0:
         dev.close()
@@ -348,6 +364,13 @@ def main():
                                           "p99_us": percentile([x for r in allr for x in r.get("kbr_samples", [])], 0.99) / 1e3
                                           if any(r.get("kbr_samples") for r in allr) else None},
         "lp_vs_kernel_boundary": lp_rate / max(1e-9, kb_rate),
+        "power_governed_variant": {"policy": "splitkernel + NVML clock-feedback power governor sizing LP's SM "
+                                             "footprint (live option power_governor)",
+                                 "mean_lp_sms": [x for r in allr for x in r["pb_gov"]],
+                                 "slo_attainment": agg["att_pb"],
+                                 "lp_throughput_vs_exclusive": agg["pb_rate"] / max(1e-9, ex_rate),
+                                 "p99_us": percentile([x for r in allr for x in r["pb_samples"]], 0.99) / 1e3,
+                                 "clocks": allr[0]["pb_clocks"]},
         "slo_ns": allr[0]["slo"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

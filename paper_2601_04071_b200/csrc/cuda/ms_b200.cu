@@ -990,7 +990,7 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   p.alpha = s.desc.alpha;
   p.n = static_cast<unsigned long long>(s.desc.n_elems);
   p.tile_elems = s.desc.tile_elems;
-  const uint64_t cap = static_cast<uint64_t>(d->prop.multiProcessorCount) * s.desc.ctas_per_sm;
+  const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve)) * s.desc.ctas_per_sm;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
   const int vpt = s.desc.tile_elems / (kStreamThreads * 8);
   switch (vpt) {

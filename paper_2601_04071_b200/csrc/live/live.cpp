@@ -13,9 +13,15 @@
 // The HP tenant's host-side bubble (hint) is reproduced from the keyed duration draw of
 // the reference (engine.hpp:583-588), so a live run and a replay of the same scenario
 // see the same arrivals, iteration counts and bubble lengths.
+#include <cuda_runtime_api.h>
+#include <dlfcn.h>
+#include <nvml.h>
 #include <time.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -78,6 +84,93 @@ struct LpTask {
   Ns tile_ns = 50000;
 };
 
+// Power governor (B200-specific; no reference counterpart).  A full-GPU tcgen05 GEMM
+// drives a B200 into its 1 kW cap (sw_power_cap, SM clock ~1.5 GHz instead of 1.965); the
+// clock recovers only on a ~10 ms scale, so HP work issued right after an LP burst runs
+// 10-25% slower and misses its SLO.  This thread samples the SM clock through NVML every
+// 5 ms and moves the LP SM budget: -6 SMs whenever the clock sits more than `slack` MHz
+// below max (default 40), +3 after 50 ms within it.  LP launches read the budget (LiveRun::lp_sms).  NVML is loaded with dlopen
+// (driver library), so hosts without it simply run ungoverned.
+class PowerGovernor {
+ public:
+  PowerGovernor(int ordinal, int n_sm, int min_sms, int start, unsigned slack_mhz)
+      : n_sm_(n_sm), min_sms_(min_sms), slack_(slack_mhz), target_(start) {
+    lib_ = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!lib_) return;
+    auto sym = [&](const char* n) { return dlsym(lib_, n); };
+    init_ = reinterpret_cast<nvmlReturn_t (*)()>(sym("nvmlInit_v2"));
+    shutdown_ = reinterpret_cast<nvmlReturn_t (*)()>(sym("nvmlShutdown"));
+    by_pci_ = reinterpret_cast<nvmlReturn_t (*)(const char*, nvmlDevice_t*)>(sym("nvmlDeviceGetHandleByPciBusId_v2"));
+    clock_ = reinterpret_cast<nvmlReturn_t (*)(nvmlDevice_t, nvmlClockType_t, unsigned int*)>(sym("nvmlDeviceGetClockInfo"));
+    max_clock_ = reinterpret_cast<nvmlReturn_t (*)(nvmlDevice_t, nvmlClockType_t, unsigned int*)>(sym("nvmlDeviceGetMaxClockInfo"));
+    char bus[64] = {0};
+    if (!init_ || !by_pci_ || !clock_ || !max_clock_ || init_() != NVML_SUCCESS) return;
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), ordinal) != cudaSuccess || by_pci_(bus, &dev_) != NVML_SUCCESS ||
+        max_clock_(dev_, NVML_CLOCK_SM, &max_mhz_) != NVML_SUCCESS)
+      return;
+    ok_ = true;
+    th_ = std::thread([this] { loop(); });
+  }
+  ~PowerGovernor() {
+    stop_.store(true);
+    if (th_.joinable()) th_.join();
+    if (ok_ && shutdown_) shutdown_();
+    if (lib_) dlclose(lib_);
+  }
+  bool ok() const { return ok_; }
+  int target() const { return target_.load(std::memory_order_relaxed); }
+  json summary() const {
+    json j = json::object();
+    j["enabled"] = json(ok_);
+    j["samples"] = json(static_cast<long long>(samples_));
+    j["max_mhz"] = json(static_cast<long long>(max_mhz_));
+    j["mean_lp_sms"] = json(samples_ ? sum_target_ / static_cast<double>(samples_) : 0.0);
+    j["mean_sm_mhz"] = json(samples_ ? sum_mhz_ / static_cast<double>(samples_) : 0.0);
+    j["at_max_fraction"] = json(samples_ ? static_cast<double>(at_max_) / static_cast<double>(samples_) : 0.0);
+    return j;
+  }
+
+ private:
+  void loop() {
+    int hold = 0;
+    while (!stop_.load(std::memory_order_relaxed)) {
+      unsigned int mhz = 0;
+      if (clock_(dev_, NVML_CLOCK_SM, &mhz) == NVML_SUCCESS) {
+        int t = target();
+        if (mhz + slack_ < max_mhz_) {
+          t = std::max(min_sms_, t - 6);
+          hold = 0;
+        } else if (++hold >= 10) {
+          t = std::min(n_sm_ - 1, t + 3);
+          hold = 0;
+        }
+        target_.store(t, std::memory_order_relaxed);
+        ++samples_;
+        sum_target_ += t;
+        sum_mhz_ += mhz;
+        at_max_ += mhz + slack_ >= max_mhz_ ? 1 : 0;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(5));
+    }
+  }
+  void* lib_ = nullptr;
+  nvmlReturn_t (*init_)() = nullptr;
+  nvmlReturn_t (*shutdown_)() = nullptr;
+  nvmlReturn_t (*by_pci_)(const char*, nvmlDevice_t*) = nullptr;
+  nvmlReturn_t (*clock_)(nvmlDevice_t, nvmlClockType_t, unsigned int*) = nullptr;
+  nvmlReturn_t (*max_clock_)(nvmlDevice_t, nvmlClockType_t, unsigned int*) = nullptr;
+  nvmlDevice_t dev_{};
+  unsigned int max_mhz_ = 0;
+  bool ok_ = false;
+  int n_sm_, min_sms_;
+  unsigned slack_;
+  std::atomic<int> target_;
+  std::atomic<bool> stop_{false};
+  std::thread th_;
+  long long samples_ = 0, at_max_ = 0;
+  double sum_target_ = 0, sum_mhz_ = 0;
+};
+
 int64_t mono_ns() {
   timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -102,10 +195,21 @@ class LiveRun {
     direct_hp_ = opts.value("direct_hp", false);  // profiler-safe: no gate kernels
     debug_runs_ = opts.value("debug_stamps", 0);   // diagnostics: per-CTA exit phases
     calibrate_ = opts.value("calibrate", true);
+    // LP SM footprint: `lp_sm_reserve` SMs stay free in every LP launch (the HP gate's home);
+    // `small_bubble_sms` > 0 caps LP at that many SMs while harvesting a bubble INSIDE an HP
+    // request (hint bubbles), so the co-running GEMM draws less power between HP iterations
+    // and the HP chain keeps its clocks (B200 runs into its 1 kW cap under a full-GPU GEMM).
+    base_reserve_ = opts.value("lp_sm_reserve", 1);
+    small_sms_ = opts.value("small_bubble_sms", 0);
+    max_sms_ = opts.value("lp_max_sms", 0);  // > 0: LP never uses more SMs (power budget)
     record_ = opts.value("timeline", true);
     ms_dev_info info{};
     ms_dev_get_info(dev_, &info);
     n_sm_ = info.sm_count;
+    if (opts.value("power_governor", false))
+      governor_ = std::make_unique<PowerGovernor>(info.ordinal, info.sm_count, opts.value("governor_min_sms", 37),
+                                                  opts.value("governor_start_sms", info.sm_count / 2),
+                                                  opts.value("governor_slack_mhz", 40u));
     for (const TaskSpec& t : sc_.tasks) {
       if (t.priority == Priority::High && want_hp_) {
         HpTask h;
@@ -310,10 +414,11 @@ class LiveRun {
     // Keyed bubble length, identical to the replay core (engine.hpp:583-593).
     const std::uint64_t req_index = art_.requests[h.request].index;
     const std::uint64_t base = hash_combine(hash_combine(sc_.seed, h.hint_hash), req_index * 17);
-    Ns dur = 0;
+    Ns dur = 0, predicted = 0;
     std::string key;
     for (const int hi : h.seg_hints[h.seg]) {
       const BubbleHint& hint = h.spec->bubble_hints[hi];
+      predicted += hint.duration.mean();  // the scheduler sizes LP from the hint's profile, not the draw
       dur += hint.duration.sample_keyed(hash_combine(
           base, hash_combine(static_cast<std::uint64_t>(h.iteration), static_cast<std::uint64_t>(hi))));
       if (!key.empty()) key += '+';
@@ -326,7 +431,7 @@ class LiveRun {
       open_hint_ = h.index;
       emit(now_, EventKind::SyncBegin, h.index, h.spec->name, "scheduler");
       emit(now_, EventKind::SyncEnd, h.index, h.spec->name, "scheduler");
-      start_harvest(dur);
+      start_harvest(std::max<Ns>(1, predicted));
     }
     push_timer(now_ + dur, kBubbleOver, h.index);
   }
@@ -398,8 +503,16 @@ class LiveRun {
   // divided by the safety factor (consolidation_prefix sizing, scheduler.hpp:66-85).
   uint64_t batch_tiles(const LpTask& l, Ns gap) const {
     const double waves = static_cast<double>(gap) / sc_.sched.safety_factor / static_cast<double>(l.tile_ns);
-    const uint64_t t = static_cast<uint64_t>(std::max(1.0, std::floor(waves)) * n_sm_);
+    const uint64_t t = static_cast<uint64_t>(std::max(1.0, std::floor(waves)) * lp_sms());
     return t;
+  }
+  // SMs the next LP launch may use
+  int lp_sms() const {
+    int n = n_sm_ - base_reserve_;
+    if (max_sms_ > 0) n = std::min(n, max_sms_);
+    if (governor_ && governor_->ok()) n = std::min(n, governor_->target());
+    if (small_sms_ > 0 && open_hint_ >= 0) n = std::min(n, small_sms_);
+    return std::max(1, n);
   }
 
   void start_harvest(Ns predicted_gap) {
@@ -417,6 +530,7 @@ class LiveRun {
     uint64_t budget = lt->total;
     if (harvest_) budget = std::min<uint64_t>(lt->total, lt->cursor + batch_tiles(*lt, harvest_gap_));
     if (debug_runs_ > 0) ms_debug_stamps(dev_, 1, nullptr, 0);
+    check(ms_set_lp_sm_reserve(dev_, lp_sms() < n_sm_ ? n_sm_ - lp_sms() : base_reserve_), "ms_set_lp_sm_reserve");
     check(ms_lp_run_ex(dev_, lt->dev_id, lt->cursor, lt->total, budget, np ? MS_RUN_NONPREEMPTIBLE : 0), "ms_lp_run");
     lp_budget_ = budget;
     lp_running_ = true;
@@ -508,6 +622,8 @@ class LiveRun {
   bool harvest_ = false, reef_ = false, reef_req_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
   bool direct_hp_ = false, calibrate_ = true;
   int debug_runs_ = 0;
+  int base_reserve_ = 1, small_sms_ = 0, max_sms_ = 0;
+  std::unique_ptr<PowerGovernor> governor_;
   std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
   int n_sm_ = 148;
   int64_t t0_ = 0, off0_ = 0, off1_ = 0, c0_ = 0, c1_ = 0;
@@ -766,6 +882,7 @@ json LiveRun::run() {
   lp["budget_extensions"] = json(static_cast<unsigned long long>(budget_extensions_));
   out["lp"] = std::move(lp);
   out["small_bubble_ns"] = json(static_cast<long long>(art_.small_bubble_time));
+  if (governor_) out["power_governor"] = governor_->summary();
   out["timeline_events"] = json(static_cast<unsigned long long>(art_.timeline.size()));
   if (opts_.contains("slo")) {
     SloThresholds slo{opts_.at("slo").at("ttft_ns").get<Ns>(), opts_.at("slo").at("tpot_ns").get<Ns>()};

@@ -31,17 +31,39 @@ def test_live_config1_short():
 
 
 def test_live_config4_short():
-    """Config 4 live: Llama-geometry decode HP (81-op fused chain) + two LP tenants (GEMM loop
-    and HBM streamer) round-robined into the HP gaps."""
+    """Config 4 live: Llama-geometry bs=1 decode HP (65-op GEMV chain) + two LP tenants (GEMM
+    loop and HBM streamer) round-robined into the HP gaps."""
     from paper_2601_04071_b200.device import Device
     from paper_2601_04071_b200.live import Config4, live_run
     dev = Device(0)
     w = Config4(dev)
     c = w.calibrate(reps=1)
-    assert c["hp_weight_gbs"] > 1000  # 2.47 GB of weights per step streamed from HBM
+    assert c["hp_weight_gbs"] > 3000  # 2.47 GB of weights per step streamed from HBM (GEMV chain)
     sc = w.scenario(seed=5, horizon_s=0.5)
     sk = live_run(dev, sc, "splitkernel", w.binding(), w.options())
     assert sk["requests"]["n"] >= 1 and sk["hp_chains"] > 10
     assert sk["lp"]["tiles_done"] > 0 and sk["lp"]["preemptions"] > 0
     assert 0 < sk["preempt_ring_to_first_hp_cta"]["p50_ns"] < 200_000
+    dev.close()
+
+
+def test_live_power_governor_and_lp_caps():
+    """LP SM budgets: a fixed cap (lp_max_sms) and the NVML clock-feedback governor both run
+    the policy to completion; the governor reports its samples and keeps LP within its
+    bounds."""
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config1, live_run
+    dev = Device(0)
+    w = Config1(dev)
+    w.calibrate(reps=2)
+    sc = w.scenario(seed=13, horizon_s=0.4)
+    capped = live_run(dev, sc, "splitkernel", w.binding(), w.options(lp_max_sms=37, small_bubble_sms=20))
+    # (requests still queued at the 0.4 s horizon end are not completed)
+    assert capped["lp"]["tiles_done"] > 0 and capped["requests"]["completed"] >= capped["requests"]["n"] - 5
+    gov = live_run(dev, sc, "splitkernel", w.binding(), w.options(power_governor=True, governor_min_sms=20))
+    g = gov["power_governor"]
+    if g["enabled"]:  # NVML present (driver library)
+        assert g["samples"] > 10 and 20 <= g["mean_lp_sms"] <= dev.info["sm_count"] - 1
+        assert g["max_mhz"] > 1000
+    assert gov["lp"]["tiles_done"] > 0
     dev.close()
