@@ -22,6 +22,7 @@
 #include "tc_gemm.cuh"
 #include "hp_fused.cuh"
 #include "hp_gemv.cuh"
+#include "tc_gemm2.cuh"
 
 using namespace msdev;
 
@@ -110,6 +111,7 @@ constexpr int kGateSmem = 40 * 1024;
 
 struct LpSlot {
   bool used = false;
+  bool pair = false;  // GEMM on CTA pairs (tc_gemm2.cuh): 256 x 256 tiles
   ms_lp_desc desc{};
   uint64_t total_tiles = 0;
   int tiles_m = 0, tiles_n = 0;
@@ -201,6 +203,7 @@ int set_smem_attrs() {
   MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                FusedCfg<4>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
   done = true;
   return 0;
 }
@@ -899,11 +902,18 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     if (desc->m % kBM || desc->n % bn || desc->k % kBK || desc->k < kBK)
       return fail(MS_E_ARG, "GEMM shape must be a multiple of (128, block_n, 64)");
     if (desc->m > (1ll << 31) || desc->n > (1ll << 31) || desc->k > (1ll << 31)) return fail(MS_E_ARG, "shape too large");
-    s.tiles_m = static_cast<int>(desc->m / kBM);
+    // MS_LP_GEMM_PAIR=1: 256-aligned shapes with 256-wide tiles run on CTA pairs
+    // (cta_group::2, tc_gemm2.cuh).  Measured at parity with the single-CTA kernel on 8192^3
+    // (1302 vs 1308 TF/s, tensor pipe ~72% active in both under the power cap), so the
+    // single-CTA kernel (lower preemption drain, fewer moving parts) stays the default.
+    s.pair = bn == 256 && desc->m % 256 == 0 && desc->n % 256 == 0 && getenv("MS_LP_GEMM_PAIR") &&
+             atoi(getenv("MS_LP_GEMM_PAIR")) != 0;
+    const int tm = s.pair ? 256 : kBM;
+    s.tiles_m = static_cast<int>(desc->m / tm);
     s.tiles_n = static_cast<int>(desc->n / bn);
     s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n;
     if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
-    if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, bn)) return rc;
+    if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, s.pair ? 128 : bn)) return rc;
     if (int rc = encode_c(&s.tma_c, reinterpret_cast<void*>(desc->c), desc->m, desc->n)) return rc;
   } else if (desc->kind == MS_LP_AXPY) {
     s.desc.tile_elems = desc->tile_elems ? desc->tile_elems : 8192;
@@ -980,6 +990,21 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.tiles_n = s.tiles_n;
     p.group_m = s.desc.group_m ? s.desc.group_m : 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
+    static const int mma_lag = [] {
+      const char* e = getenv("MS_LP_MMA_LAG");
+      const int v = e ? atoi(e) : 2;
+      return v < 0 ? 0 : v > 4 ? 4 : v;
+    }();
+    p.mma_lag = mma_lag;
+    if (s.pair) {
+      // one CTA pair per tile; pairs of SMs left after the reserve
+      const int pairs = static_cast<int>(std::max<uint64_t>(
+          1, std::min<uint64_t>(work, static_cast<uint64_t>(std::max(2, d->prop.multiProcessorCount - d->lp_sm_reserve) / 2))));
+      p.group_m = s.desc.group_m ? s.desc.group_m : 8;
+      MS_CUDA(launch_kc(tc_gemm2_kernel, 2 * pairs, 256, Gemm2Cfg::kSmemBytes, d->lp, false, 2, s.tma_a, s.tma_b,
+                        s.tma_c, p));
+      return 0;
+    }
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount - d->lp_sm_reserve)));
     return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, s.tma_c, p, grid, d->lp);
   }

@@ -43,6 +43,9 @@ struct GemmParams {
   // B stored k-block-major ([K/64][N][64], a 3-D tensor map): every B box is one
   // contiguous BN x 128 B chunk of HBM (DRAM-page friendly streaming of HP weights).
   int b_kblock_major;
+  // Preemptible runs keep at most mma_lag k-blocks of MMAs queued on the tensor core
+  // (1..4; 0 = unbounded): an abort then drains <= mma_lag k-blocks.
+  int mma_lag;
 };
 
 template <int BN>
@@ -185,11 +188,14 @@ __global__ void __launch_bounds__(256, 1)
     // ===================== UMMA issuer =====================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, drain_phase = 0;
-      // Preemptible runs keep at most 2 k-blocks of MMAs queued on the tensor core: an abort
-      // then drains <= 2 k-blocks instead of the whole smem ring (lower preemption latency;
-      // the queue still never runs dry).
-      uint32_t h_stage0 = 0, h_phase0 = 0, h_stage1 = 0, h_phase1 = 0;  // kLag = 2 history
-      int issued = 0;
+      // Preemptible runs keep at most mma_lag k-blocks of MMAs queued on the tensor core: an
+      // abort then drains <= mma_lag k-blocks instead of the whole smem ring (lower
+      // preemption latency; the queue still never runs dry).
+      // (Stages are consumed in ring order, so the k-block `lag` steps back sits at stage
+      // - lag with the phase flipped on wrap-around: no history arrays, which would live in
+      // local memory and slow this issue loop by ~9%.)
+      const int lag = p.run.preemptible ? p.mma_lag : 0;
+      int consumed = 0;
       for (int j = 0;; ++j) {
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
@@ -208,17 +214,14 @@ __global__ void __launch_bounds__(256, 1)
           if (aborted) {
             mbar_arrive(&s->empty[stage]);
           } else {
-            if (p.run.preemptible) {
-              const bool odd = issued & 1;
-              if (issued >= 2) mbar_wait(&s->empty[odd ? h_stage1 : h_stage0], odd ? h_phase1 : h_phase0);
-              if (odd) {
-                h_stage1 = stage;
-                h_phase1 = phase;
-              } else {
-                h_stage0 = stage;
-                h_phase0 = phase;
+            if (lag > 0 && consumed >= lag) {
+              int ps = static_cast<int>(stage) - lag;
+              uint32_t pp = phase;
+              if (ps < 0) {
+                ps += S;
+                pp ^= 1;
               }
-              ++issued;
+              mbar_wait(&s->empty[ps], pp);
             }
             const uint64_t a0 = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kABytes));
             const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + stage * Cfg::kBBytes));
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(256, 1)
             }
             umma_commit(&s->empty[stage]);
           }
+          ++consumed;
           if (++stage == S) {
             stage = 0;
             phase ^= 1;

@@ -104,12 +104,15 @@ __device__ __forceinline__ void poll_mirror(const TileRun& r, uint32_t* preempt,
 // from the host-mapped line with one 16-byte ld.acquire.sys per iteration, forwards them
 // to the device mirror, and publishes the claim counter to the host.  Stays alive until
 // every other CTA has exited so scheduler-initiated preemptions keep propagating.
-__device__ __forceinline__ void poll_host(const TileRun& r, const uint32_t* preempt, const uint32_t* producer_done) {
+// `group`: CTAs (this one included) that cannot exit before this CTA does — 1, or 2 for a
+// CTA pair whose teardown cluster barrier waits for this CTA.
+__device__ __forceinline__ void poll_host(const TileRun& r, const uint32_t* preempt, const uint32_t* producer_done,
+                                          unsigned int group = 1) {
   uint32_t mirrored = 0;
   for (;;) {
     if (ld_volatile_smem(preempt)) break;  // CTA 0 is leaving anyway
     if (ld_volatile_smem(producer_done) &&
-        *reinterpret_cast<volatile unsigned int*>(&r.ctl->exited) + 1 >= gridDim.x)
+        *reinterpret_cast<volatile unsigned int*>(&r.ctl->exited) + group >= gridDim.x)
       break;
     if (r.host_progress)
       st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(r.host_progress),

@@ -95,6 +95,7 @@ class Config1:
         self.calib = {
             "lp_gemm_ms": ms_gemm,
             "lp_gemm_tile_ns": tile_ns,
+            "lp_gemm_tiles": int(self.lp.total_tiles),
             "hp_chain_ms": ms_chain,
             "hp_gemm_tile_ns": int(ms_chain * 1e6 * 0.95 / 4),
             "hp_ew_tile_ns": max(1000, int(ms_chain * 1e6 * 0.05)),
@@ -188,6 +189,7 @@ class Config4:
             "lp_gemm_ms": ms_gemm, "lp_axpy_ms": ms_axpy, "hp_step_ms": ms_chain,
             "hp_weight_gbs": self.weight_bytes / (ms_chain * 1e-3) / 1e9,
             "lp_gemm_tile_ns": int(ms_gemm * 1e6 / math.ceil(self.lp_gemm.total_tiles / sm)),
+            "lp_gemm_tiles": int(self.lp_gemm.total_tiles),
             # one "tile" of the pacing model = one tile per SM per wave
             "lp_ew_tile_ns": int(ms_axpy * 1e6 / math.ceil(self.lp_axpy.total_tiles / sm)),
             "lp_ew_tiles": int(self.lp_axpy.total_tiles),

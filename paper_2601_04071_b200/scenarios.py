@@ -64,7 +64,7 @@ def config1(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
         "kernels": [
             _kernel("hp_gemm_128x4096x4096", 128, c["hp_gemm_tile_ns"], c["hp_gemm_tile_bytes"], False),
             _kernel("hp_bias_gelu", 128, c["hp_ew_tile_ns"], c["hp_ew_tile_bytes"], False),
-            _kernel("lp_gemm_8192", 2048, c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"]),
+            _kernel("lp_gemm_8192", c.get("lp_gemm_tiles", 2048), c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"]),
         ],
         "tasks": [
             {"name": "hp_infer", "priority": "high", "kind": "serving", "trace": "hp_trace",
@@ -90,7 +90,7 @@ def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
         "kernels": [
             _kernel("hp_decode_layer", 148, c.get("hp_layer_ns", 20_000), 148 * 1024 * 1024 // 148, False),
             _kernel("hp_lm_head", 148, c.get("hp_lm_head_ns", 40_000), 2048 * 128256 * 2 // 148, False),
-            _kernel("lp_gemm_8192", 2048, c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"]),
+            _kernel("lp_gemm_8192", c.get("lp_gemm_tiles", 2048), c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"]),
             _kernel("lp_axpy_1g", c.get("lp_ew_tiles", 16384), c["lp_ew_tile_ns"], c["lp_ew_tile_bytes"], per_sm=4),
         ],
         "tasks": [

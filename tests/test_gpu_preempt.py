@@ -73,17 +73,67 @@ def test_gemm_preempt_resume_bit_exact(dev, gemm):
 def test_budget_bounds_the_run(dev, gemm):
     n, c, k, ref = gemm
     dev.lp_reset(k)
-    dev.lp_run(k, 0, k.total_tiles, budget=300)
+    budget = k.total_tiles // 2
+    dev.lp_run(k, 0, k.total_tiles, budget=budget)
     st = dev.lp_wait(k, 30)
     assert not st["preempted"]
     done_fresh = st["tiles_done"]
-    assert st["cursor"] >= 300 and done_fresh <= 300 + 148
+    assert st["cursor"] >= budget and done_fresh <= budget + 148
     # the rest of the range, including parked tiles, completes the GEMM exactly
     dev.lp_run(k, st["cursor"], k.total_tiles)
     st2 = dev.lp_wait(k, 30)
     assert st2["cursor"] == k.total_tiles and st2["redo_count"] == 0
     assert st["tiles_done"] + st2["tiles_done"] == k.total_tiles
     assert np.array_equal(d2h(dev, c, n * n), ref)
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+def test_gemm_cta_pair_kernel_preempt_resume(dev, pair):
+    """The cta_group::2 LP GEMM (MS_LP_GEMM_PAIR=1, tc_gemm2.cuh) and the single-CTA one
+    produce the same bits, uninterrupted and preempted + resumed."""
+    import os
+    n = 2048
+    a, b, c = dev.alloc(n * n * 2), dev.alloc(n * n * 2), dev.alloc(n * n * 2)
+    dev.fill_synth(a, n * n, 8, 1, 1.0)
+    dev.fill_synth(b, n * n, 8, 2, float(np.float32(1 / math.sqrt(n))))
+    old = os.environ.get("MS_LP_GEMM_PAIR")
+    os.environ["MS_LP_GEMM_PAIR"] = str(pair)
+    try:
+        k = dev.lp_register_gemm(a, b, c, n, n, n, block_n=256)
+    finally:
+        if old is None:
+            os.environ.pop("MS_LP_GEMM_PAIR")
+        else:
+            os.environ["MS_LP_GEMM_PAIR"] = old
+    assert k.total_tiles == (n // 256) ** 2 if pair else (n // 128) * (n // 256)
+    dev.lp_run(k, 0, k.total_tiles)
+    dev.lp_wait(k, 30)
+    ref = d2h(dev, c, n * n)
+    dev.memset(c, 0, n * n * 2)
+    dev.lp_reset(k)
+    begin, runs = 0, 0
+    while True:
+        dev.lp_run(k, begin, k.total_tiles)
+        runs += 1
+        spin(15e-6)
+        dev.preempt_raise()
+        st = dev.lp_wait(k, 30)
+        begin = st["cursor"]
+        if begin >= k.total_tiles and st["redo_count"] == 0:
+            break
+        assert runs < 3000
+    assert np.array_equal(d2h(dev, c, n * n), ref)
+    if pair:  # same bits as the single-CTA kernel
+        os.environ.pop("MS_LP_GEMM_PAIR", None)
+        k1 = dev.lp_register_gemm(a, b, c, n, n, n, block_n=256)
+        dev.memset(c, 0, n * n * 2)
+        dev.lp_run(k1, 0, k1.total_tiles)
+        dev.lp_wait(k1, 30)
+        assert np.array_equal(d2h(dev, c, n * n), ref)
+        dev.lp_unregister(k1)
+    dev.lp_unregister(k)
+    for p_ in (a, b, c):
+        dev.free(p_)
 
 
 def test_axpy_preempt_resume_exact(dev):
