@@ -200,6 +200,61 @@ def aggregate_ranks(allr, horizon_total):
             "att_kbr": att("kbr_rows") if all("kbr_rows" in r for r in allr) else None}
 
 
+# ----------------------------------------------------------------------------- config-4 leg
+CFG4_POLICIES = ("splitkernel", "reef_req", "reef")
+
+
+def run_config4_leg(dev, horizon_s: float, seed: int) -> dict:
+    """Config 4 (BASELINE configs[3]): Llama-3.2-1B-geometry bs=1 decode HP at 80% HP load
+    (GEMV chain) + LP GEMM and HBM-streamer tenants.  Every LP-running policy runs under the
+    power governor (the same LP power budget for all), so the comparison isolates the
+    scheduling policy: splitkernel vs the kernel-boundary baselines."""
+    from paper_2601_04071_b200.live import Config4, live_run
+    w = Config4(dev)
+    w.calibrate()
+    sc = w.scenario(seed=seed, horizon_s=horizon_s, rate=w.hp_rate(0.8))
+    ex = live_run(dev, sc, "exclusive", w.binding(), w.options(timeline=False))
+    slo = {"ttft_ns": ex["own_p99"]["ttft_ns"], "tpot_ns": ex["own_p99"]["tpot_ns"]}
+    gov = {"power_governor": True}
+    exlp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options(timeline=False, **gov))
+    out = {"slo": slo, "ex_rows": ex["requests"]["rows"], "exlp_tiles": exlp["lp"]["tiles_done"],
+           "rate": sc["traces"][0]["bursty"]["rate"], "step_ms": w.calib["hp_step_ms"]}
+    for pol in CFG4_POLICIES:
+        r = live_run(dev, sc, pol, w.binding(), w.options(timeline=False, **gov))
+        out[pol] = {"rows": r["requests"]["rows"], "tiles": r["lp"]["tiles_done"],
+                    "ring": r["samples"]["ring_to_first_hp_cta_all"],
+                    "lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms")}
+    return out
+
+
+def aggregate_config4(parts: list) -> dict:
+    """Pool the per-rank config-4 legs: attainment = sum met / sum requests against each
+    rank's own exclusive p99 SLO; LP throughput = sum tiles / sum exclusive-LP tiles."""
+    def att(key):
+        met = tot = 0
+        for p_ in parts:
+            rows = p_["ex_rows"] if key is None else p_[key]["rows"]
+            met += sum(1 for x in rows if x[4] and x[1] <= p_["slo"]["ttft_ns"] and x[2] <= p_["slo"]["tpot_ns"])
+            tot += len(rows)
+        return met / max(1, tot)
+
+    exlp = sum(p_["exlp_tiles"] for p_ in parts)
+    res = {"workload": "cfg4 (BASELINE configs[3]) live: HP Llama-3.2-1B-geometry bs=1 decode (GEMV chain, "
+                       "2.47 GB/token) at 80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 "
+                       "axpy streamer; power governor on every LP-running policy",
+           "rate_req_s": parts[0]["rate"], "hp_step_ms": parts[0]["step_ms"],
+           "requests": sum(len(p_["ex_rows"]) for p_ in parts), "slo_attainment_exclusive": att(None)}
+    for pol in CFG4_POLICIES:
+        ring = [x for p_ in parts for x in p_[pol]["ring"]]
+        res[pol] = {"slo_attainment": att(pol),
+                    "lp_throughput_vs_exclusive": sum(p_[pol]["tiles"] for p_ in parts) / max(1, exlp),
+                    "ring_to_first_hp_cta_p99_us": percentile(ring, 0.99) / 1e3 if ring else None,
+                    "mean_lp_sms": parts[0][pol]["lp_sms"]}
+    res["lp_splitkernel_vs_reef_req"] = res["splitkernel"]["lp_throughput_vs_exclusive"] / max(
+        1e-9, res["reef_req"]["lp_throughput_vs_exclusive"])
+    return res
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -210,6 +265,8 @@ def main():
     ap.add_argument("--step-s", type=float, default=2.5)
     ap.add_argument("--warmup-s", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cfg4-s", type=float, default=10.0,
+                    help="config-4 leg (decode HP at 80%% load, governed): trace seconds; 0 skips it")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if ws > 1:
@@ -313,7 +370,9 @@ def main():
     e2e = live_run(dev, sc(0, args.step_s), "splitkernel", w.binding(e2e=True), w.options(timeline=False))
     e2e_samples = e2e["samples"]["preempt_ring_to_first_hp_cta"]
 
-    mine = {"samples": samples, "lp_exit": lp_exit, "rows": rows, "tiles": tiles, "kb_rows": kb_rows,
+    cfg4 = run_config4_leg(dev, args.cfg4_s, 7 + 10_000 * rank) if args.cfg4_s > 0 and not profiling else None
+
+    mine = {"cfg4": cfg4, "samples": samples, "lp_exit": lp_exit, "rows": rows, "tiles": tiles, "kb_rows": kb_rows,
             "kb_tiles": kb_tiles, "kb_samples": kb_samples, "kbr_rows": kbr_rows, "kbr_tiles": kbr_tiles,
             "kbr_samples": kbr_samples, "exlp_rate": exlp_rate, "ex_rows": ex_rows,
             "step_ms": step_ms, "wall": wall, "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"],
@@ -383,6 +442,7 @@ def main():
         "gpu_launches": int(sum(r["launches"] + 6 * r["chains"] for r in allr)),
         "clocks": allr[0]["clocks"],
         "calib": allr[0]["calib"],
+        "config4_decode_high_load": aggregate_config4([r["cfg4"] for r in allr]) if allr[0]["cfg4"] else None,
     }
     if not args.no_cpu_baseline:
         from paper_2601_04071_b200 import scenarios as S

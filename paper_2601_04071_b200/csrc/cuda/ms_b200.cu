@@ -107,6 +107,7 @@ int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint6
 }
 
 constexpr int kRedoCap = 8192;
+constexpr int kAxpyMaxPad = 200 * 1024;  // residency-capping dynamic smem of the HBM streamer
 constexpr int kGateSmem = 40 * 1024;
 
 struct LpSlot {
@@ -204,6 +205,10 @@ int set_smem_attrs() {
                                FusedCfg<4>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   done = true;
   return 0;
 }
@@ -1018,11 +1023,15 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve)) * s.desc.ctas_per_sm;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
   const int vpt = s.desc.tile_elems / (kStreamThreads * 8);
+  // Unused dynamic shared memory caps residency at ctas_per_sm CTAs per SM, so the grid
+  // ((SMs - reserve) x ctas_per_sm) really leaves the reserved SM empty for the HP gate and
+  // the first HP CTA (an HP chain CTA needs a whole SM's shared memory).
+  const int pad = std::min(kAxpyMaxPad, (228 * 1024) / s.desc.ctas_per_sm - 6 * 1024);
   switch (vpt) {
-    case 1: axpy_kernel<1><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
-    case 2: axpy_kernel<2><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
-    case 4: axpy_kernel<4><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
-    case 8: axpy_kernel<8><<<grid, kStreamThreads + 64, 0, d->lp>>>(p); break;
+    case 1: axpy_kernel<1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+    case 2: axpy_kernel<2><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+    case 4: axpy_kernel<4><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+    case 8: axpy_kernel<8><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
     default: return fail(MS_E_ARG, "tile_elems must be 2048 * {1,2,4,8}");
   }
   MS_CUDA(cudaGetLastError());
