@@ -136,11 +136,14 @@ int ms_preempt_raise(ms_dev* dev, uint32_t* epoch, int64_t* t_host_ns);
 uint32_t ms_preempt_epoch(ms_dev* dev);
 
 /* ---- HP chains --------------------------------------------------------------------- */
-#define MS_HP_GEMM 1      /* C = A * B^T (non-preemptible tcgen05 GEMM) */
+#define MS_HP_GEMM 1      /* C = A * B^T (non-preemptible tcgen05 GEMM); m == 1: batch-1 matrix-vector
+                             product — a chain whose GEMM ops all have m == 1 runs as one HBM-streaming
+                             GEMV launch (weights row-major [n,k] read in place, k <= 8192) */
 #define MS_HP_BIAS_GELU 2 /* c = gelu(a + bias) over m x n */
 #define MS_HP_SILU_MUL 5  /* c[m, n] = silu(a[m, j]) * a[m, n + j]: a is [m x 2n] = [gate | up] */
 #define MS_HP_GEMM_SWIGLU 6 /* c[m, n] = silu(a b_gate^T) * (a b_up^T); b = [2n x k] = [gate rows; up
-                               rows] (row-major); the SwiGLU is applied to the fp32 accumulators */
+                               rows] (row-major); the SwiGLU is applied to the fp32 accumulators
+                               (m == 1: GEMV chain, k <= 4096) */
 #define MS_HP_H2D 3       /* copy m bytes: pinned host a -> device c (e2e request input) */
 #define MS_HP_D2H 4       /* copy m bytes: device a -> pinned host c (e2e request output) */
 

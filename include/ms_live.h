@@ -17,9 +17,16 @@
  *                  "hp": {"<task name>": [<chain id of segment 0>, ...], ...}}
  * options_json  : {"eager": bool, "slo": {"ttft_ns": .., "tpot_ns": ..},
  *                  "tile_ns": {"<lp kernel name>": ns}, "timeline": bool,
- *                  "start_delay_ns": ns, "ndjson_path": str}
+ *                  "start_delay_ns": ns, "ndjson_path": str,
+ *                  LP SM footprint (B200 power cap):
+ *                  "lp_sm_reserve": n (SMs every LP launch leaves free, default 1),
+ *                  "lp_max_sms": n (fixed LP SM budget), "small_bubble_sms": n (budget
+ *                  while harvesting a bubble inside an HP request),
+ *                  "power_governor": bool (NVML SM-clock feedback sizes the LP budget),
+ *                  "governor_min_sms", "governor_start_sms", "governor_slack_mhz"}
  * *result_json  : requests, preemption delays (ring -> first HP CTA, and flag -> last LP
- *                 CTA exit), LP tiles / parents completed, SLO report, timeline summary.
+ *                 CTA exit), LP tiles / parents completed, SLO report, timeline summary,
+ *                 power-governor summary (mean LP SMs, SM clock).
  */
 #ifndef MS_LIVE_H_
 #define MS_LIVE_H_
