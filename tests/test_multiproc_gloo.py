@@ -49,3 +49,26 @@ def test_two_rank_replicas(tmp_path):
         pooled += M.run_scenario(S.config1(seed=100 + rank, horizon_s=1.0), "splitkernel", delays=True)["delays"]
     assert res["n"] == len(pooled) == sum(res["per_rank_n"])
     assert res["p99"] == M.percentile(pooled, 0.99)
+
+
+def test_config4_leg_pooling():
+    """bench.aggregate_config4 pools the per-rank config-4 legs: attainment = sum met / sum
+    requests against each rank's own SLO, LP = sum tiles / sum exclusive-LP tiles."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    row = lambda ttft, tpot, done=True: [0, ttft, tpot, 8, done]  # noqa: E731
+    part = lambda slo, ex_rows, split_rows, reef_rows, tiles: {  # noqa: E731
+        "slo": {"ttft_ns": slo, "tpot_ns": slo}, "ex_rows": ex_rows, "exlp_tiles": 100, "rate": 9.0, "step_ms": 0.6,
+        "splitkernel": {"rows": split_rows, "tiles": tiles[0], "ring": [5000, 7000], "lp_sms": 70.0},
+        "reef_req": {"rows": reef_rows, "tiles": tiles[1], "ring": [4000], "lp_sms": 60.0},
+        "reef": {"rows": reef_rows, "tiles": tiles[2], "ring": [900000], "lp_sms": 60.0}}
+    a = part(10, [row(5, 5), row(9, 9)], [row(5, 5), row(11, 5)], [row(12, 5), row(5, 5, False)], (40, 20, 70))
+    b = part(20, [row(5, 5), row(25, 5)], [row(5, 5), row(19, 19)], [row(5, 5), row(5, 5)], (50, 20, 80))
+    r = bench.aggregate_config4([a, b])
+    assert r["requests"] == 4
+    assert r["slo_attainment_exclusive"] == 3 / 4
+    assert r["splitkernel"]["slo_attainment"] == 3 / 4
+    assert r["reef_req"]["slo_attainment"] == 2 / 4
+    assert r["splitkernel"]["lp_throughput_vs_exclusive"] == 90 / 200
+    assert r["lp_splitkernel_vs_reef_req"] == (90 / 200) / (40 / 200)
+    assert r["reef"]["ring_to_first_hp_cta_p99_us"] == 900.0
