@@ -62,16 +62,16 @@ struct GemvOpDesc {
   uint32_t* y_wire;  // tagged copy of y for later ops (null: none)
 };
 
-static_assert(sizeof(GemvOpDesc) % 4 == 0, "descriptor copied as words");
+static_assert(sizeof(GemvOpDesc) % 16 == 0, "descriptors are bulk-copied (16-byte granules)");
 
 struct GemvParams {
   TileRun run;  // HP bookkeeping (first-CTA stamp, completion record, phase-counter reset)
   uint32_t* phase_cnt;  // [n_ops]: CTAs that finished op i
+  const GemvOpDesc* ops;  // [n_ops] in global memory (16-byte aligned), bulk-copied to smem
   int n_ops;
   uint32_t tag;  // this launch's wire tag (16 bits)
   int inflight;  // max units issued but not yet landed (the rest of the ring buffers landed data)
   int prefetch;  // L2 lookahead in units past the issue point
-  GemvOpDesc ops[kGemvMaxOps];
 };
 
 __device__ __forceinline__ uint4 ld_relaxed_v4(const uint32_t* p) {
@@ -322,24 +322,31 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 127) & ~uintptr_t(127));
   uint8_t* xs = ring + kGemvStages * kGemvStageBytes;
   const uint32_t ring_s = smem_u32(ring), xs_s = smem_u32(xs);
-  __shared__ uint64_t full[kGemvStages], empty[kGemvStages];
-  // Op descriptors in shared memory: dynamically indexed kernel-parameter reads go through
-  // the constant cache, whose misses wait behind the saturated memory system.
-  __shared__ GemvOpDesc sops[kGemvMaxOps];
-  for (int i = threadIdx.x; i < p.n_ops * static_cast<int>(sizeof(GemvOpDesc) / 4); i += blockDim.x)
-    reinterpret_cast<uint32_t*>(sops)[i] = reinterpret_cast<const uint32_t*>(p.ops)[i];
+  __shared__ uint64_t full[kGemvStages], empty[kGemvStages], desc_bar;
+  // Op descriptors live in shared memory (one bulk copy from global at entry): dynamically
+  // indexed kernel-parameter reads go through the constant cache, whose misses wait behind
+  // the saturated memory system, and small parameters keep the launch itself short.
+  __shared__ __align__(16) GemvOpDesc sops[kGemvMaxOps];
   const int G = static_cast<int>(gridDim.x);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
+    cta_started(p.run);  // first HP CTA dispatched (the preemption-latency end point)
+    gemv_stamp(p.run, 63);
     for (int i = 0; i < kGemvStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
+    mbar_init(&desc_bar, 1);
     fence_mbar_init();
-    cta_started(p.run);
-    gemv_stamp(p.run, 63);
+    const uint32_t bytes = static_cast<uint32_t>(p.n_ops * sizeof(GemvOpDesc));
+    mbar_arrive_expect_tx(&desc_bar, bytes);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sops)),
+                 "l"(p.ops), "r"(bytes), "r"(smem_u32(&desc_bar))
+                 : "memory");
   }
   __syncthreads();
+  mbar_wait(&desc_bar, 0);
   if (p.run.pdl_wait) pdl_wait();
 
   if (warp == 0) {

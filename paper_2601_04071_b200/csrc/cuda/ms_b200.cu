@@ -158,6 +158,7 @@ struct HpChain {
   // Batch-1 chain (every kernel op has m == 1): one hp_gemv_kernel launch (hp_gemv.cuh).
   bool gemv = false;
   std::vector<GemvOpDesc> gemv_descs;
+  GemvOpDesc* gemv_descs_d = nullptr;  // device copy (bulk-loaded by every CTA)
   uint32_t* wire_d = nullptr;       // tagged op->op handoff words
   mutable uint32_t launches = 0;    // wire tag source (one tag per launch, stream-ordered)
 };
@@ -666,6 +667,8 @@ int plan_gemv(ms_dev* d, HpChain& ch) {
       ch.gemv_descs[j - 1].arrive = 1;
     }
   }
+  MS_CUDA(cudaMalloc(&ch.gemv_descs_d, sizeof(GemvOpDesc) * n));
+  MS_CUDA(cudaMemcpy(ch.gemv_descs_d, ch.gemv_descs.data(), sizeof(GemvOpDesc) * n, cudaMemcpyHostToDevice));
   const int np = n;
   MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * np));
   MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * np));
@@ -694,6 +697,7 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
   p.run.n_reset = ch.n_phases;
   p.phase_cnt = ch.phase_d;
   p.n_ops = static_cast<int>(ch.gemv_descs.size());
+  p.ops = ch.gemv_descs_d;
   p.tag = (++ch.launches) & 0xFFFFu;
   static const int inflight = [] {
     const char* e = getenv("MS_GEMV_INFLIGHT");
@@ -706,7 +710,6 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
     return e ? std::max(0, atoi(e)) : 16;
   }();
   p.prefetch = prefetch;
-  for (size_t i = 0; i < ch.gemv_descs.size(); ++i) p.ops[i] = ch.gemv_descs[i];
   MS_CUDA(launch_kc(hp_gemv_kernel, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
   return 0;
 }
@@ -1259,6 +1262,7 @@ int ms_hp_unregister_chain(ms_dev* d, int cid) {
   if (ch.prog_d) cudaFree(ch.prog_d);
   if (ch.phase_d) cudaFree(ch.phase_d);
   if (ch.wire_d) cudaFree(ch.wire_d);
+  if (ch.gemv_descs_d) cudaFree(ch.gemv_descs_d);
   ch = HpChain{};
   return 0;
 }
