@@ -1026,10 +1026,13 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve)) * s.desc.ctas_per_sm;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
   const int vpt = s.desc.tile_elems / (kStreamThreads * 8);
-  // Unused dynamic shared memory caps residency at ctas_per_sm CTAs per SM, so the grid
-  // ((SMs - reserve) x ctas_per_sm) really leaves the reserved SM empty for the HP gate and
-  // the first HP CTA (an HP chain CTA needs a whole SM's shared memory).
-  const int pad = std::min(kAxpyMaxPad, (228 * 1024) / s.desc.ctas_per_sm - 6 * 1024);
+  // Residency is capped at 4 CTAs per SM by registers (__launch_bounds__(320, 4): 48
+  // registers, a 5th CTA does not fit), so the grid ((SMs - reserve) x 4) really leaves the
+  // reserved SM empty for the first HP CTA.  (Capping it with unused dynamic shared memory
+  // instead shrank the L1 carve-out and cost 20% of the streaming bandwidth; an uncapped
+  // 53-register build fitted only 3 CTAs per SM and left 144 CTAs pending, which tripled the
+  // preemption drain.)
+  const int pad = 0;
   switch (vpt) {
     case 1: axpy_kernel<1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
     case 2: axpy_kernel<2><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;

@@ -58,7 +58,7 @@ __device__ __forceinline__ uint32_t axpy2(float a, uint32_t xv, uint32_t yv) {
 }
 
 template <int VPT>  // 16-byte vectors per thread per tile
-__global__ void __launch_bounds__(kStreamThreads + 64) axpy_kernel(const __grid_constant__ StreamParams p) {
+__global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __grid_constant__ StreamParams p) {
   __shared__ uint32_t preempt, producer_done, tiles_done;
   __shared__ long long tile_sh[2];
   const int warp = threadIdx.x / 32;
