@@ -223,7 +223,10 @@ def run_config4_leg(dev, horizon_s: float, seed: int) -> dict:
         r = live_run(dev, sc, pol, w.binding(), w.options(timeline=False, **gov))
         out[pol] = {"rows": r["requests"]["rows"], "tiles": r["lp"]["tiles_done"],
                     "ring": r["samples"]["ring_to_first_hp_cta_all"],
+                    "lp_exit": r["samples"]["preempt_flag_to_last_lp_exit"],
+                    "step_p50_us": r["hp_chain_duration"].get("p50_ns", 0) / 1e3,
                     "lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms")}
+    out["ex_step_p50_us"] = ex["hp_chain_duration"].get("p50_ns", 0) / 1e3
     return out
 
 
@@ -243,12 +246,16 @@ def aggregate_config4(parts: list) -> dict:
                        "2.47 GB/token) at 80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 "
                        "axpy streamer; power governor on every LP-running policy",
            "rate_req_s": parts[0]["rate"], "hp_step_ms": parts[0]["step_ms"],
-           "requests": sum(len(p_["ex_rows"]) for p_ in parts), "slo_attainment_exclusive": att(None)}
+           "requests": sum(len(p_["ex_rows"]) for p_ in parts), "slo_attainment_exclusive": att(None),
+           "exclusive_step_p50_us": parts[0].get("ex_step_p50_us")}
     for pol in CFG4_POLICIES:
         ring = [x for p_ in parts for x in p_[pol]["ring"]]
         res[pol] = {"slo_attainment": att(pol),
                     "lp_throughput_vs_exclusive": sum(p_[pol]["tiles"] for p_ in parts) / max(1, exlp),
                     "ring_to_first_hp_cta_p99_us": percentile(ring, 0.99) / 1e3 if ring else None,
+                    "flag_to_last_lp_exit_p99_us": (percentile(lx, 0.99) / 1e3) if (lx := [
+                        x for p_ in parts for x in p_[pol].get("lp_exit", [])]) else None,
+                    "hp_step_p50_us": parts[0][pol].get("step_p50_us"),
                     "mean_lp_sms": parts[0][pol]["lp_sms"]}
     res["lp_splitkernel_vs_reef_req"] = res["splitkernel"]["lp_throughput_vs_exclusive"] / max(
         1e-9, res["reef_req"]["lp_throughput_vs_exclusive"])

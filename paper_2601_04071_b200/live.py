@@ -168,9 +168,11 @@ class Config4:
         self.x, self.y = dev.alloc(self.N_EW * 2), dev.alloc(self.N_EW * 2)
         dev.fill_synth(self.x, self.N_EW, seed, 21, 1.0)
         dev.fill_synth(self.y, self.N_EW, seed, 22, 1.0)
-        # 4096-element tiles: 6.4 vs 7.0 TB/s for 8192, but the preemption drain (a CTA finishes its
-        # claimed tile) drops from ~11 to ~8 us (tools/axpy_probe.py)
-        self.lp_axpy = dev.lp_register_axpy(self.x, self.y, self.N_EW, 0.5, tile_elems=4096)
+        # 8192-element tiles (7.0 TB/s).  4096 cut the preemption drain from ~11 to ~8 us and the
+        # config-4 ring -> first HP CTA p99 from ~10.3 to ~6.5 us, but the governor then granted
+        # LP ~90 instead of ~78 SMs and HP SLO attainment fell 4-9 points below exclusive in
+        # three runs (tools/axpy_probe.py, tools/policy_compare.py)
+        self.lp_axpy = dev.lp_register_axpy(self.x, self.y, self.N_EW, 0.5, tile_elems=8192)
         self.calib = None
 
     @property
@@ -195,7 +197,7 @@ class Config4:
             # one "tile" of the pacing model = one tile per SM per wave
             "lp_ew_tile_ns": int(ms_axpy * 1e6 / math.ceil(self.lp_axpy.total_tiles / sm)),
             "lp_ew_tiles": int(self.lp_axpy.total_tiles),
-            "lp_ew_tile_bytes": 6 * 4096,
+            "lp_ew_tile_bytes": 6 * 8192,
             "hp_layer_ns": int(ms_chain * 1e6 * 0.79 / self.LAYERS),
             "hp_lm_head_ns": int(ms_chain * 1e6 * 0.21),
         }
