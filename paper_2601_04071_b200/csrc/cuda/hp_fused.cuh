@@ -55,19 +55,19 @@ struct alignas(64) FusedOp {
 // block cluster and are reduced through distributed shared memory (no fp32 partials in
 // HBM/L2, no extra grid phase): CTA rank r owns output columns [r*W, r*W + W), W = BN/CS,
 // and receives the other CS-1 slices of that strip into `recv` with st.async.
-template <int CS>
+template <int CS, int BN = kFusedBN>
 struct FusedCfg {
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = kFusedBN * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStripCols = kFusedBN / CS;
+  static constexpr int kStripCols = BN / CS;
   static constexpr int kRecvSliceBytes = CS > 1 ? kBM * kStripCols * 4 : 0;
   static constexpr int kRecvBytes = CS > 1 ? (CS - 1) * kRecvSliceBytes : 0;
   static constexpr int kStagesRaw = (220 * 1024 - kRecvBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kTmemCols = 2 * kFusedBN;
+  static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kRecvBytes + 1024;
-  static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, kFusedBN);
+  static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN);
   static_assert(CS == 1 || CS == 2 || CS == 4, "cluster split must be 1, 2 or 4");
 };
 
@@ -87,6 +87,7 @@ struct FusedParams {
   uint32_t* phase_cnt;
   int n_ops;
   int l2_prefetch;
+  int full_fence;  // 1: __threadfence before each phase release (MS_FUSED_FULL_FENCE=1; default 0)
   FusedOpDesc ops[kFusedMaxOps];
 };
 
@@ -102,13 +103,17 @@ __device__ __forceinline__ void phase_wait(const uint32_t* cnt, uint32_t target)
 }
 
 // Epilogue-warp group (128 threads, named barrier 1): publish this CTA's part of a phase.
-__device__ __forceinline__ void group_arrive(uint32_t* cnt, bool leader, const TileRun* run = nullptr, int slot = 0) {
+// The release reduction alone orders the group's writes (bar.sync makes them precede the
+// leader's release, which is cumulative); `full_fence` adds the older __threadfence
+// (MEMBAR.SC.GPU) in front of it.
+__device__ __forceinline__ void group_arrive(uint32_t* cnt, bool leader, const TileRun* run = nullptr, int slot = 0,
+                                             bool full_fence = true) {
   fence_proxy_async_global();  // results may be read by other CTAs' TMA loads
   if (leader && run) dbg_stamp_ext(*run, slot);
   asm volatile("bar.sync 1, 128;" ::: "memory");
   if (leader) {
     if (run) dbg_stamp_ext(*run, slot + 1);
-    __threadfence();
+    if (full_fence) __threadfence();
     if (run) dbg_stamp_ext(*run, slot + 2);
     red_release_gpu_add(cnt, 1u);
   }
@@ -121,8 +126,9 @@ __device__ __forceinline__ void group_wait(const uint32_t* cnt, uint32_t target,
 // ---- grid phases (epilogue warps, 128 threads per CTA).  Each thread owns items
 // blockIdx.x * 128 + t + b * G * 128; all loads of a batch are issued before the first
 // add so one L2 latency covers the batch (the phases are latency-, not bandwidth-bound).
+template <int BN>
 __device__ __forceinline__ void reduce_store(const FusedOpDesc& o, int i, const float4& x) {
-  constexpr int quads = kFusedBN / 4;
+  constexpr int quads = BN / 4;
   const int row = i % kBM;
   const int tq = i / kBM;
   const int cq = tq % quads;
@@ -131,10 +137,11 @@ __device__ __forceinline__ void reduce_store(const FusedOpDesc& o, int i, const 
   uint2 out;
   out.x = pack_bf16x2(x.x, x.y);
   out.y = pack_bf16x2(x.z, x.w);
-  *reinterpret_cast<uint2*>(o.c + static_cast<size_t>(mb * kBM + row) * o.n + static_cast<size_t>(nb) * kFusedBN + cq * 4) = out;
+  *reinterpret_cast<uint2*>(o.c + static_cast<size_t>(mb * kBM + row) * o.n + static_cast<size_t>(nb) * BN + cq * 4) = out;
 }
+template <int BN>
 __device__ __forceinline__ const float4* reduce_src(const FusedOpDesc& o, int i) {
-  constexpr int quads = kFusedBN / 4;
+  constexpr int quads = BN / 4;
   const int row = i % kBM;
   const int tq = i / kBM;
   const int cq = tq % quads;
@@ -143,10 +150,10 @@ __device__ __forceinline__ const float4* reduce_src(const FusedOpDesc& o, int i)
          static_cast<size_t>(cq) * kBM + row;
 }
 
-template <int SPLIT, int B>
+template <int SPLIT, int B, int BN>
 __device__ __forceinline__ void reduce_slices(const FusedOpDesc& o, int t, int G) {
-  constexpr size_t slice_stride = kBM * kFusedBN / 4;
-  const int total = o.tiles_m * o.tiles_n * (kFusedBN / 4) * kBM;
+  constexpr size_t slice_stride = kBM * BN / 4;
+  const int total = o.tiles_m * o.tiles_n * (BN / 4) * kBM;
   const int step = G * 128;
   for (int i0 = blockIdx.x * 128 + t; i0 < total; i0 += step * B) {
     float4 v[B][SPLIT];
@@ -154,7 +161,7 @@ __device__ __forceinline__ void reduce_slices(const FusedOpDesc& o, int t, int G
     for (int b = 0; b < B; ++b) {
       const int i = i0 + b * step;
       if (i < total) {
-        const float4* src = reduce_src(o, i);
+        const float4* src = reduce_src<BN>(o, i);
 #pragma unroll
         for (int sl = 0; sl < SPLIT; ++sl) v[b][sl] = src[sl * slice_stride];
       }
@@ -168,23 +175,24 @@ __device__ __forceinline__ void reduce_slices(const FusedOpDesc& o, int t, int G
         for (int sl = 1; sl < SPLIT; ++sl) {  // slice order: deterministic
           x.x += v[b][sl].x; x.y += v[b][sl].y; x.z += v[b][sl].z; x.w += v[b][sl].w;
         }
-        reduce_store(o, i, x);
+        reduce_store<BN>(o, i, x);
       }
     }
   }
 }
 
+template <int BN>
 __device__ __forceinline__ void reduce_slices_any(const FusedOpDesc& o, int t, int G) {
-  constexpr size_t slice_stride = kBM * kFusedBN / 4;
-  const int total = o.tiles_m * o.tiles_n * (kFusedBN / 4) * kBM;
+  constexpr size_t slice_stride = kBM * BN / 4;
+  const int total = o.tiles_m * o.tiles_n * (BN / 4) * kBM;
   for (int i = blockIdx.x * 128 + t; i < total; i += G * 128) {
-    const float4* src = reduce_src(o, i);
+    const float4* src = reduce_src<BN>(o, i);
     float4 x = src[0];
     for (int sl = 1; sl < o.split; ++sl) {
       const float4 u = src[sl * slice_stride];
       x.x += u.x; x.y += u.y; x.z += u.z; x.w += u.w;
     }
-    reduce_store(o, i, x);
+    reduce_store<BN>(o, i, x);
   }
 }
 
@@ -352,10 +360,9 @@ __device__ __forceinline__ void silu_mul_phase(const FusedOpDesc& o, int t, int 
   }
 }
 
-template <int CS>
+template <int CS, int BN = kFusedBN>
 __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant__ FusedParams p) {
-  using Cfg = FusedCfg<CS>;
-  constexpr int BN = kFusedBN;
+  using Cfg = FusedCfg<CS, BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -534,7 +541,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
             ++j;
           }
           if (leader) dbg_stamp_ext(p.run, oi * 8 + 6);
-          group_arrive(p.phase_cnt + o.ready_phase, leader, &p.run, 40 + oi * 6 + 2);
+          group_arrive(p.phase_cnt + o.ready_phase, leader, &p.run, 40 + oi * 6 + 2, p.full_fence);
           if (leader) dbg_stamp_ext(p.run, oi * 8 + 7);
           continue;
         }
@@ -549,7 +556,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
           fused_unit_coords(o, u, mb, nb, kb0);
           const int row_in_tile = q * 32 + lane;
           const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * BN);
-          if (o.swiglu) {
+          if (BN == kFusedBN && o.swiglu) {  // (narrow plans never carry SwiGLU ops)
             // columns [0, 64) = gate, [64, 128) = up of output features [64 nb, 64 nb + 64)
             __nv_bfloat16* crow = o.c + static_cast<size_t>(mb * kBM + row_in_tile) * o.n + static_cast<size_t>(nb) * 64;
 #pragma unroll 1
@@ -602,20 +609,20 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
           if (leader) mbar_arrive(&s->tmem_empty[slot]);
         }
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 6);
-        group_arrive(p.phase_cnt + o.mma_phase, leader);
+        group_arrive(p.phase_cnt + o.mma_phase, leader, nullptr, 0, p.full_fence);
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 7);
         if (CS == 1 && o.split > 1) {
           // Reduce the k-slices (slice order) into bf16 C across the whole grid.
           group_wait(p.phase_cnt + o.mma_phase, static_cast<uint32_t>(G), leader);
           if (leader) dbg_stamp_ext(p.run, 40 + oi * 2);
           switch (o.split) {
-            case 2: reduce_slices<2, 6>(o, t, G); break;
-            case 4: reduce_slices<4, 3>(o, t, G); break;
-            case 8: reduce_slices<8, 1>(o, t, G); break;
-            default: reduce_slices_any(o, t, G); break;
+            case 2: reduce_slices<2, 6, BN>(o, t, G); break;
+            case 4: reduce_slices<4, 3, BN>(o, t, G); break;
+            case 8: reduce_slices<8, 1, BN>(o, t, G); break;
+            default: reduce_slices_any<BN>(o, t, G); break;
           }
           if (leader) dbg_stamp_ext(p.run, 41 + oi * 2);
-          group_arrive(p.phase_cnt + o.ready_phase, leader);
+          group_arrive(p.phase_cnt + o.ready_phase, leader, nullptr, 0, p.full_fence);
         }
       } else {
         // BIAS_GELU (tanh form, same arithmetic as bias_gelu_kernel / oracle tr_bias_gelu)
@@ -627,7 +634,7 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
         else
           bias_gelu_phase(o, t, G);
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 6);
-        group_arrive(p.phase_cnt + o.ready_phase, leader);
+        group_arrive(p.phase_cnt + o.ready_phase, leader, nullptr, 0, p.full_fence);
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 7);
       }
     }

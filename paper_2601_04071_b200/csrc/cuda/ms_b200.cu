@@ -149,6 +149,7 @@ struct HpChain {
   int fused_grid = 0;
   int fused_ctl = 0;
   int fused_cs = 1;  // cluster size (k-slices reduced through DSMEM) or 1
+  int fused_bn = 128;  // output tile width of the fused plan (32: narrow plan)
   int n_phases = 0;
   FusedProgram* prog_d = nullptr;
   uint32_t* phase_d = nullptr;
@@ -204,6 +205,8 @@ int set_smem_attrs() {
                                FusedCfg<2>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                FusedCfg<4>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               FusedCfg<1, 32>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
@@ -412,7 +415,8 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   for (int i = first; i <= last; ++i) {
     const ms_hp_op& op = ch.ops[i].op;
     if (is_copy(op)) return 0;  // copies between kernels: keep per-op launches
-    if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % kFusedBN || op.k % kBK)) return 0;
+    if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % 32 || op.k % kBK)) return 0;
+    if (op.kind == MS_HP_GEMM && op.n % kFusedBN && !(op.m == kBM && d->hp_fused == 1)) return 0;
     if (op.kind == MS_HP_GEMM_SWIGLU && (op.m % kBM || op.n % 64 || op.k % kBK)) return 0;
     if ((op.kind == MS_HP_BIAS_GELU || op.kind == MS_HP_SILU_MUL) && op.n % 8) return 0;
   }
@@ -423,6 +427,28 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   // until its not-yet-resident CTAs have run; a fused chain that needed every SM could then
   // wait at its first grid phase for an SM that only frees after the LP stragglers run.
   const int max_grid = sms - 1;
+  // Narrow plan (opt-in, MS_FUSED_NARROW=1; BN = 32, whole K per unit, no clusters): chains
+  // of m = 128 GEMMs without SwiGLU run one 128 x 32 output tile per CTA — no split-K
+  // exchange and no cluster placement.  Measured slower on the config-1 chain (90 vs 57 us):
+  // 128 CTAs re-reading the same 1 MB activation from L2 per op cost more than the DSMEM
+  // exchange + cluster reduction they replace.
+  int bn = kFusedBN;
+  {
+    const char* env = getenv("MS_FUSED_NARROW");
+    bool narrow = d->hp_fused == 1 && env && atoi(env) == 1;
+    int widest = 0;
+    for (int i = first; i <= last && narrow; ++i) {
+      const ms_hp_op& op = ch.ops[i].op;
+      if (op.kind == MS_HP_GEMM_SWIGLU) narrow = false;
+      if (op.kind == MS_HP_GEMM) {
+        if (op.m != kBM || op.n % 32 || op.n / 32 > max_grid || op.split_k > 1) narrow = false;
+        widest = std::max(widest, static_cast<int>(op.n / 32));
+      }
+    }
+    if (narrow && widest > 0) bn = 32;
+  }
+  for (int i = first; i <= last; ++i)
+    if (ch.ops[i].op.kind == MS_HP_GEMM && ch.ops[i].op.n % bn) return 0;  // per-op launches
   struct GemmShape {
     int idx, tiles, kbs, req;
   };
@@ -433,8 +459,8 @@ int plan_fused(ms_dev* d, HpChain& ch) {
       gemms.push_back({i - first, static_cast<int>(op.m / kBM) * static_cast<int>(2 * op.n / kFusedBN),
                        static_cast<int>(op.k / kBK), 1});
     if (op.kind != MS_HP_GEMM) continue;
-    gemms.push_back({i - first, static_cast<int>(op.m / kBM) * static_cast<int>(op.n / kFusedBN),
-                     static_cast<int>(op.k / kBK), op.split_k});
+    gemms.push_back({i - first, static_cast<int>(op.m / kBM) * static_cast<int>(op.n / bn),
+                     static_cast<int>(op.k / kBK), bn == kFusedBN ? op.split_k : 1});
   }
   std::vector<int> splits(prog.n_ops, 1);
   int cs = 1, max_units = 0;
@@ -442,7 +468,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   // tiles x CS fit one unit per CTA (else split 1, tiles spread over the grid); all CTAs
   // must be co-resident as clusters (the grid phases need co-residency).
   for (int c : {4, 2}) {
-    if (d->hp_fused == 2 || gemms.empty()) break;
+    if (d->hp_fused == 2 || gemms.empty() || bn != kFusedBN) break;
     std::vector<int> sp(prog.n_ops, 1);
     int mu = 0, n_split = 0;
     bool ok = true;
@@ -529,7 +555,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
       f.d.kind = kFusedGemm;
       f.d.swiglu = o.op.kind == MS_HP_GEMM_SWIGLU;
       f.d.tiles_m = f.d.m / kBM;
-      f.d.tiles_n = (f.d.swiglu ? 2 * f.d.n : f.d.n) / kFusedBN;
+      f.d.tiles_n = (f.d.swiglu ? 2 * f.d.n : f.d.n) / bn;
       const int split = splits[i - first];
       f.d.split = split;
       f.d.kb_per_unit = f.d.k / kBK / split;
@@ -539,9 +565,9 @@ int plan_fused(ms_dev* d, HpChain& ch) {
         f.d.b_kmajor = 1;
         const void* wb = o.b_tiled ? static_cast<const void*>(o.b_tiled) : reinterpret_cast<const void*>(o.op.b);
         const uint64_t bn_rows = f.d.swiglu ? 2 * o.op.n : o.op.n;
-        if (int rc = encode_kblock_major(&f.tma_b, wb, bn_rows, o.op.k, kFusedBN)) return rc;
+        if (int rc = encode_kblock_major(&f.tma_b, wb, bn_rows, o.op.k, bn)) return rc;
       } else {
-        if (int rc = encode_2d(&f.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, kFusedBN)) return rc;
+        if (int rc = encode_2d(&f.tma_b, reinterpret_cast<void*>(o.op.b), o.op.n, o.op.k, bn)) return rc;
       }
       if (cs > 1 && split > 1) {  // slices reduced inside the cluster: one phase (output ready)
         f.d.mma_phase = -1;
@@ -568,6 +594,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   }
   if (cs > 1) grid = max_units;  // a multiple of the cluster size
   ch.fused_cs = cs;
+  ch.fused_bn = bn;
   prog.n_phases = np;
   // L2 prefetch of the next op's weights: measured +2% on cluster launches (config-1 chain
   // 59.7 vs 60.9 us) but -11% on long non-cluster chains (config-4 step 1.03 vs 0.92 ms: the
@@ -729,7 +756,16 @@ int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool 
   p.phase_cnt = ch.phase_d;
   p.n_ops = static_cast<int>(ch.descs.size());
   p.l2_prefetch = ch.l2_prefetch;
+  static const int full_fence = [] {
+    const char* e = getenv("MS_FUSED_FULL_FENCE");
+    return e ? atoi(e) : 0;  // the release reduction suffices: 58 vs 60 us per config-1 chain
+  }();
+  p.full_fence = full_fence;
   for (size_t i = 0; i < ch.descs.size(); ++i) p.ops[i] = ch.descs[i];
+  if (ch.fused_bn == 32) {
+    MS_CUDA(launch_kc(hp_fused_kernel<1, 32>, ch.fused_grid, 256, FusedCfg<1, 32>::kSmemBytes, d->hp, pdl, 1, p));
+    return 0;
+  }
   switch (ch.fused_cs) {
     case 4:
       MS_CUDA(launch_kc(hp_fused_kernel<4>, ch.fused_grid, 256, FusedCfg<4>::kSmemBytes, d->hp, pdl, 4, p));
