@@ -198,6 +198,9 @@ int ms_clock_calibrate(ms_dev* dev, int rounds, int64_t* offset_ns, int64_t* rtt
 /* ---- kernel timing (CUDA events on the launching stream) ---------------------------- */
 /* Time `reps` back-to-back full runs of LP kernel `id` over [0, total); returns mean ms. */
 int ms_lp_time_full(ms_dev* dev, int id, int reps, float* ms_per_run);
+/* Same over the tile range [begin, end) (the on-B200 profiler behind KernelSpec.measured_time,
+ * which the reference consumes at engine.hpp:461-481 / splitter.hpp:141-207). */
+int ms_lp_time_range(ms_dev* dev, int id, uint64_t begin, uint64_t end, int reps, float* ms_per_run);
 /* Time `reps` direct launches of an HP chain; returns mean ms per chain. */
 int ms_hp_time_chain(ms_dev* dev, int chain_id, int reps, float* ms_per_chain);
 

@@ -1431,6 +1431,33 @@ int ms_lp_time_full(ms_dev* d, int id, int reps, float* ms_per_run) {
   return 0;
 }
 
+int ms_lp_time_range(ms_dev* d, int id, uint64_t begin, uint64_t end, int reps, float* ms_per_run) {
+  if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
+  LpSlot& s = d->lp_slots[id];
+  if (begin >= end || end > s.total_tiles || reps < 1) return fail(MS_E_ARG, "bad tile range");
+  cudaEvent_t a, b;
+  MS_CUDA(cudaEventCreate(&a));
+  MS_CUDA(cudaEventCreate(&b));
+  ms_lp_status st;
+  ms_lp_reset(d, id);
+  if (int rc = ms_lp_run(d, id, begin, end, end)) return rc;  // warm-up
+  if (int rc = ms_lp_wait(d, id, 20000000000ll, &st)) return rc;
+  MS_CUDA(cudaEventRecord(a, d->lp));
+  for (int i = 0; i < reps; ++i) {
+    ms_lp_reset(d, id);
+    if (int rc = ms_lp_run(d, id, begin, end, end)) return rc;
+  }
+  MS_CUDA(cudaEventRecord(b, d->lp));
+  MS_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  MS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  *ms_per_run = ms / reps;
+  ms_lp_poll(d, id, &st);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return 0;
+}
+
 int ms_hp_time_chain(ms_dev* d, int cid, int reps, float* ms_per_chain) {
   cudaEvent_t a, b;
   MS_CUDA(cudaEventCreate(&a));

@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
             "ms_hp_wait": (I, [P, I, U32, I64, C.POINTER(HpTimes)]),
             "ms_clock_calibrate": (I, [P, I, C.POINTER(I64), C.POINTER(I64)]),
             "ms_lp_time_full": (I, [P, I, I, C.POINTER(F)]),
+            "ms_lp_time_range": (I, [P, I, U64, U64, I, C.POINTER(F)]),
             "ms_hp_time_chain": (I, [P, I, I, C.POINTER(F)]),
         }
         for name, (res, args) in sig.items():
@@ -216,6 +217,12 @@ class Device:
     def lp_time_full(self, k: LpKernel, reps: int = 5) -> float:
         ms = C.c_float()
         _ck(lib().ms_lp_time_full(self._h, k.id, reps, C.byref(ms)))
+        return ms.value
+
+    def lp_time_range(self, k: LpKernel, begin: int, end: int, reps: int = 3) -> float:
+        """CUDA-event time (ms) of an LP run over tiles [begin, end)."""
+        ms = C.c_float()
+        _ck(lib().ms_lp_time_range(self._h, k.id, begin, end, reps, C.byref(ms)))
         return ms.value
 
     def set_lp_sm_reserve(self, n: int):

@@ -67,3 +67,32 @@ def test_live_power_governor_and_lp_caps():
         assert g["max_mhz"] > 1000
     assert gov["lp"]["tiles_done"] > 0
     dev.close()
+
+
+def test_profiler_kernelspec_and_split_plan():
+    """On-B200 profiler: measured_time rows grow with the tile count, the spec parses in the
+    reference schema (Eq. 1 capacity = resident CTAs) and yields a split plan whose slices
+    respect the cap."""
+    import math
+    from paper_2601_04071_b200 import microslice as M, profiler, scenarios
+    from paper_2601_04071_b200.device import Device
+    dev = Device(0)
+    n = 4096
+    a, b, c = dev.alloc(n * n * 2), dev.alloc(n * n * 2), dev.alloc(n * n * 2)
+    dev.fill_synth(a, n * n, 3, 1, 1.0)
+    dev.fill_synth(b, n * n, 3, 2, 1 / 64)
+    k = dev.lp_register_gemm(a, b, c, n, n, n, block_n=256)
+    sms = dev.info["sm_count"]
+    spec = profiler.profile_lp_kernel(dev, k, "g4096", sms - 1, (128 + 256) * n * 2, reps=2)
+    rows = [(r["n_blocks"], r["time"]["value"]) for r in spec["measured_time"]]
+    assert rows[-1][0] == k.total_tiles and all(t > 0 for _, t in rows)
+    assert rows[-1][1] > rows[0][1]
+    gpu = scenarios.gpu_b200(scenarios.DEFAULT_CALIB)
+    assert M.concurrent_capacity(gpu, spec) == sms  # one persistent CTA per SM
+    plan = profiler.split_plan(gpu, spec, cap_ns=200_000)
+    assert plan["blocks_per_slice"] >= 1
+    assert sum(math.prod(s[3:6]) for s in plan["slices"]) == k.total_tiles
+    dev.lp_unregister(k)
+    for p_ in (a, b, c):
+        dev.free(p_)
+    dev.close()
