@@ -202,6 +202,7 @@ class LiveRun {
     base_reserve_ = opts.value("lp_sm_reserve", 1);
     small_sms_ = opts.value("small_bubble_sms", 0);
     max_sms_ = opts.value("lp_max_sms", 0);  // > 0: LP never uses more SMs (power budget)
+    bound_hints_ = opts.value("bound_hint_harvest", false);
     record_ = opts.value("timeline", true);
     ms_dev_info info{};
     ms_dev_get_info(dev_, &info);
@@ -431,7 +432,7 @@ class LiveRun {
       open_hint_ = h.index;
       emit(now_, EventKind::SyncBegin, h.index, h.spec->name, "scheduler");
       emit(now_, EventKind::SyncEnd, h.index, h.spec->name, "scheduler");
-      start_harvest(std::max<Ns>(1, predicted));
+      start_harvest(std::max<Ns>(1, predicted), bound_hints_);
     }
     push_timer(now_ + dur, kBubbleOver, h.index);
   }
@@ -443,6 +444,7 @@ class LiveRun {
       open_hint_ = -1;
       ++generation_;
       harvest_open_ = false;
+      harvest_deadline_ = 0;
       const bool more = h.seg + 1 < h.seg_kernels.size() || h.iteration + 1 < h.n_iterations || !h.backlog.empty();
       if (!more && !eager_) stop_lp_soft();
       if (harvest_ && hp_active_ == 0 && !eager_)
@@ -515,9 +517,12 @@ class LiveRun {
     return std::max(1, n);
   }
 
-  void start_harvest(Ns predicted_gap) {
+  void start_harvest(Ns predicted_gap, bool bounded = false) {
     harvest_open_ = true;
     harvest_gap_ = predicted_gap;
+    // bounded: a hint bubble of known profile — LP stops at the predicted end / safety
+    // instead of being extended or relaunched into the next HP iteration
+    harvest_deadline_ = bounded ? now_ + static_cast<Ns>(predicted_gap / sc_.sched.safety_factor) : 0;
     if (!lp_running_) launch_lp();
   }
 
@@ -528,7 +533,19 @@ class LiveRun {
     ensure_parent(*lt);
     const bool np = reef_ || policy_ == "exclusive_lp";
     uint64_t budget = lt->total;
-    if (harvest_) budget = std::min<uint64_t>(lt->total, lt->cursor + batch_tiles(*lt, harvest_gap_));
+    if (harvest_) {
+      // Tiles that fit the gap, less the parked (redo) tiles every run finishes first.  A
+      // bounded hint bubble only gets what fits before its predicted end.
+      Ns gap = harvest_gap_;
+      if (harvest_deadline_ > 0) {
+        gap = harvest_deadline_ - now_;
+        if (gap * 1.0 < static_cast<double>(lt->tile_ns)) return;  // not even one wave left
+        gap = static_cast<Ns>(gap * sc_.sched.safety_factor);  // batch_tiles divides it back out
+      }
+      const uint64_t want = batch_tiles(*lt, gap);
+      const uint64_t fresh = want > lt->redo ? want - lt->redo : 0;
+      budget = std::min<uint64_t>(lt->total, lt->cursor + fresh);
+    }
     if (debug_runs_ > 0) ms_debug_stamps(dev_, 1, nullptr, 0);
     check(ms_set_lp_sm_reserve(dev_, lp_sms() < n_sm_ ? n_sm_ - lp_sms() : base_reserve_), "ms_set_lp_sm_reserve");
     check(ms_lp_run_ex(dev_, lt->dev_id, lt->cursor, lt->total, budget, np ? MS_RUN_NONPREEMPTIBLE : 0), "ms_lp_run");
@@ -553,7 +570,7 @@ class LiveRun {
   }
 
   void maybe_extend_budget() {
-    if (!harvest_ || !lp_running_ || !harvest_open_ || p_flag_) return;
+    if (!harvest_ || !lp_running_ || !harvest_open_ || p_flag_ || harvest_deadline_ > 0) return;
     LpTask& l = lp_[lp_cur_];
     if (lp_budget_ >= l.total) return;
     const uint64_t claimed = ms_lp_progress(dev_, l.dev_id);
@@ -623,6 +640,7 @@ class LiveRun {
   bool direct_hp_ = false, calibrate_ = true;
   int debug_runs_ = 0;
   int base_reserve_ = 1, small_sms_ = 0, max_sms_ = 0;
+  bool bound_hints_ = false;
   std::unique_ptr<PowerGovernor> governor_;
   std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
   int n_sm_ = 148;
@@ -658,7 +676,7 @@ class LiveRun {
   // LP
   bool lp_running_ = false, harvest_open_ = false, preempt_raised_ = false;
   int lp_cur_ = -1, lp_rr_ = 0;
-  Ns harvest_gap_ = 0, t_raise_ = 0;
+  Ns harvest_gap_ = 0, t_raise_ = 0, harvest_deadline_ = 0;
   uint64_t lp_budget_ = 0, run_begin_ = 0, run_redo_in_ = 0;
   uint64_t lp_tiles_done_ = 0, lp_launches_ = 0, lp_preemptions_ = 0, budget_extensions_ = 0;
   std::vector<Ns> ring_to_first_, preempt_delays_, lp_exit_lat_, lp_seen_lat_, gate_to_first_, chain_durations_;

@@ -1,6 +1,7 @@
 """Development driver: live policy comparison on one B200 for config 1 or 4, optionally
 with the power governor on every policy that runs LP work.
-usage: policy_compare.py <cfg 1|4> <horizon_s> [governor 0|1] [seed] [config-4 HP utilisation]"""
+usage: policy_compare.py <cfg 1|4> <horizon_s> [governor 0|1] [seed] [config-4 HP utilisation]
+                         [extra splitkernel options json]"""
 from __future__ import annotations
 
 import json
@@ -29,23 +30,26 @@ def main():
     slo = {"ttft_ns": ex["own_p99"]["ttft_ns"], "tpot_ns": ex["own_p99"]["tpot_ns"]}
     ex2 = live_run(dev, sc, "exclusive", w.binding(), w.options(timeline=False, slo=slo))
     extra = {"power_governor": True} if gov else {}
+    sk_extra = json.loads(sys.argv[6]) if len(sys.argv) > 6 else {}
     exlp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options(timeline=False, **extra))
     res = {"config": cfg, "horizon_s": horizon, "governor": gov, "seed": seed, "hp_utilisation": util,
            "rate": sc["traces"][0]["bursty"]["rate"],
            "requests": ex["requests"]["n"], "exclusive_slo": ex2["slo_attainment"],
            "exclusive_lp_tiles_per_s": exlp["lp"]["tiles_per_s"]}
     print("exclusive", res, flush=True)
-    for pol in ("splitkernel", "reef_req", "reef"):
+    for pol in (("splitkernel",) if sk_extra else ("splitkernel", "reef_req", "reef")):
         with ClockSampler(0) as clk:
-            r = live_run(dev, sc, pol, w.binding(), w.options(timeline=False, slo=slo, **extra))
+            r = live_run(dev, sc, pol, w.binding(),
+                         w.options(timeline=False, slo=slo, **extra, **(sk_extra if pol == "splitkernel" else {})))
         b = {"slo": r["slo_attainment"], "lp_norm": r["lp"]["tiles_per_s"] / max(1e-9, exlp["lp"]["tiles_per_s"]),
              "ring_p99_us": r["ring_to_first_hp_cta_all"].get("p99_ns", 0) / 1e3,
              "chain_p50_us": r["hp_chain_duration"].get("p50_ns", 0) / 1e3, "clocks": clk.summary(),
              "mean_lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms")}
         res[pol] = b
         print(pol, json.dumps(b), flush=True)
-    res["lp_split_over_reef_req"] = res["splitkernel"]["lp_norm"] / max(1e-9, res["reef_req"]["lp_norm"])
-    print("lp splitkernel / reef_req =", res["lp_split_over_reef_req"], flush=True)
+    if "reef_req" in res:
+        res["lp_split_over_reef_req"] = res["splitkernel"]["lp_norm"] / max(1e-9, res["reef_req"]["lp_norm"])
+        print("lp splitkernel / reef_req =", res["lp_split_over_reef_req"], flush=True)
     (ROOT / "gpurun_out" / f"policy_compare_cfg{cfg}_gov{int(gov)}_u{util or 0.5}.json").write_text(json.dumps(res, indent=1))
     dev.close()
 
