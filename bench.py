@@ -211,6 +211,7 @@ def run_config4_leg(dev, horizon_s: float, seed: int) -> dict:
     scheduling policy: splitkernel vs the kernel-boundary baselines."""
     from paper_2601_04071_b200.live import Config4, live_run
     w = Config4(dev)
+    time.sleep(0.5)  # let the part leave the power cap the config-1 GEMM runs put it in
     w.calibrate()
     sc = w.scenario(seed=seed, horizon_s=horizon_s, rate=w.hp_rate(0.8))
     ex = live_run(dev, sc, "exclusive", w.binding(), w.options(timeline=False))
