@@ -516,7 +516,7 @@ class LiveRun {
         --debug_runs_;
       }
     }
-    lp_samples_.push_back(LpSample{st.preempted && preempt_raised_ ? t_raise_ : -1, st.t_seen, st.t_exit,
+    lp_samples_.push_back(LpSample{st.preempted && preempt_raised_ ? t_raise_ : -1, st.t_seen, st.t_exit, st.t_start,
                                    static_cast<int>(hp_.size()) + lp_cur_, l.kernel,
                                    "tiles=" + std::to_string(st.tiles_done) + ";cursor=" + std::to_string(st.cursor) +
                                        ";redo=" + std::to_string(st.redo_count) +
@@ -572,7 +572,7 @@ class LiveRun {
   };
   struct LpSample {
     Ns raise;  // -1: not a preemption we raised
-    uint64_t seen, exit;
+    uint64_t seen, exit, start;
     int stream;
     std::string kernel, detail;
   };
@@ -597,6 +597,7 @@ class LiveRun {
   uint64_t lp_budget_ = 0, run_begin_ = 0, run_redo_in_ = 0;
   uint64_t lp_tiles_done_ = 0, lp_launches_ = 0, lp_preemptions_ = 0, budget_extensions_ = 0;
   std::vector<Ns> ring_to_first_, preempt_delays_, lp_exit_lat_, lp_seen_lat_, gate_to_first_, chain_durations_;
+  std::vector<Ns> lp_queued_exit_lat_;  // preempted runs that had not started at the raise
   RunArtifacts art_;
 
 };
@@ -711,8 +712,15 @@ json LiveRun::run() {
   }
   for (const LpSample& smp : lp_samples_) {
     if (smp.raise >= 0) {
-      lp_exit_lat_.push_back(dev_to_host(smp.exit) - smp.raise);
-      if (smp.seen) lp_seen_lat_.push_back(dev_to_host(smp.seen) - smp.raise);
+      // A run whose first CTA started after the raise was still queued behind the HP chain
+      // (its CTAs get SMs only when HP leaves them): it never occupied an SM HP needed, so
+      // its exit time is reported apart from the drain of running LP work.
+      if (smp.start && dev_to_host(smp.start) > smp.raise) {
+        lp_queued_exit_lat_.push_back(dev_to_host(smp.exit) - smp.raise);
+      } else {
+        lp_exit_lat_.push_back(dev_to_host(smp.exit) - smp.raise);
+        if (smp.seen) lp_seen_lat_.push_back(dev_to_host(smp.seen) - smp.raise);
+      }
     }
     emit(dev_to_host(smp.exit), EventKind::KernelDone, smp.stream, smp.kernel, smp.detail);
   }
@@ -747,6 +755,7 @@ json LiveRun::run() {
   out["ring_to_first_hp_cta_all"] = summarize(ring_to_first_);
   out["preempt_flag_to_last_lp_exit"] = summarize(lp_exit_lat_);
   out["preempt_flag_to_first_lp_seen"] = summarize(lp_seen_lat_);
+  out["preempt_flag_to_exit_of_queued_lp_runs"] = summarize(lp_queued_exit_lat_);
   std::vector<Ns> g2f;
   for (const Ns x : gate_to_first_)
     if (x >= 0) g2f.push_back(x);

@@ -42,19 +42,24 @@ def profile_lp_kernel(dev: Device, k: LpKernel, name: str, resident: int, tile_b
                  Eq. 1 capacity the spec must reproduce (tpb 256, occupancy resident/8/SMs)
     tile_bytes : compulsory HBM bytes per tile (bw_demand_per_block = bytes / tile time)
     """
-    sms = dev.info["sm_count"]
     pts = points or sweep_points(k.total_tiles, resident)
     rows = []
     for n in pts:
         ms = dev.lp_time_range(k, 0, n, reps)
         rows.append((n, int(round(ms * 1e6))))
+    return kernel_spec(name, k.total_tiles, resident, dev.info["sm_count"], tile_bytes, rows)
+
+
+def kernel_spec(name: str, total: int, resident: int, sms: int, tile_bytes: float, rows: list) -> dict:
+    """Reference-schema KernelSpec from measured (n_tiles, ns) rows (the last row = the
+    whole tile space)."""
     full_ns = rows[-1][1]
-    waves = math.ceil(k.total_tiles / resident)
+    waves = math.ceil(total / resident)
     tile_ns = max(1, full_ns // waves)
     per_sm = max(1, round(resident / sms))  # whole CTAs per SM (Eq. 1 floors o * 2048 / 256)
     return {
         "name": name,
-        "grid": [int(k.total_tiles), 1, 1],
+        "grid": [int(total), 1, 1],
         "threads_per_block": 256,
         "occupancy": per_sm / 8.0,  # Eq. 1 (PerSmFloor): n_sm * floor(o * 2048 / 256) = n_sm * per_sm
         "block_time": {"dist": "point", "value": _dur(tile_ns)},
