@@ -48,3 +48,4 @@ for oi in range(0, 8):
     print(f"op{oi}->{oi + 1}: done {dn.min():6.2f}/{np.median(dn):6.2f}/{dn.max():6.2f}  x {xr.min():6.2f}/{np.median(xr):6.2f}/{xr.max():6.2f}"
           f"  slowest-done CTA {int(np.argmax(dn))}")
 dev.close()
+
