@@ -58,6 +58,8 @@ enum class Detail : std::uint8_t {
   Hint,           // hint=<interned a>
   Consolidate,    // consolidate=a->b
   Chunk,          // chunk=a
+  MemFault,       // tier=<peer if b == 1 else dram>;chunk=a
+  Probe,          // link=a;score=g
 };
 
 struct TimelineRecord {

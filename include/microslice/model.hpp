@@ -15,7 +15,7 @@
 
 namespace microslice {
 
-struct NvlinkPeer {  // model.hpp:13-18 (memory tier: configuration only here)
+struct NvlinkPeer {  // model.hpp:13-18 (memory tier links, microslice/memory.hpp)
   int peer_id = 0;
   Ns baseline_latency = us(2);
   double bandwidth = 600.0e9;
@@ -125,8 +125,7 @@ struct ReefConfig {
 
 enum class EvictionPolicy { ContentionFirst, RoundRobin };
 
-/// Memory-tier knobs (model.hpp:205-225).  The tier itself is out of scope for this
-/// build: a scenario with `enabled` is rejected by Engine.
+/// Memory-tier knobs (model.hpp:205-225); the tier is microslice/memory.hpp.
 struct MemParams {
   bool enabled = false;
   double hbm_gb = 80.0;

@@ -18,9 +18,11 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <queue>
 #include <sstream>
 
 #include "microslice/engine.hpp"
+#include "microslice/memory.hpp"
 
 namespace microslice {
 namespace {
@@ -34,6 +36,7 @@ enum class EvType : std::uint8_t {
   LargeBubbleCheck,
   Poke,
   UtilTick,
+  ProbeTick,  // memory tier: periodic link ping-probe (engine.hpp:1263-1276)
 };
 
 // Event priority classes (Appendix A #2): HP work 0, LP work / ticks 1, infra 2.
@@ -174,6 +177,7 @@ struct TaskRt {
   // LP state
   std::size_t seq_cursor = 0;
   long parents_made = 0;
+  std::vector<std::int64_t> chunk_ids;  // memory tier placement (engine.hpp:396-407)
 };
 
 struct PolicyTraits {
@@ -212,7 +216,20 @@ class SimDevice {
 
   std::int64_t total_threads() const { return total_threads_; }
   std::int64_t busy_threads() const { return total_threads_ - free_threads_; }
-  double bw_demand() const { return wave_bw_; }
+  /// HBM demand now: resident waves + in-flight memory-tier chunk transfers, which hold
+  /// HBM at their link's nominal rate until they end (engine.hpp:266-273, 1221-1224).
+  double bw_demand(Ns now) {
+    while (!transfers_.empty() && transfers_.top().first <= now) {
+      transfer_bw_ -= transfers_.top().second;
+      transfers_.pop();
+    }
+    if (transfers_.empty()) transfer_bw_ = 0.0;
+    return wave_bw_ + transfer_bw_;
+  }
+  void add_transfer(Ns end, double bw) {
+    transfers_.push({end, bw});
+    transfer_bw_ += bw;
+  }
   void note_occupancy(Ns now) {
     busy_integral_ += static_cast<double>(total_threads_ - free_threads_) *
                       static_cast<double>(now - last_occ_change_);
@@ -228,6 +245,8 @@ class SimDevice {
   Core& core_;
   std::int64_t total_threads_ = 0, free_threads_ = 0;
   double wave_bw_ = 0.0;
+  std::priority_queue<std::pair<Ns, double>, std::vector<std::pair<Ns, double>>, std::greater<>> transfers_;
+  double transfer_bw_ = 0.0;
   double busy_integral_ = 0.0;
   Ns last_occ_change_ = 0;
 };
@@ -262,6 +281,8 @@ class Core {
   void reef_on_flag();
   bool p_flag() const { return p_flag_; }
   double scenario_hbm() const { return sc_.gpu.hbm_bandwidth; }
+  bool memory_tier() const { return mem_.has_value(); }
+  Ns wave_memory_extra(const Instance& i);
 
   void emit(Ns ts, EventKind k, int stream, std::int32_t kernel, Detail d, std::int64_t a = 0,
             std::int64_t b = 0, double g = 0.0) {
@@ -362,6 +383,7 @@ class Core {
   Ns reef_gate_ = 0;
 
   std::optional<PreemptionRecord> pending_preempt_;
+  std::optional<MemoryManager> mem_;
   RunArtifacts art_;
 
   std::int32_t id_scheduler_ = 0, id_resync_ = 0, id_empty_ = 0;
@@ -432,8 +454,10 @@ void SimDevice::dispatch_wave(Instance& i, std::int64_t n) {
   note_occupancy(now);
   const KernelRt& k = core_.krt(i.kernel);
   const double own_bw = static_cast<double>(n) * k.bw;
-  const double stretch = std::max(1.0, (wave_bw_ + own_bw) / core_.scenario_hbm());
-  Ns wave_time = static_cast<Ns>(static_cast<double>(i.block_time) * stretch);
+  const double stretch = std::max(1.0, (bw_demand(now) + own_bw) / core_.scenario_hbm());
+  Ns extra = 0;
+  if (i.prio == Priority::Low && core_.memory_tier()) extra = core_.wave_memory_extra(i);
+  Ns wave_time = static_cast<Ns>(static_cast<double>(i.block_time) * stretch) + extra;
   if (wave_time < 1) wave_time = 1;
 
   if (i.state == InstState::Queued) i.state = InstState::Running;
@@ -550,8 +574,6 @@ void Core::build_plans() {
 }
 
 void Core::setup() {
-  if (sc_.mem.enabled)
-    throw ValidationError("memory", "the memory tier is not part of this build's preemption path");
   dev_.init(static_cast<std::int64_t>(sc_.gpu.n_sm) * sc_.gpu.sm_max_threads);
   art_.policy = policy_;
   art_.scenario = sc_.name;
@@ -593,6 +615,20 @@ void Core::setup() {
       dev_.streams.push_back(StreamRt{t.index, want, {}});
       (want == Priority::High ? hp_tasks_ : lp_tasks_).push_back(t.index);
     }
+  }
+
+  if (sc_.mem.enabled) {  // engine.hpp:398-411: HP chunks first (pinned), then LP
+    mem_.emplace(sc_.gpu, sc_.mem);
+    std::vector<ChunkRelocation> moves;
+    for (const auto* group : {&hp_tasks_, &lp_tasks_})
+      for (int ti : *group)
+        tasks_[ti].chunk_ids = mem_->allocate(ti, tasks_[ti].spec->priority, tasks_[ti].spec->memory_footprint,
+                                              0, &moves);
+    if (!moves.empty()) {
+      const std::int32_t chunk = art_.timeline.intern("chunk");
+      for (const ChunkRelocation& m : moves) emit(0, EventKind::Evict, -1, chunk, Detail::Chunk, m.chunk_id);
+    }
+    if (!sc_.gpu.nvlink_peers.empty()) eq_.push(0, kPrioInfra, -1, EvType::ProbeTick, 0, 0);
   }
 
   if (traits_.harvest) build_plans();
@@ -865,6 +901,32 @@ void Core::on_kernel_done(int id) {
   }
 }
 
+// engine.hpp:1199-1229: an LP wave touches accesses_per_wave keyed-random chunks of its
+// task; off-device chunks add their transfer latency (the wave waits for the slowest) and
+// peer transfers load the link (congestion) and HBM (the DMA engine's nominal rate).
+Ns Core::wave_memory_extra(const Instance& i) {
+  const TaskRt& t = tasks_[i.task];
+  if (t.chunk_ids.empty()) return 0;
+  const std::uint64_t wave_key = hash_combine(i.uid, static_cast<std::uint64_t>(i.blocks_dispatched) * 977);
+  const std::uint64_t n_chunks = t.chunk_ids.size();
+  Ns worst = 0;
+  for (int a = 0; a < sc_.mem.accesses_per_wave; ++a) {
+    const std::int64_t cid =
+        t.chunk_ids[splitmix64(hash_combine(wave_key, static_cast<std::uint64_t>(a))) % n_chunks];
+    const AccessResult r = mem_->access(cid, now_);
+    if (r.tier == Tier::Local) continue;
+    emit(now_, EventKind::MemFault, i.stream, kernels_[i.kernel].name_id, Detail::MemFault, cid,
+         r.tier == Tier::Peer ? 1 : 2);
+    if (r.tier == Tier::Peer) {
+      const Ns dur = std::max<Ns>(r.latency, 1);
+      mem_->congestion().add_transfer(r.peer, static_cast<double>(kChunkBytes) / to_sec(dur), now_ + dur);
+      dev_.add_transfer(now_ + dur, sc_.gpu.nvlink_peers[static_cast<std::size_t>(r.peer)].bandwidth);
+    }
+    worst = std::max(worst, r.latency);
+  }
+  return worst;
+}
+
 void Core::evict(Instance& i, Ns at) {
   const bool counted = i.state != InstState::Evicted;
   i.state = InstState::Evicted;
@@ -1115,9 +1177,18 @@ RunArtifacts Core::run() {
         UtilSample s;
         s.ts = now_;
         s.sm_active = static_cast<double>(dev_.busy_threads()) / static_cast<double>(dev_.total_threads());
-        s.hbm_bw = std::min(1.0, dev_.bw_demand() / sc_.gpu.hbm_bandwidth);
+        s.hbm_bw = std::min(1.0, dev_.bw_demand(now_) / sc_.gpu.hbm_bandwidth);
         art_.util_samples.push_back(s);
         eq_.push(now_ + opts_.util_sample_period, kPrioInfra, -1, EvType::UtilTick, 0, 0);
+        break;
+      }
+      case EvType::ProbeTick: {  // engine.hpp:1263-1276: 10 ms while any link is congested
+        CongestionTable& links = mem_->congestion();
+        for (std::size_t l = 0; l < links.size(); ++l) {
+          const double score = links.probe(static_cast<int>(l), now_);
+          emit(now_, EventKind::Probe, -1, 0, Detail::Probe, static_cast<std::int64_t>(l), 0, score);
+        }
+        eq_.push(now_ + (links.any_score_above(1.2) ? ms(10) : ms(100)), kPrioInfra, -1, EvType::ProbeTick, 0, 0);
         break;
       }
     }

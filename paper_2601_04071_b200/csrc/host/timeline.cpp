@@ -140,6 +140,16 @@ static void render_detail(const Timeline& tl, const TimelineRecord& r, std::stri
       out += "chunk=";
       put_int(out, r.a);
       return;
+    case Detail::MemFault:
+      out += r.b == 1 ? "tier=peer;chunk=" : "tier=dram;chunk=";
+      put_int(out, r.a);
+      return;
+    case Detail::Probe:
+      out += "link=";
+      put_int(out, r.a);
+      out += ";score=";
+      put_g(out, r.g);
+      return;
   }
 }
 

@@ -108,7 +108,29 @@ def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
     return sc
 
 
-CONFIGS = {"cfg1": config1, "cfg4": config4}
+def config_memory(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, rate: float = 20.0,
+                  hp_gb: float = 60.0, lp_gb: tuple = (90.0, 60.0), hbm_gb: float = 180.0,
+                  peer_free_gb: tuple = (40.0,) * 7, peer_load: tuple = (6e11, 0, 0, 3e11, 0, 0, 0),
+                  eviction: str = "contention_first", accesses_per_wave: int = 4) -> dict:
+    """Memory-intensive case on one B200 of an
+    HGX node: config 4's tenants with footprints that overflow the 180 GB HBM (HP 60 GB
+    pinned local; LP 150 GB, ~30 GB of it spilled), 7 NVLink-5 peers behind NVSwitch
+    (900 GB/s each way, ~2 us zero-load latency), two of them carrying background traffic,
+    DRAM as the last tier.  LP waves pay for their off-device chunks (engine.hpp:1199-1229);
+    contention-first eviction steers spills away from the loaded links."""
+    sc = config4(seed, horizon_s, calib, rate)
+    sc["name"] = f"memory_{eviction}"
+    sc["gpu"]["nvlink_peers"] = [{"peer_id": i + 1, "baseline_latency": _dur(2000), "bandwidth": 900e9,
+                                  "background_load": float(peer_load[i])} for i in range(len(peer_free_gb))]
+    sc["memory"] = {"hbm_gb": hbm_gb, "peer_links": [{"free_gb": g} for g in peer_free_gb],
+                    "probe_mb": 4.0, "score_threshold": 1.5, "eviction": eviction,
+                    "accesses_per_wave": accesses_per_wave}
+    for t in sc["tasks"]:
+        t["memory_footprint_gb"] = hp_gb if t["priority"] == "high" else lp_gb[0 if t["name"] == "lp_gemm" else 1]
+    return sc
+
+
+CONFIGS = {"cfg1": config1, "cfg4": config4, "memory": config_memory}
 
 
 def with_seed(sc: dict, seed: int) -> dict:

@@ -19,7 +19,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 
 from oracle import ref as R  # noqa: E402
 from paper_2601_04071_b200 import scenarios as S  # noqa: E402
-from scenario_gen import random_scenario  # noqa: E402
+from scenario_gen import random_memory_scenario, random_scenario  # noqa: E402
 
 GPU_A100 = {"n_sm": 108, "sm_max_threads": 2048, "hbm_bandwidth": 2e12,
             "launch_overhead": {"value": 7, "unit": "us"}, "sync_overhead": {"value": 5, "unit": "us"}}
@@ -93,6 +93,10 @@ def digests() -> dict:
              "cfg4_seed1_0p2s": S.config4(seed=1, horizon_s=0.2)}
     for seed in range(40):
         cases[f"rand{seed}"] = random_scenario(1000 + seed)
+    for seed in range(12):
+        cases[f"mem{seed}"] = random_memory_scenario(2000 + seed)
+    for ev in ("contention_first", "round_robin"):
+        cases[f"memory_{ev}_0p3s"] = S.config_memory(seed=1, horizon_s=0.3, eviction=ev)
     for name, sc in cases.items():
         out[name] = {"scenario": sc, "policies": {}}
         for pol in ("exclusive", "exclusive_lp", "splitkernel", "spatial", "reef"):

@@ -98,3 +98,32 @@ def random_scenario(seed: int, horizon_ms: float | None = None) -> dict:
                         "square_tiling": rng.random() < 0.3, "consolidation": rng.random() < 0.8},
           "reef": {"queue_cap": rng.randint(1, 4), "evict_cost_us": rng.choice([0, 1, 3])}}
     return sc
+
+
+def random_memory_scenario(seed: int) -> dict:
+    """random_scenario + the memory tier (engine.hpp:396-411, 1199-1276): task footprints
+    that overflow a small local HBM, 0-3 NVLink peers with background load and limited
+    free space, contention-first or round-robin eviction, 0-6 accesses per wave."""
+    sc = random_scenario(seed)
+    rng = random.Random(seed * 7919 + 13)
+    n_peers = rng.choice([0, 1, 2, 3])
+    sc["gpu"]["nvlink_peers"] = [
+        {"peer_id": p + 1, "baseline_latency": _dur(rng.randint(500, 5000)),
+         "bandwidth": rng.choice([5e10, 4.5e11, 9e11]),
+         "background_load": rng.choice([0.0, 0.0, 1e11, 6e11, 2e12])} for p in range(n_peers)]
+    if rng.random() < 0.5:
+        sc["gpu"]["dram_latency_factor"] = rng.choice([1.0, 2.5, 8.0])
+    hbm = rng.choice([0.05, 0.2, 1.0, 80.0])
+    sc["memory"] = {"hbm_gb": hbm,
+                    "peer_links": [{"free_gb": rng.choice([0.0, 0.01, 0.1, 5.0])} for _ in range(n_peers)],
+                    "probe_mb": rng.choice([1.0, 4.0, 16.0]),
+                    "score_threshold": rng.choice([1.05, 1.5, 3.0]),
+                    "eviction": rng.choice(["contention_first", "round_robin"]),
+                    "accesses_per_wave": rng.randint(0, 6)}
+    if rng.random() < 0.5:
+        sc["memory"]["dram_factor"] = rng.choice([1.0, 4.0, 10.0])
+    for t in sc["tasks"]:
+        if rng.random() < 0.85:
+            limit = hbm * (0.6 if t["priority"] == "high" else 3.0)
+            t["memory_footprint_gb"] = round(rng.uniform(0.0, limit), 4)
+    return sc

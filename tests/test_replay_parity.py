@@ -11,7 +11,7 @@ from pathlib import Path
 
 import pytest
 
-from scenario_gen import random_scenario
+from scenario_gen import random_memory_scenario, random_scenario
 
 GOLD = json.loads((Path(__file__).resolve().parent / "golden" / "replay_digests.json").read_text())
 POLICIES = ("exclusive", "exclusive_lp", "splitkernel", "spatial", "reef")
@@ -49,6 +49,29 @@ def test_replay_differential_random(ms, ref, block):
                 assert str(ei.value) in str(e)
                 continue
             assert _strip(ms.run_scenario(sc, pol)) == want, (seed, pol)
+
+
+@pytest.mark.parametrize("block", range(3))
+def test_replay_memory_tier_differential(ms, ref, block):
+    """Memory tier (memory.hpp; engine.hpp:396-411, 798-801, 1199-1276): chunk placement,
+    HP displacement errors, peer / DRAM faults, link congestion, ProbeTick cadence —
+    NDJSON byte-equal with the compiled reference."""
+    faults = 0
+    for seed in range(block * 40, block * 40 + 40):
+        sc = random_memory_scenario(seed)
+        for pol in POLICIES:
+            try:
+                want = ref.run_scenario(sc, pol, ndjson=True)
+            except ref.RefError as e:
+                with pytest.raises((ms.ValidationError, ms.EngineError)) as ei:
+                    ms.run_scenario(sc, pol)
+                assert str(ei.value) in str(e)
+                continue
+            got = ms.run_scenario(sc, pol, ndjson=True)
+            faults += want["ndjson"].count('"mem_fault"')
+            assert got["ndjson"] == want["ndjson"], (seed, pol)
+            assert _strip(got) == _strip(want), (seed, pol)
+    assert faults > 0
 
 
 def test_replay_ndjson_bytes_and_options(ms, ref):
