@@ -34,7 +34,7 @@ build/cuda/%.o: $(PKG)/csrc/cuda/%.cu $(CUDA_HDR) include/ms_b200.h
 	@mkdir -p build/cuda
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/cuda/$*.ptxas.txt || (cat build/cuda/$*.ptxas.txt; exit 1)
 
-build/live/%.o: $(PKG)/csrc/live/%.cpp $(wildcard include/microslice/*.hpp) $(wildcard $(PKG)/csrc/live/*.hpp) include/ms_b200.h include/ms_live.h include/ms_session.h
+build/live/%.o: $(PKG)/csrc/live/%.cpp $(wildcard include/microslice/*.hpp) $(wildcard $(PKG)/csrc/live/*.hpp) include/ms_b200.h include/ms_live.h include/ms_session.h include/ms_tier.h
 	@mkdir -p build/live
 	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
 

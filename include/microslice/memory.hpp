@@ -6,12 +6,13 @@
 // wave_memory_extra, 1263-1276 ProbeTick).  The public surface is source-compatible with
 // the reference; implementation in paper_2601_04071_b200/csrc/host/memory.cpp.
 //
-// On B200 the same placement decisions drive the live tier (include/ms_b200.h,
-// ms_mem_*): chunks are real 2 MB allocations in local HBM, a peer's HBM (NVLink 5 /
-// NVSwitch, cudaDeviceEnablePeerAccess) or pinned host memory.
+// On B200 the same placement decisions drive the live tier (include/ms_tier.h,
+// csrc/live/mem_tier.cpp): chunks are real 2 MB VMM allocations in local HBM, a peer's
+// HBM (NVLink 5 / NVSwitch) or pinned host DRAM, mapped into one virtual range per buffer.
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <utility>
 #include <vector>
@@ -42,8 +43,13 @@ struct ChunkRelocation {
   int to_peer = -1;
 };
 
+/// Live link measurement: ns to move `bytes` over link `link` now (B200 tier: a timed
+/// copy).  Absent in replay, where latency follows the load model below.
+using LiveProbe = std::function<Ns(int link, std::int64_t bytes)>;
+
 /// Per-link congestion: a calibrated zero-load probe latency t_base and the load seen
 /// through registered transfers (+ configured background traffic); score = t_now / t_base.
+/// With a LiveProbe, t_base and t_now are measured instead (extension for the live tier).
 class CongestionTable {
  public:
   struct Link {
@@ -54,6 +60,7 @@ class CongestionTable {
   };
 
   void init(const std::vector<NvlinkPeer>& peers, double probe_bytes);
+  void set_live_probe(LiveProbe f) { live_ = std::move(f); }
   std::size_t size() const { return links_.size(); }
   const Link& link(int i) const { return links_.at(static_cast<std::size_t>(i)); }
 
@@ -72,6 +79,7 @@ class CongestionTable {
   double probe_bytes_ = 4.0 * 1024 * 1024;
   std::vector<Link> links_;
   std::vector<double> scores_;
+  LiveProbe live_;
 };
 
 struct AccessResult {
@@ -83,6 +91,8 @@ struct AccessResult {
 class MemoryManager {
  public:
   MemoryManager(const GpuConfig& gpu, const MemParams& params);
+  /// Live tier: link latencies come from `live` (calibrated at construction).
+  MemoryManager(const GpuConfig& gpu, const MemParams& params, LiveProbe live);
 
   struct Destination {
     Tier tier = Tier::Dram;
@@ -105,6 +115,9 @@ class MemoryManager {
   /// Extra latency of a kernel of the owner touching `chunk_id` now.
   AccessResult access(std::int64_t chunk_id, Ns now);
   bool chunk_pinned(std::int64_t id) const { return chunks_.at(static_cast<std::size_t>(id)).pinned; }
+  /// Return chunks to their tier (live tier: ms_tier_free).  Released chunks keep their
+  /// ids with owner_task = -1 and count against no tier.
+  void release(const std::vector<std::int64_t>& ids);
 
  private:
   void place(Chunk& c, const Destination& d);

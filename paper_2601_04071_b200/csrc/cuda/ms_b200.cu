@@ -801,6 +801,7 @@ int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after
 extern "C" {
 
 const char* ms_last_error(void) { return g_err.c_str(); }
+int ms_internal_fail(int code, const char* what) { return fail(code, what ? what : ""); }
 int64_t ms_host_now_ns(void) { return now_ns(); }
 
 int ms_dev_open(int ordinal, ms_dev** out) {

@@ -27,8 +27,10 @@ void CongestionTable::init(const std::vector<NvlinkPeer>& peers, double probe_by
 }
 
 void CongestionTable::calibrate() {  // memory.hpp:60-67: zero-load probe latency
-  for (Link& l : links_) {
-    l.t_base = l.cfg.baseline_latency + static_cast<Ns>(probe_bytes_ / l.cfg.bandwidth * 1e9);
+  for (std::size_t i = 0; i < links_.size(); ++i) {
+    Link& l = links_[i];
+    l.t_base = live_ ? std::max<Ns>(1, live_(static_cast<int>(i), static_cast<std::int64_t>(probe_bytes_)))
+                     : l.cfg.baseline_latency + static_cast<Ns>(probe_bytes_ / l.cfg.bandwidth * 1e9);
     l.calibrated = true;
   }
 }
@@ -64,7 +66,8 @@ double CongestionTable::probe(int link, Ns now) {  // memory.hpp:96-109
   if (!l.calibrated)
     throw ValidationError("memory.probe",
                           "link " + std::to_string(link) + " probed before baseline calibration");
-  const Ns t_now = transfer_time(link, static_cast<std::int64_t>(probe_bytes_), now);
+  const Ns t_now = live_ ? live_(link, static_cast<std::int64_t>(probe_bytes_))
+                        : transfer_time(link, static_cast<std::int64_t>(probe_bytes_), now);
   const double score = static_cast<double>(t_now) / static_cast<double>(l.t_base);
   if (scores_.size() < links_.size()) scores_.resize(links_.size(), 1.0);
   scores_[static_cast<std::size_t>(link)] = score;
@@ -82,7 +85,11 @@ bool CongestionTable::any_score_above(double v) const {
 // ------------------------------------------------------------------ MemoryManager
 // memory.hpp:138-323
 
-MemoryManager::MemoryManager(const GpuConfig& gpu, const MemParams& params) : gpu_(gpu), params_(params) {
+MemoryManager::MemoryManager(const GpuConfig& gpu, const MemParams& params)
+    : MemoryManager(gpu, params, LiveProbe{}) {}
+
+MemoryManager::MemoryManager(const GpuConfig& gpu, const MemParams& params, LiveProbe live)
+    : gpu_(gpu), params_(params) {
   local_capacity_ = static_cast<std::int64_t>(params.hbm_gb * 1e9 / kChunkBytes);
   const std::size_t n = gpu.nvlink_peers.size();
   peer_capacity_.assign(n, 0);
@@ -90,6 +97,7 @@ MemoryManager::MemoryManager(const GpuConfig& gpu, const MemParams& params) : gp
   for (std::size_t i = 0; i < n && i < params.peer_free_gb.size(); ++i)
     peer_capacity_[i] = static_cast<std::int64_t>(params.peer_free_gb[i] * 1e9 / kChunkBytes);
   links_.init(gpu.nvlink_peers, params.probe_mb * 1024 * 1024);
+  links_.set_live_probe(std::move(live));
   links_.calibrate();
 }
 
@@ -196,6 +204,17 @@ std::vector<std::int64_t> MemoryManager::allocate(int task, Priority prio, std::
     ids.push_back(static_cast<std::int64_t>(chunks_.size()) - 1);
   }
   return ids;
+}
+
+void MemoryManager::release(const std::vector<std::int64_t>& ids) {
+  for (std::int64_t id : ids) {
+    Chunk& c = chunks_.at(static_cast<std::size_t>(id));
+    if (c.owner_task < 0) continue;
+    if (c.tier == Tier::Local) --local_used_;
+    if (c.tier == Tier::Peer) --peer_used_[static_cast<std::size_t>(c.peer)];
+    c = Chunk{};
+    c.tier = Tier::Dram;  // never a displacement victim again
+  }
 }
 
 // memory.hpp:313-321: one chunk over the first peer link at zero load (or 2 us + 600 GB/s)

@@ -17,7 +17,7 @@ def declared(header: str) -> set[str]:
 
 
 @pytest.mark.parametrize("lib,headers", [("libmicroslice.so", ["ms_replay.h"]),
-                                         ("libms_b200.so", ["ms_b200.h", "ms_live.h", "ms_session.h"])])
+                                         ("libms_b200.so", ["ms_b200.h", "ms_live.h", "ms_session.h", "ms_tier.h"])])
 def test_exports_every_declared_symbol(lib, headers):
     so = C.CDLL(str(LIB / lib))
     names = set().union(*(declared(h) for h in headers))

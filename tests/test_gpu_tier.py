@@ -1,0 +1,101 @@
+"""Live memory tier on B200 (include/ms_tier.h): LP buffers that
+overflow the tier's HBM budget spill 2 MB chunks to host DRAM (no NVLink peer on a 1-GPU
+box) inside ONE virtual range, the unmodified preemptible LP streamer computes on them
+bit-exactly, and an HP allocation displaces LP chunks (priority isolation) without
+changing a byte the LP tenant sees.  Placement decisions = MemoryManager (the replay
+engine's code, parity-tested against the reference in test_replay_parity.py)."""
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+CHUNK = 2 << 20
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2601_04071_b200.device import Device
+    d = Device(0)
+    yield d
+    d.close()
+
+
+def d2h(dev, ptr, n):
+    out = np.empty(n, np.uint16)
+    dev.d2h(out.ctypes.data, ptr, n * 2)
+    return out
+
+
+def run_preempted(dev, k, preemptions=3):
+    begin = 0
+    for i in range(100):
+        dev.lp_run(k, begin, k.total_tiles)
+        if i < preemptions:
+            time.sleep(50e-6)
+            dev.preempt_raise()
+        st = dev.lp_wait(k, 60)
+        begin = st["cursor"]
+        if begin >= k.total_tiles:
+            return i + 1
+    raise AssertionError("LP run did not finish")
+
+
+def test_tier_spill_relocation_and_axpy_exact(dev):
+    from oracle import tenant as T
+    from paper_2601_04071_b200.tier import MemoryTier
+    n = 1 << 26                                  # 128 MB per bf16 tensor = 64 chunks
+    budget_chunks = int(0.2e9 // CHUNK)          # 95
+    with MemoryTier(dev, {"hbm_gb": 0.2}) as tier:
+        x = tier.alloc(1, 2 * n)
+        y = tier.alloc(1, 2 * n)
+        cx, cy = tier.chunks(x), tier.chunks(y)
+        assert [c[0] for c in cx] == ["local"] * 64
+        n_local_y = budget_chunks - 64
+        assert [c[0] for c in cy] == ["local"] * n_local_y + ["dram"] * (64 - n_local_y)
+        assert not any(c[3] for c in cx + cy)
+        st = tier.stats()
+        assert st["local_used_chunks"] == budget_chunks and st["chunks_dram"] == 64 - n_local_y
+
+        dev.fill_synth(x, n, 9, 1, 1.0)
+        dev.fill_synth(y, n, 9, 2, 1.0)
+        xs, ys = T.synth_bf16(n, 9, 1, 1.0), T.synth_bf16(n, 9, 2, 1.0)
+        k = dev.lp_register_axpy(x, y, n, 1.5)
+        assert run_preempted(dev, k) > 1
+        want = T.axpy(ys, xs, 1.5)
+        assert np.array_equal(d2h(dev, y, n), want)
+
+        # HP allocation with the budget full: pinned local, displaces the 40 oldest LP chunks
+        h = tier.alloc(0, 40 * CHUNK, high_priority=True)
+        assert all(c == ("local", -1, 0, True) for c in tier.chunks(h))
+        cx = tier.chunks(x)
+        assert [c[0] for c in cx[:40]] == ["dram"] * 40 and [c[0] for c in cx[40:]] == ["local"] * 24
+        st = tier.stats()
+        assert st["relocations"] == 40 and st["relocated_bytes"] == 40 * CHUNK
+        assert np.array_equal(d2h(dev, x, n), xs)     # relocation preserved every byte
+        assert np.array_equal(d2h(dev, y, n), want)
+
+        dev.memset(h, 0x5A, 40 * CHUNK)               # HP writes its own chunks only
+        dev.lp_reset(k)
+        run_preempted(dev, k, preemptions=1)
+        assert np.array_equal(d2h(dev, y, n), T.axpy(want, xs, 1.5))
+        assert np.array_equal(d2h(dev, x, n), xs)
+        dev.lp_unregister(k)
+        for p in (x, y, h):
+            tier.free(p)
+        assert tier.stats()["local_used_chunks"] == 0
+
+
+def test_tier_errors(dev):
+    from paper_2601_04071_b200.device import DeviceError
+    from paper_2601_04071_b200.tier import MemoryTier
+    with pytest.raises(DeviceError, match="eviction"):
+        MemoryTier(dev, {"eviction": "lru"})
+    with pytest.raises(DeviceError, match="P2P peer"):
+        MemoryTier(dev, {"peers": [{"device": 0, "free_gb": 1.0}]})
+    with MemoryTier(dev, {"hbm_gb": 0.01}) as tier:   # 4 chunks
+        with pytest.raises(DeviceError, match="no such link"):
+            tier.probe(0)
+        tier.alloc(0, 4 * CHUNK, high_priority=True)
+        with pytest.raises(DeviceError, match="exhausted by pinned"):
+            tier.alloc(0, CHUNK, high_priority=True)
