@@ -51,6 +51,8 @@ typedef struct ms_tier_stats {
   int64_t chunks_local, chunks_peer, chunks_dram;
   int64_t relocations;      /* LP chunks moved out of HBM by HP allocations */
   int64_t relocated_bytes;  /* bytes copied by those moves */
+  int64_t relocate_copy_ns;  /* host time in relocation: granules + staging + copies */
+  int64_t relocate_remap_ns; /* host time in relocation: VA unmap / map / access */
   int64_t probes;           /* live link probes issued */
   int32_t n_links;
   int32_t pad;

@@ -148,32 +148,50 @@ struct ms_tier {
     return va;
   }
 
-  // Move chunk `id` (mapped at its VA) to the tier the manager already recorded for it.
-  void relocate(const ChunkRelocation& m) {
-    // new granule -> temporary VA, copy, then the chunk's own VA is re-pointed at it
-    const CUdeviceptr va = chunk_va.at(m.chunk_id);
-    const CUmemGenericAllocationHandle h = granule(m.to, m.to_peer);
-    const CUdeviceptr tmp = reserve(kChunkBytes);
-    CUresult mapped = vmm.map(tmp, kChunkBytes, 0, h, 0);
+  // Move displaced chunks to the tiers the manager recorded for them, in three batched
+  // phases: new granules mapped side by side in a staging range, one async copy per chunk
+  // and a single sync, then each chunk's VA unmapped and re-pointed at its new granule.
+  void relocate(const std::vector<ChunkRelocation>& moves) {
+    const size_t n = moves.size();
+    const int64_t t0 = mono_ns();
+    std::vector<CUmemGenericAllocationHandle> hs;
+    hs.reserve(n);
+    const CUdeviceptr stage = reserve(n * kChunkBytes);
+    size_t mapped = 0;
+    auto cleanup = [&]() {
+      for (size_t i = 0; i < mapped; ++i) vmm.unmap(stage + i * kChunkBytes, kChunkBytes);
+      vmm.addr_free(stage, n * kChunkBytes);
+      for (CUmemGenericAllocationHandle h : hs) vmm.release(h);
+    };
     try {
-      ck(mapped, "cuMemMap");
-      grant(tmp, kChunkBytes);
-      ck(cudaMemcpy(reinterpret_cast<void*>(tmp), reinterpret_cast<void*>(va), kChunkBytes, cudaMemcpyDefault),
-         "relocation copy");
-      ck(vmm.unmap(va, kChunkBytes), "cuMemUnmap");
-      ck(vmm.map(va, kChunkBytes, 0, h, 0), "cuMemMap");
-      grant(va, kChunkBytes);
+      for (size_t i = 0; i < n; ++i) {
+        hs.push_back(granule(moves[i].to, moves[i].to_peer));
+        ck(vmm.map(stage + i * kChunkBytes, kChunkBytes, 0, hs.back(), 0), "cuMemMap");
+        ++mapped;
+      }
+      grant(stage, n * kChunkBytes);
+      for (size_t i = 0; i < n; ++i)
+        ck(cudaMemcpyAsync(reinterpret_cast<void*>(stage + i * kChunkBytes),
+                           reinterpret_cast<void*>(chunk_va.at(moves[i].chunk_id)), kChunkBytes, cudaMemcpyDefault,
+                           probe_stream),
+           "relocation copy");
+      ck(cudaStreamSynchronize(probe_stream), "relocation sync");
+      const int64_t t1 = mono_ns();
+      for (size_t i = 0; i < n; ++i) {
+        const CUdeviceptr va = chunk_va.at(moves[i].chunk_id);
+        ck(vmm.unmap(va, kChunkBytes), "cuMemUnmap");
+        ck(vmm.map(va, kChunkBytes, 0, hs[i], 0), "cuMemMap");
+        grant(va, kChunkBytes);
+      }
+      stats.relocate_copy_ns += t1 - t0;
+      stats.relocate_remap_ns += mono_ns() - t1;
     } catch (...) {
-      if (mapped == CUDA_SUCCESS) vmm.unmap(tmp, kChunkBytes);
-      vmm.addr_free(tmp, kChunkBytes);
-      vmm.release(h);
+      cleanup();
       throw;
     }
-    vmm.unmap(tmp, kChunkBytes);
-    vmm.addr_free(tmp, kChunkBytes);
-    vmm.release(h);
-    ++stats.relocations;
-    stats.relocated_bytes += kChunkBytes;
+    cleanup();
+    stats.relocations += static_cast<int64_t>(n);
+    stats.relocated_bytes += static_cast<int64_t>(n) * kChunkBytes;
   }
 
   // Timed copy of `bytes` to link's probe buffer on the lowest-priority stream.
@@ -305,7 +323,7 @@ extern "C" int ms_tier_alloc(ms_tier* t, int task, int high_priority, uint64_t b
         t->mm->allocate(task, prio, static_cast<std::int64_t>(bytes), mono_ns(), &moves);
     if (!moves.empty()) {
       ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize (before relocation)");
-      for (const ChunkRelocation& m : moves) t->relocate(m);
+      t->relocate(moves);
     }
     Buffer b;
     b.bytes = ids.size() * static_cast<size_t>(kChunkBytes);

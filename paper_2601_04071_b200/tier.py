@@ -24,7 +24,8 @@ class TierChunk(C.Structure):
 class TierStats(C.Structure):
     _fields_ = [("local_capacity_chunks", C.c_int64), ("local_used_chunks", C.c_int64),
                 ("chunks_local", C.c_int64), ("chunks_peer", C.c_int64), ("chunks_dram", C.c_int64),
-                ("relocations", C.c_int64), ("relocated_bytes", C.c_int64), ("probes", C.c_int64),
+                ("relocations", C.c_int64), ("relocated_bytes", C.c_int64), ("relocate_copy_ns", C.c_int64),
+                ("relocate_remap_ns", C.c_int64), ("probes", C.c_int64),
                 ("n_links", C.c_int32), ("pad", C.c_int32)]
 
 

@@ -48,7 +48,8 @@ def main():
     dt = time.perf_counter() - t0
     st = tier.stats()
     out["relocation"] = {"chunks": st["relocations"], "ms": dt * 1e3,
-                         "gb_s": st["relocated_bytes"] / dt / 1e9, "us_per_chunk": dt * 1e6 / max(1, st["relocations"])}
+                         "gb_s": st["relocated_bytes"] / dt / 1e9, "us_per_chunk": dt * 1e6 / max(1, st["relocations"]),
+                         "copy_ms": st["relocate_copy_ns"] / 1e6, "remap_ms": st["relocate_remap_ns"] / 1e6}
     print(json.dumps(out["relocation"]), flush=True)
     tier.close()
     dev.close()
