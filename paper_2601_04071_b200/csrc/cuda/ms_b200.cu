@@ -123,6 +123,9 @@ struct LpSlot {
   uint64_t last_begin = 0, last_end = 0, last_redo_in = 0;
   int64_t t_launch_host = 0;
   bool launched = false;
+  uint8_t* slow = nullptr;          // streamer off-device tile groups (ms_lp_set_slow_tiles)
+  unsigned int* slow_sem = nullptr;
+  int slow_group = 0, slow_max = 0;
 };
 
 struct HpOpRt {
@@ -985,9 +988,34 @@ int ms_lp_unregister(ms_dev* d, int id) {
     if (r) cudaFree(r);
     r = nullptr;
   }
+  if (s.slow) cudaFree(s.slow);
+  if (s.slow_sem) cudaFree(s.slow_sem);
   const uint64_t keep_run_id = s.run_id;  // run ids stay monotonic per slot (exit records)
   s = LpSlot{};
   s.run_id = keep_run_id;
+  return 0;
+}
+
+int ms_lp_set_slow_tiles(ms_dev* d, int id, const uint8_t* slow_groups, uint64_t n_groups, int tiles_per_group,
+                         int max_inflight) {
+  if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
+  LpSlot& s = d->lp_slots[id];
+  if (s.desc.kind != MS_LP_AXPY) return fail(MS_E_ARG, "slow-tile admission is a streamer (MS_LP_AXPY) option");
+  MS_CUDA(cudaStreamSynchronize(d->lp));
+  if (s.slow) cudaFree(s.slow);
+  s.slow = nullptr;
+  if (!slow_groups || n_groups == 0) return 0;  // disable
+  if (tiles_per_group <= 0 || max_inflight <= 0) return fail(MS_E_ARG, "tiles_per_group and max_inflight must be > 0");
+  if (n_groups * static_cast<uint64_t>(tiles_per_group) < s.total_tiles)
+    return fail(MS_E_ARG, "slow-tile map does not cover the kernel's tiles");
+  MS_CUDA(cudaMalloc(&s.slow, n_groups));
+  MS_CUDA(cudaMemcpy(s.slow, slow_groups, n_groups, cudaMemcpyHostToDevice));
+  if (!s.slow_sem) {
+    MS_CUDA(cudaMalloc(&s.slow_sem, sizeof(unsigned int)));
+    MS_CUDA(cudaMemset(s.slow_sem, 0, sizeof(unsigned int)));
+  }
+  s.slow_group = tiles_per_group;
+  s.slow_max = max_inflight;
   return 0;
 }
 
@@ -1060,6 +1088,10 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   p.alpha = s.desc.alpha;
   p.n = static_cast<unsigned long long>(s.desc.n_elems);
   p.tile_elems = s.desc.tile_elems;
+  p.slow = s.slow;
+  p.slow_sem = s.slow_sem;
+  p.slow_group = s.slow_group;
+  p.slow_max = s.slow_max;
   const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve)) * s.desc.ctas_per_sm;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
   const int vpt = s.desc.tile_elems / (kStreamThreads * 8);

@@ -25,6 +25,13 @@ struct StreamParams {
   float alpha;
   unsigned long long n;
   int tile_elems;  // multiple of 256 * 8
+  // Off-device admission (memory tier, ms_lp_set_slow_tiles): tiles of group
+  // t / slow_group with slow[group] != 0 touch host-DRAM / peer chunks; at most slow_max of
+  // them are in flight device-wide (slow_sem), so a preemption drains at most
+  // slow_max tiles over the slow link instead of one per CTA.
+  const uint8_t* slow;
+  unsigned int* slow_sem;
+  int slow_group, slow_max;
 };
 
 constexpr int kStreamThreads = 256;  // streaming warps 0-7; warp 8 = mirror poller; warp 9 = host poller (CTA 0)
@@ -76,9 +83,26 @@ __global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __gr
   } else {
     const int tid = threadIdx.x;
     for (int j = 0;; ++j) {
+      bool slow_held = false;
       if (tid == 0) {
         long long t = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&preempt))) t = claim_tile(p.run);
+        if (t >= 0 && p.slow && p.slow[t / p.slow_group]) {
+          // admission: wait for one of slow_max slots; a preemption meanwhile parks the tile
+          for (;;) {
+            if (atomicAdd(p.slow_sem, 1u) < static_cast<unsigned>(p.slow_max)) {
+              slow_held = true;
+              break;
+            }
+            atomicSub(p.slow_sem, 1u);
+            if (p.run.preemptible && ld_volatile_smem(&preempt)) {
+              push_redo(p.run, static_cast<unsigned long long>(t));
+              t = -1;
+              break;
+            }
+            __nanosleep(256);
+          }
+        }
         tile_sh[j & 1] = t;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
@@ -106,6 +130,11 @@ __global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __gr
         o.z = axpy2(p.alpha, xv[v].z, yv[v].z);
         o.w = axpy2(p.alpha, xv[v].w, yv[v].w);
         st_stream(p.y + e, o);
+      }
+      if (p.slow) {
+        // every thread's slow-tile loads have returned once all reach this barrier
+        asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
+        if (slow_held) atomicSub(p.slow_sem, 1u);
       }
       if (tid == 0) ++tiles_done;
     }

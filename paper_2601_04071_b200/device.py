@@ -79,6 +79,7 @@ def lib() -> C.CDLL:
             "ms_fill_synth_bf16": (I, [P, U64, U64, U64, U64, F]),
             "ms_lp_register": (I, [P, C.POINTER(LpDesc), C.POINTER(I), C.POINTER(U64)]),
             "ms_lp_run": (I, [P, I, U64, U64, U64]), "ms_lp_set_budget": (I, [P, I, U64]),
+            "ms_lp_set_slow_tiles": (I, [P, I, C.c_char_p, U64, I, I]),
             "ms_lp_poll": (I, [P, I, C.POINTER(LpStatus)]),
             "ms_lp_wait": (I, [P, I, I64, C.POINTER(LpStatus)]), "ms_lp_reset": (I, [P, I]),
             "ms_preempt_raise": (I, [P, C.POINTER(U32), C.POINTER(I64)]), "ms_preempt_epoch": (U32, [P]),
@@ -192,6 +193,15 @@ class Device:
         kid, tiles = C.c_int(), C.c_uint64()
         _ck(lib().ms_lp_register(self._h, C.byref(d), C.byref(kid), C.byref(tiles)))
         return LpKernel(kid.value, tiles.value)
+
+    def lp_set_slow_tiles(self, k: LpKernel, slow_groups, tiles_per_group: int, max_inflight: int = 8):
+        """Memory tier: bound the streamer's in-flight tiles over off-device chunks
+        (include/ms_b200.h ms_lp_set_slow_tiles).  slow_groups=None disables."""
+        if slow_groups is None:
+            _ck(lib().ms_lp_set_slow_tiles(self._h, k.id, None, 0, 0, 0))
+            return
+        b = bytes(1 if g else 0 for g in slow_groups)
+        _ck(lib().ms_lp_set_slow_tiles(self._h, k.id, b, len(b), tiles_per_group, max_inflight))
 
     def lp_unregister(self, k: LpKernel):
         _ck(lib().ms_lp_unregister(self._h, k.id))

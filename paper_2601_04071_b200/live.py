@@ -142,31 +142,37 @@ class Config4:
     N_LP = 8192
     N_EW = 1 << 30
 
-    def __init__(self, dev: Device, seed: int = SEED, m: int | None = None):
+    def __init__(self, dev: Device, seed: int = SEED, m: int | None = None, tier=None, slow_max: int = 8):
+        """tier: a MemoryTier (tier.py) to place the tenants' memory through — HP buffers
+        and weights pinned (task 0), LP GEMM (task 1) and streamer (task 2) spillable, in
+        that allocation order (the memory-intensive case)."""
         self.dev = dev
         if m is not None:
             self.M = m
+        hp_alloc = (lambda nb: tier.alloc(0, nb, high_priority=True)) if tier else dev.alloc
+        gemm_alloc = (lambda nb: tier.alloc(1, nb)) if tier else dev.alloc
+        ew_alloc = (lambda nb: tier.alloc(2, nb)) if tier else dev.alloc
         M, H, Q, F, V = self.M, self.H, self.Q, self.F, self.V
-        self.bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
+        self.bufs = [hp_alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
         dev.fill_synth(self.bufs[0], M * H, seed, 400, 1.0)
         self.weights = []
         for l in range(self.LAYERS):
             ws = []
             for j, (n, k) in enumerate([(Q, H), (H, H), (2 * F, H), (H, F)]):
-                p = dev.alloc(n * k * 2)
+                p = hp_alloc(n * k * 2)
                 dev.fill_synth(p, n * k, seed, 401 + 4 * l + j, 1.0 / math.sqrt(k))
                 ws.append(p)
             self.weights.append(ws)
-        self.lm = dev.alloc(V * H * 2)
+        self.lm = hp_alloc(V * H * 2)
         dev.fill_synth(self.lm, V * H, seed, 499, 1.0 / math.sqrt(H))
         self.chain = dev.hp_register_chain(decode_step_ops(M, H, Q, F, V, self.LAYERS, self.bufs,
                                                            self.weights, self.lm))
         n = self.N_LP
-        self.a, self.b, self.c = dev.alloc(n * n * 2), dev.alloc(n * n * 2), dev.alloc(n * n * 2)
+        self.a, self.b, self.c = gemm_alloc(n * n * 2), gemm_alloc(n * n * 2), gemm_alloc(n * n * 2)
         dev.fill_synth(self.a, n * n, seed, 1, 1.0)
         dev.fill_synth(self.b, n * n, seed, 2, 1.0 / math.sqrt(n))
         self.lp_gemm = dev.lp_register_gemm(self.a, self.b, self.c, n, n, n, block_n=256)
-        self.x, self.y = dev.alloc(self.N_EW * 2), dev.alloc(self.N_EW * 2)
+        self.x, self.y = ew_alloc(self.N_EW * 2), ew_alloc(self.N_EW * 2)
         dev.fill_synth(self.x, self.N_EW, seed, 21, 1.0)
         dev.fill_synth(self.y, self.N_EW, seed, 22, 1.0)
         # 8192-element tiles (7.0 TB/s).  4096 cut the preemption drain from ~11 to ~8 us and the
@@ -174,6 +180,10 @@ class Config4:
         # LP ~90 instead of ~78 SMs and HP SLO attainment fell 4-9 points below exclusive in
         # three runs (tools/axpy_probe.py, tools/policy_compare.py)
         self.lp_axpy = dev.lp_register_axpy(self.x, self.y, self.N_EW, 0.5, tile_elems=8192)
+        if tier is not None and slow_max:
+            slow = tier.off_device(self.x, self.y)
+            if any(slow):  # bound the drain over PCIe / NVLink (ms_lp_set_slow_tiles)
+                dev.lp_set_slow_tiles(self.lp_axpy, slow, tier.CHUNK // (2 * 8192), slow_max)
         self.calib = None
 
     @property

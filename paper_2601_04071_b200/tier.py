@@ -66,6 +66,12 @@ class MemoryTier:
         _ck(_lib().ms_tier_chunks(self._h, ptr, arr, n))
         return [(TIERS[c.tier], c.peer, c.owner, bool(c.pinned)) for c in arr]
 
+    def off_device(self, *ptrs: int) -> list[bool]:
+        """Per 2 MB chunk index: True when that chunk of ANY of the equally sized buffers
+        lives off the device (the streamer's slow-tile map, ms_lp_set_slow_tiles)."""
+        maps = [[c[0] != "local" for c in self.chunks(p)] for p in ptrs]
+        return [any(col) for col in zip(*maps)]
+
     def probe(self, link: int) -> tuple[float, int]:
         s, t = C.c_double(), C.c_int64()
         _ck(_lib().ms_tier_probe(self._h, link, C.byref(s), C.byref(t)))

@@ -80,6 +80,17 @@ def test_tier_spill_relocation_and_axpy_exact(dev):
         run_preempted(dev, k, preemptions=1)
         assert np.array_equal(d2h(dev, y, n), T.axpy(want, xs, 1.5))
         assert np.array_equal(d2h(dev, x, n), xs)
+        # bounded off-device admission: same bytes, preempted mid-run
+        slow = tier.off_device(x, y)
+        assert sum(slow) == len(set(range(40)) | set(range(n_local_y, 64)))
+        ys2 = d2h(dev, y, n)
+        dev.lp_set_slow_tiles(k, slow, CHUNK // (2 * 8192), 2)
+        dev.lp_reset(k)
+        assert run_preempted(dev, k, preemptions=4) > 1
+        assert np.array_equal(d2h(dev, y, n), T.axpy(ys2, xs, 1.5))
+        with pytest.raises(Exception, match="cover"):
+            dev.lp_set_slow_tiles(k, slow[:3], CHUNK // (2 * 8192), 2)
+        dev.lp_set_slow_tiles(k, None, 0)
         dev.lp_unregister(k)
         for p in (x, y, h):
             tier.free(p)
