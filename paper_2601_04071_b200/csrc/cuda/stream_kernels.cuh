@@ -89,12 +89,13 @@ __global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __gr
         if (!(p.run.preemptible && ld_volatile_smem(&preempt))) t = claim_tile(p.run);
         if (t >= 0 && p.slow && p.slow[t / p.slow_group]) {
           // admission: wait for one of slow_max slots; a preemption meanwhile parks the tile
+          // (read, then CAS: waiters never inflate the count the way add-then-undo would)
           for (;;) {
-            if (atomicAdd(p.slow_sem, 1u) < static_cast<unsigned>(p.slow_max)) {
+            const unsigned c = *reinterpret_cast<volatile unsigned int*>(p.slow_sem);
+            if (c < static_cast<unsigned>(p.slow_max) && atomicCAS(p.slow_sem, c, c + 1) == c) {
               slow_held = true;
               break;
             }
-            atomicSub(p.slow_sem, 1u);
             if (p.run.preemptible && ld_volatile_smem(&preempt)) {
               push_redo(p.run, static_cast<unsigned long long>(t));
               t = -1;
