@@ -239,7 +239,7 @@ int guarded(F&& f) {
 extern "C" int ms_tier_open(ms_dev* dev, const char* options_json, ms_tier** out) {
   if (!dev || !out) return ms_internal_fail(MS_E_ARG, "ms_tier_open: null argument");
   return guarded([&]() -> int {
-    auto t = std::make_unique<ms_tier>();
+    auto t = std::unique_ptr<ms_tier, int (*)(ms_tier*)>(new ms_tier, ms_tier_close);  // frees partial state
     t->dev = dev;
     ms_dev_info info;
     if (ms_dev_get_info(dev, &info) < 0) return MS_E_ARG;
