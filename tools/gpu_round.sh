@@ -29,5 +29,8 @@ timeout 300 python tools/first_cta_probe.py > gpurun_out/first_cta_probe.log 2>&
 timeout 300 python tools/gemv_probe.py > gpurun_out/gemv_probe.log 2>&1
 timeout 200 python tools/gemm_probe.py > gpurun_out/gemm_probe.log 2>&1
 timeout 300 python tools/axpy_probe.py > gpurun_out/axpy_probe.log 2>&1
+timeout 300 python tools/tier_probe.py gpurun_out/tier_probe.json > gpurun_out/tier_probe.log 2>&1
+timeout 1200 python tools/live_memory_case.py 6 gpurun_out/live_memory_case.json > gpurun_out/live_memory_case.log 2>&1
+timeout 300 python tools/gemm_group_sweep.py gpurun_out/gemm_group_sweep.json > gpurun_out/gemm_group_sweep.log 2>&1
 fi
 tail -n 2 gpurun_out/smoke.log gpurun_out/pytest_gpu.log; tail -c 1500 gpurun_out/bench.log; tail -c 800 gpurun_out/bench_ref.log
