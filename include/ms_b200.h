@@ -77,7 +77,9 @@ typedef struct ms_lp_desc {
   int32_t block_n;    /* GEMM tile N: 64, 128 or 256 (tile M is 128, k-block 64) */
   int32_t group_m;    /* GEMM raster group (L2 reuse), 0 = default 16 */
   int32_t tile_elems; /* AXPY tile (elements, multiple of 2048), 0 = default 8192 */
-  int32_t ctas_per_sm;/* AXPY residency, 0 = default 4 */
+  int32_t ctas_per_sm;/* AXPY layout: 1 (default, 0) = ONE CTA per SM with 3 x 256 streaming
+                         threads, so a capped grid leaves whole SMs free for HP; 2..4 = that
+                         many 256-thread CTAs per SM (the block scheduler spreads them) */
   int32_t pad;
   uint64_t a, b, c;
   int64_t m, n, k;

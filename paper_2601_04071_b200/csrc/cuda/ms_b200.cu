@@ -212,10 +212,10 @@ int set_smem_attrs() {
                                FusedCfg<1, 32>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
-  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
-  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
-  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
-  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  MS_CUDA(cudaFuncSetAttribute(axpy_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   done = true;
   return 0;
 }
@@ -965,7 +965,7 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     if (int rc = encode_c(&s.tma_c, reinterpret_cast<void*>(desc->c), desc->m, desc->n)) return rc;
   } else if (desc->kind == MS_LP_AXPY) {
     s.desc.tile_elems = desc->tile_elems ? desc->tile_elems : 8192;
-    s.desc.ctas_per_sm = desc->ctas_per_sm ? desc->ctas_per_sm : 4;
+    s.desc.ctas_per_sm = desc->ctas_per_sm ? desc->ctas_per_sm : 1;  // default: grouped, one CTA per SM
     if (s.desc.tile_elems % (kStreamThreads * 8) || s.desc.tile_elems > kStreamThreads * 8 * 8)
       return fail(MS_E_ARG, "tile_elems must be a multiple of 2048 and <= 16384");
     if (desc->n_elems % 8) return fail(MS_E_ARG, "n_elems must be a multiple of 8");
@@ -1092,8 +1092,12 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   p.slow_sem = s.slow_sem;
   p.slow_group = s.slow_group;
   p.slow_max = s.slow_max;
-  const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve)) * s.desc.ctas_per_sm;
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, cap)));
+  // ctas_per_sm == 1: the grouped one-CTA-per-SM streamer (3 x 256 streaming threads)
+  const bool grouped = s.desc.ctas_per_sm == 1;
+  const uint64_t per_cta = grouped ? kAxpyGroups : 1;
+  const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve)) *
+                       (grouped ? 1 : s.desc.ctas_per_sm);
+  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((work + per_cta - 1) / per_cta, cap)));
   const int vpt = s.desc.tile_elems / (kStreamThreads * 8);
   // Residency is capped at 4 CTAs per SM by registers (__launch_bounds__(320, 4): 48
   // registers, a 5th CTA does not fit), so the grid ((SMs - reserve) x 4) really leaves the
@@ -1102,12 +1106,23 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
   // 53-register build fitted only 3 CTAs per SM and left 144 CTAs pending, which tripled the
   // preemption drain.)
   const int pad = 0;
-  switch (vpt) {
-    case 1: axpy_kernel<1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
-    case 2: axpy_kernel<2><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
-    case 4: axpy_kernel<4><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
-    case 8: axpy_kernel<8><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
-    default: return fail(MS_E_ARG, "tile_elems must be 2048 * {1,2,4,8}");
+  if (grouped) {
+    const int threads = kAxpyGroups * kStreamThreads + 64;
+    switch (vpt) {
+      case 1: axpy_kernel<1, kAxpyGroups><<<grid, threads, 0, d->lp>>>(p); break;
+      case 2: axpy_kernel<2, kAxpyGroups><<<grid, threads, 0, d->lp>>>(p); break;
+      case 4: axpy_kernel<4, kAxpyGroups><<<grid, threads, 0, d->lp>>>(p); break;
+      case 8: axpy_kernel<8, kAxpyGroups><<<grid, threads, 0, d->lp>>>(p); break;
+      default: return fail(MS_E_ARG, "tile_elems must be 2048 * {1,2,4,8}");
+    }
+  } else {
+    switch (vpt) {
+      case 1: axpy_kernel<1, 1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+      case 2: axpy_kernel<2, 1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+      case 4: axpy_kernel<4, 1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+      case 8: axpy_kernel<8, 1><<<grid, kStreamThreads + 64, pad, d->lp>>>(p); break;
+      default: return fail(MS_E_ARG, "tile_elems must be 2048 * {1,2,4,8}");
+    }
   }
   MS_CUDA(cudaGetLastError());
   return 0;

@@ -34,7 +34,8 @@ struct StreamParams {
   int slow_group, slow_max;
 };
 
-constexpr int kStreamThreads = 256;  // streaming warps 0-7; warp 8 = mirror poller; warp 9 = host poller (CTA 0)
+constexpr int kStreamThreads = 256;  // one streaming group = 8 warps; then mirror poller + host poller (CTA 0) warps
+constexpr int kAxpyGroups = 3;       // streaming groups of the one-CTA-per-SM streamer (ctas_per_sm == 1)
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 v;
@@ -64,24 +65,47 @@ __device__ __forceinline__ uint32_t axpy2(float a, uint32_t xv, uint32_t yv) {
   return pack_bf16x2(lo, hi);
 }
 
-template <int VPT>  // 16-byte vectors per thread per tile
-__global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __grid_constant__ StreamParams p) {
-  __shared__ uint32_t preempt, producer_done, tiles_done;
-  __shared__ long long tile_sh[2];
+// GROUPS independent 256-thread streaming groups per CTA (each claims its own tiles, own
+// named barrier), then the two poller warps.  GROUPS = 1: 4 CTAs per SM (register-capped).
+// GROUPS = 3: ONE CTA per SM (832 threads) — a capped grid (governor, SM reserve) then
+// really leaves whole SMs empty for the HP chain, which several small CTAs per SM never
+// do (the block scheduler spreads them over every SM).
+// Named barrier of streaming group g (ids 1..GROUPS; id 0 = __syncthreads).  Immediate ids
+// so ptxas reserves only the barriers used (a register id reserves all 16).
+template <int GROUPS>
+__device__ __forceinline__ void group_bar(int g) {
+  if constexpr (GROUPS == 1) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
+  } else {
+    static_assert(GROUPS == 3, "group_bar: add the ids");
+    if (g == 0) asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
+    else if (g == 1) asm volatile("bar.sync 2, %0;" ::"n"(kStreamThreads) : "memory");
+    else asm volatile("bar.sync 3, %0;" ::"n"(kStreamThreads) : "memory");
+  }
+}
+
+template <int VPT, int GROUPS>  // 16-byte vectors per thread per tile
+__global__ void __launch_bounds__(GROUPS * kStreamThreads + 64, GROUPS == 1 ? 4 : 1)
+    axpy_kernel(const __grid_constant__ StreamParams p) {
+  __shared__ uint32_t preempt, producer_done, tiles_done, groups_left;
+  __shared__ long long tile_sh[GROUPS][2];
+  constexpr int kStreamWarps = GROUPS * kStreamThreads / 32;
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
     preempt = 0;
     producer_done = 0;
     tiles_done = 0;
+    groups_left = GROUPS;
     cta_started(p.run);
   }
   __syncthreads();
-  if (warp == kStreamThreads / 32) {
+  if (warp == kStreamWarps) {
     if ((threadIdx.x & 31) == 0 && p.run.preemptible) poll_mirror(p.run, &preempt, &producer_done);
-  } else if (warp == kStreamThreads / 32 + 1) {
+  } else if (warp == kStreamWarps + 1) {
     if ((threadIdx.x & 31) == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &preempt, &producer_done);
   } else {
-    const int tid = threadIdx.x;
+    const int g = warp / (kStreamThreads / 32);
+    const int tid = threadIdx.x % kStreamThreads;
     for (int j = 0;; ++j) {
       bool slow_held = false;
       if (tid == 0) {
@@ -104,10 +128,10 @@ __global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __gr
             __nanosleep(256);
           }
         }
-        tile_sh[j & 1] = t;
+        tile_sh[g][j & 1] = t;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
-      const long long t = tile_sh[j & 1];
+      group_bar<GROUPS>(g);
+      const long long t = tile_sh[g][j & 1];
       if (t < 0) break;
       const unsigned long long base = static_cast<unsigned long long>(t) * p.tile_elems;
       uint4 xv[VPT], yv[VPT];
@@ -134,12 +158,12 @@ __global__ void __launch_bounds__(kStreamThreads + 64, 4) axpy_kernel(const __gr
       }
       if (p.slow) {
         // every thread's slow-tile loads have returned once all reach this barrier
-        asm volatile("bar.sync 1, %0;" ::"n"(kStreamThreads) : "memory");
+        group_bar<GROUPS>(g);
         if (slow_held) atomicSub(p.slow_sem, 1u);
       }
-      if (tid == 0) ++tiles_done;
+      if (tid == 0) atomicAdd(&tiles_done, 1u);
     }
-    if (tid == 0) st_volatile_smem(&producer_done, 1u);
+    if (tid == 0 && atomicSub(&groups_left, 1u) == 1u) st_volatile_smem(&producer_done, 1u);
   }
   __syncthreads();
   if (threadIdx.x == 0) cta_exit(p.run, tiles_done);

@@ -184,7 +184,7 @@ class Device:
         return self._lp_register(d)
 
     def lp_register_axpy(self, x: int, y: int, n_elems: int, alpha: float, tile_elems: int = 8192,
-                         ctas_per_sm: int = 4) -> LpKernel:
+                         ctas_per_sm: int = 1) -> LpKernel:
         d = LpDesc(kind=MS_LP_AXPY, tile_elems=tile_elems, ctas_per_sm=ctas_per_sm, x=x, y=y,
                    alpha=alpha, n_elems=n_elems)
         return self._lp_register(d)

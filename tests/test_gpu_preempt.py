@@ -136,13 +136,14 @@ def test_gemm_cta_pair_kernel_preempt_resume(dev, pair):
         dev.free(p_)
 
 
-def test_axpy_preempt_resume_exact(dev):
+@pytest.mark.parametrize("ctas_per_sm", [4, 1])  # 1 = grouped one-CTA-per-SM streamer
+def test_axpy_preempt_resume_exact(dev, ctas_per_sm):
     from oracle import tenant as T
     n = 1 << 26
     x, y = dev.alloc(2 * n), dev.alloc(2 * n)
     dev.fill_synth(x, n, 3, 1, 1.0)
     dev.fill_synth(y, n, 3, 2, 1.0)
-    k = dev.lp_register_axpy(x, y, n, 1.5)
+    k = dev.lp_register_axpy(x, y, n, 1.5, ctas_per_sm=ctas_per_sm)
     begin, runs = 0, 0
     while True:
         dev.lp_run(k, begin, k.total_tiles)
@@ -157,6 +158,9 @@ def test_axpy_preempt_resume_exact(dev):
     assert runs > 1
     want = T.axpy(T.synth_bf16(n, 3, 2, 1.0), T.synth_bf16(n, 3, 1, 1.0), 1.5)
     assert np.array_equal(d2h(dev, y, n), want)
+    dev.lp_unregister(k)
+    dev.free(x)
+    dev.free(y)
 
 
 def test_doorbell_releases_armed_chain(dev):
