@@ -188,6 +188,7 @@ struct ms_dev {
   unsigned long long* dbg = nullptr;  // per-CTA phase stamps of the next LP run (diagnostics)
   unsigned long long* dbg_buf = nullptr;
   int lp_sm_reserve = 1;  // SMs an LP GEMM grid leaves free (the HP gate's home)
+  int lp_align_clusters[5] = {0, 0, 0, 0, 0};  // max active C-CTA clusters of the LP GEMM (MS_LP_CLUSTER_ALIGN)
   int hp_fused = 1;       // 0: per-op kernels; 1: fused launch (cluster split-K when it fits); 2: fused, no clusters
 };
 
@@ -1079,6 +1080,32 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
       return 0;
     }
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount - d->lp_sm_reserve)));
+    // Experimental (MS_LP_CLUSTER_ALIGN=C): launch the LP GEMM as C-CTA clusters and keep
+    // one cluster slot of the machine free, so the HP chain's first C-CTA cluster finds C
+    // empty SMs of one GPC without waiting for LP CTAs to exit.
+    const char* ca = std::getenv("MS_LP_CLUSTER_ALIGN");
+    const int align = ca ? atoi(ca) : 0;
+    if ((align == 2 || align == 4) && s.desc.block_n == 256) {
+      if (d->lp_align_clusters[align] == 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(align * 64);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = GemmCfg<256>::kSmemBytes;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim = {static_cast<unsigned>(align), 1, 1};
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int mc = 0;
+        MS_CUDA(cudaOccupancyMaxActiveClusters(&mc, tc_gemm_kernel<256>, &cfg));
+        d->lp_align_clusters[align] = mc;
+      }
+      const int slots = std::min(d->lp_align_clusters[align] - 1, grid / align);
+      const int gc = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((work + align - 1) / align, std::max(1, slots))));
+      MS_CUDA(launch_kc(tc_gemm_kernel<256>, gc * align, 256, GemmCfg<256>::kSmemBytes, d->lp, false, align, s.tma_a,
+                        s.tma_b, s.tma_c, p));
+      return 0;
+    }
     return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, s.tma_c, p, grid, d->lp);
   }
   StreamParams p{};
@@ -1373,7 +1400,11 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   if (!ch.used) return fail(MS_E_ARG, "bad chain");
   // 40 KB of (unused) shared memory keeps a 193 KB LP GEMM CTA off the gate's SM: an LP
   // CTA co-resident with the spinning gate observed preemptions ~5 us late.
-  gate_kernel<<<1, 32 * kGateWarps, kGateSmem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
+  static const int gate_smem = [] {
+    const char* e = std::getenv("MS_GATE_SMEM");
+    return e ? std::max(0, std::min(atoi(e), kGateSmem)) : kGateSmem;
+  }();
+  gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
   return launch_chain(d, cid, ch, seq, true);
 }
