@@ -1064,9 +1064,9 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.tiles_n = s.tiles_n;
     p.group_m = s.desc.group_m ? s.desc.group_m : 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
-    static const int mma_lag = [] {
+    const int mma_lag = [] {  // read per launch (A/B probes flip it in-process)
       const char* e = getenv("MS_LP_MMA_LAG");
-      const int v = e ? atoi(e) : 2;
+      const int v = e ? atoi(e) : 0;  // unbounded: +2.5% TFLOP/s, same drain (profiles/r01_mma_lag_ab.json)
       return v < 0 ? 0 : v > 4 ? 4 : v;
     }();
     p.mma_lag = mma_lag;
