@@ -120,6 +120,7 @@ class LiveRun {
     // it (config 4, 3 x 15 s A/B: HP SLO attainment 0.92-0.93 vs 0.84-0.86 unbounded, LP
     // 0.37-0.39 vs 0.43-0.47 of exclusive).  false: extend while the bubble is open.
     bound_hints_ = opts.value("bound_hint_harvest", true);
+    hint_quantile_ = opts.value("hint_quantile", -1.0);
     record_ = opts.value("timeline", true);
     ms_dev_info info{};
     ms_dev_get_info(dev_, &info);
@@ -336,7 +337,9 @@ class LiveRun {
     std::string key;
     for (const int hi : h.seg_hints[h.seg]) {
       const BubbleHint& hint = h.spec->bubble_hints[hi];
-      predicted += hint.duration.mean();  // the scheduler sizes LP from the hint's profile, not the draw
+      // the scheduler sizes LP from the hint's profile, not the draw: its mean, or a low
+      // quantile (option hint_quantile) so that most bubbles outlast the LP batch
+      predicted += hint_quantile_ >= 0 ? hint.duration.sample(hint_quantile_) : hint.duration.mean();
       dur += hint.duration.sample_keyed(hash_combine(
           base, hash_combine(static_cast<std::uint64_t>(h.iteration), static_cast<std::uint64_t>(hi))));
       if (!key.empty()) key += '+';
@@ -558,6 +561,7 @@ class LiveRun {
   int debug_runs_ = 0;
   int base_reserve_ = 1, small_sms_ = 0, max_sms_ = 0;
   bool bound_hints_ = false;
+  double hint_quantile_ = -1.0;  // < 0: size hint harvests from the hint's mean
   std::unique_ptr<PowerGovernor> governor_;
   std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
   int n_sm_ = 148;
