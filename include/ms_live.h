@@ -23,7 +23,10 @@
  *                  "lp_max_sms": n (fixed LP SM budget), "small_bubble_sms": n (budget
  *                  while harvesting a bubble inside an HP request),
  *                  "power_governor": bool (NVML SM-clock feedback sizes the LP budget),
- *                  "governor_min_sms", "governor_start_sms", "governor_slack_mhz"}
+ *                  "governor_min_sms", "governor_start_sms", "governor_slack_mhz",
+ *                  hint bubbles: "bound_hint_harvest": bool (default true: LP stops at the
+ *                  predicted end / safety), "hint_quantile": q (size from the q-quantile of
+ *                  the hint's duration profile instead of its mean)}
  * *result_json  : requests, preemption delays (ring -> first HP CTA, and flag -> last LP
  *                 CTA exit), LP tiles / parents completed, SLO report, timeline summary,
  *                 power-governor summary (mean LP SMs, SM clock).
