@@ -1066,7 +1066,10 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
     const int mma_lag = [] {  // read per launch (A/B probes flip it in-process)
       const char* e = getenv("MS_LP_MMA_LAG");
-      const int v = e ? atoi(e) : 0;  // unbounded: +2.5% TFLOP/s, same drain (profiles/r01_mma_lag_ab.json)
+      // default 2: unbounded is +2.5% TFLOP/s alone (profiles/r01_mma_lag_ab.json) but under the
+      // 1 kW cap it lowers the HP clock (bench A/B: SLO -2 points, p99 +0.25 us;
+      // profiles/r01_lag_bench_ab/)
+      const int v = e ? atoi(e) : 2;
       return v < 0 ? 0 : v > 4 ? 4 : v;
     }();
     p.mma_lag = mma_lag;
