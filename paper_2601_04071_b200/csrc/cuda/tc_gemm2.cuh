@@ -44,12 +44,11 @@ struct Gemm2Cfg {
 struct Gemm2Ctl {
   uint64_t full[Gemm2Cfg::kStages];   // leader: one arrive_expect_tx + both CTAs' TMA bytes
   uint64_t empty[Gemm2Cfg::kStages];  // leader: MMA commit (both CTAs' stage reads done)
-  uint64_t go[2][Gemm2Cfg::kStages];  // peer: leader's command for (use parity, stage)
-  uint64_t skip_ack;                  // leader: the peer consumed an abort (skip) command
+  uint64_t go[Gemm2Cfg::kStages];     // peer: leader's command for this stage
   uint64_t tmem_full[2], tmem_empty[2], tile_full[2], tile_empty[2];
   uint64_t mma_drain;
   long long tile_id[2];
-  alignas(16) int4 cmd[2][Gemm2Cfg::kStages];  // peer: {tile lo, tile hi, kb, 0}; tile -1 skip, -2 end
+  alignas(16) int4 cmd[Gemm2Cfg::kStages];  // peer: {tile lo, tile hi, kb, 0}; tile -1 skip, -2 end
   uint32_t tile_abort[2];
   uint32_t stage_flag[Gemm2Cfg::kStages];  // leader: 0 data, 1 data + last k-block, 2 aborted
   uint32_t tmem_base;
@@ -141,8 +140,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < S; ++i) {
       mbar_init(&s->full[i], 1);
       mbar_init(&s->empty[i], 1);
-      mbar_init(&s->go[0][i], 1);
-      mbar_init(&s->go[1][i], 1);
+      mbar_init(&s->go[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s->tmem_full[i], 1);
@@ -151,7 +149,6 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&s->tile_empty[i], 2);  // both CTAs' epilogues
     }
     mbar_init(&s->mma_drain, 1);
-    mbar_init(&s->skip_ack, 1);
     s->preempt = 0;
     s->producer_done = 0;
     s->tiles_done = 0;
@@ -170,35 +167,26 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = s->tmem_base;
   const int num_kb = p.k / kBK;
   if (!leader && threadIdx.x == 0)
-    for (int i = 0; i < S; ++i) {  // first command of each (use parity, slot)
-      mbar_arrive_expect_tx(&s->go[0][i], 16);
-      mbar_arrive_expect_tx(&s->go[1][i], 16);
-    }
+    for (int i = 0; i < S; ++i) mbar_arrive_expect_tx(&s->go[i], 16);  // first command of each slot
 
   if (warp == 0) {
     if (lane == 0) {
       if (leader) {
         // ===================== leader: scheduler + producer + peer commands =====================
-        // Early commands: the command for a stage goes to the peer BEFORE the leader waits
-        // for that stage to drain; the peer waits on its own copy of the stage's empty
-        // barrier (the MMA commit is multicast to both CTAs), so its half of the load is
-        // issued as soon as the stage frees instead of one DSMEM round trip later.
-        // Commands are double-buffered by use parity: cmd(s, u) overwrites cmd(s, u - 2),
-        // which the peer has consumed once empty(s, u - 2) completed (its bytes fed that
-        // use) — or, for an abort (skip) command, once the peer acknowledged it (skip_ack).
-        uint32_t stage = 0, phase = 0, skip_phase = 0;
-        const uint32_t peer_cmd = mapa_shared(smem_u32(&s->cmd[0][0]), 1);
-        const uint32_t peer_go = mapa_shared(smem_u32(&s->go[0][0]), 1);
+        uint32_t stage = 0, phase = 0;
+        const uint32_t peer_cmd = mapa_shared(smem_u32(&s->cmd[0]), 1);
+        const uint32_t peer_go = mapa_shared(smem_u32(&s->go[0]), 1);
         const uint32_t peer_tile_id = mapa_shared(smem_u32(&s->tile_id[0]), 1);
         const uint32_t peer_tile_abort = mapa_shared(smem_u32(&s->tile_abort[0]), 1);
         const uint32_t peer_tile_full = mapa_shared(smem_u32(&s->tile_full[0]), 1);
-        // One 16-byte st.async carries the command and completes the peer's go barrier (no
-        // release fence: a release.cluster arrive costs a MEMBAR.GPU per stage).
+        // Command to the peer: load (tile, kb) / skip (-1) / end (-2).  One 16-byte st.async
+        // carries the data and completes the peer's go barrier (no release fence: a
+        // release.cluster arrive costs a MEMBAR.GPU per stage, which capped this loop at one
+        // stage per ~0.9 us).
         auto command = [&](long long tile, int kb) {
           const unsigned long long t = static_cast<unsigned long long>(tile);
-          const uint32_t slot = phase * S + stage;
-          st_async_v4(peer_cmd + slot * 16, static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
-                      static_cast<uint32_t>(kb), 0u, peer_go + slot * 8);
+          st_async_v4(peer_cmd + stage * 16, static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
+                      static_cast<uint32_t>(kb), 0u, peer_go + stage * 8);
         };
         for (int j = 0;; ++j) {
           const int slot = j & 1;
@@ -219,18 +207,15 @@ __global__ void __launch_bounds__(256, 1)
           tile_coords(tile, p, mb, nb);
           for (int kb = 0; kb < num_kb; ++kb) {
             const bool abort = p.run.preemptible && kb > 0 && ld_volatile_smem(&s->preempt);
-            command(abort ? -1 : tile, kb);
-            if (abort) {
-              mbar_wait(&s->skip_ack, skip_phase);
-              skip_phase ^= 1;
-            }
             mbar_wait(&s->empty[stage], phase ^ 1);
             if (abort) {
               s->stage_flag[stage] = 2;  // the MMA warp owns the redo push for this tile
+              command(-1, kb);
               mbar_arrive(&s->full[stage]);
             } else {
               s->stage_flag[stage] = (kb == num_kb - 1) ? 1u : 0u;
-              mbar_arrive_expect_tx(&s->full[stage], 2 * Cfg::kStageBytes);
+              mbar_arrive_expect_tx(&s->full[stage], 2 * Cfg::kStageBytes);  // before any peer byte lands
+              command(tile, kb);
               const uint32_t fb = smem_u32(&s->full[stage]);
               tma_load_2d_pair(smem_u32(smem_a + stage * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256);
               tma_load_2d_pair(smem_u32(smem_b + stage * Cfg::kHalfBytes), &tma_b, fb, kb * kBK, nb * 256);
@@ -244,34 +229,29 @@ __global__ void __launch_bounds__(256, 1)
         }
       } else {
         // ===================== peer: follow the leader's stage commands =====================
-        uint32_t stage = 0, phase = 0, use = 0;  // use = wraps of the ring (all stages in step)
-        const uint32_t leader_skip_ack = mapa_shared(smem_u32(&s->skip_ack), 0);
+        uint32_t stage = 0, phase = 0;
         for (;;) {
-          mbar_wait(&s->go[phase][stage], (use >> 1) & 1);
+          mbar_wait(&s->go[stage], phase);
           uint32_t c0, c1, c2, c3;
           asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(c0), "=r"(c1), "=r"(c2), "=r"(c3)
-                       : "r"(smem_u32(&s->cmd[phase][stage]))
+                       : "r"(smem_u32(&s->cmd[stage]))
                        : "memory");
           const long long tile = static_cast<long long>((static_cast<unsigned long long>(c1) << 32) | c0);
           const int kb = static_cast<int>(c2);
           (void)c3;
           if (tile == -2) break;
-          mbar_arrive_expect_tx(&s->go[phase][stage], 16);  // arm this buffer's next command
-          mbar_wait(&s->empty[stage], phase ^ 1);           // own copy: the stage's last use drained
+          mbar_arrive_expect_tx(&s->go[stage], 16);  // arm the slot's next command
           if (tile >= 0) {
             int mb, nb;
             tile_coords(tile, p, mb, nb);
             const uint32_t fb = mapa_shared(smem_u32(&s->full[stage]), 0);
             tma_load_2d_pair(smem_u32(smem_a + stage * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256 + 128);
             tma_load_2d_pair(smem_u32(smem_b + stage * Cfg::kHalfBytes), &tma_b, fb, kb * kBK, nb * 256 + 128);
-          } else {
-            mbar_arrive_cluster(leader_skip_ack);  // abort command consumed
           }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
-            ++use;
           }
         }
       }
@@ -285,7 +265,6 @@ __global__ void __launch_bounds__(256, 1)
       int consumed = 0;
       const uint32_t peer_tile_abort = mapa_shared(smem_u32(&s->tile_abort[0]), 1);
       const uint32_t peer_tmem_full = mapa_shared(smem_u32(&s->tmem_full[0]), 1);
-      const uint32_t peer_empty = mapa_shared(smem_u32(&s->empty[0]), 1);
       for (int j = 0;; ++j) {
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
@@ -300,9 +279,8 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t flag = s->stage_flag[stage];
           if (!aborted && p.run.preemptible && ld_volatile_smem(&s->preempt)) aborted = true;
           if (flag == 2) aborted = true;
-          if (aborted) {  // both CTAs track the stage's empty barrier
+          if (aborted) {
             mbar_arrive(&s->empty[stage]);
-            mbar_arrive_cluster(peer_empty + stage * 8);
           } else {
             if (lag > 0 && consumed >= lag) {
               int ps = static_cast<int>(stage) - lag;
@@ -318,7 +296,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int k = 0; k < kBK / kUmmaK; ++k)
               umma_bf16_pair(d_tmem, a0 + 2ull * k, b0 + 2ull * k, Cfg::kIdesc, (kb | k) != 0 ? 1u : 0u);
-            umma_commit_pair_mc(&s->empty[stage], 0x3);
+            umma_commit_pair(&s->empty[stage]);
           }
           ++consumed;
           if (++stage == S) {
