@@ -291,7 +291,8 @@ class LiveRun {
   void hp_chain_done(HpTask& h, const ms_hp_times& tm) {
     h.inflight = false;
     // Device timestamps are converted after the run with a drift-corrected clock fit.
-    HpSample smp{h.ring_t, tm.t_first_cta, tm.t_done, tm.t_gate, pending_preempt_.has_value(), h.index, tm.seq};
+    HpSample smp{h.ring_t, tm.t_first_cta, tm.t_done, tm.t_gate, pending_preempt_.has_value(), h.index, tm.seq,
+                 now_};
     hp_samples_.push_back(smp);
     if (pending_preempt_) {
       art_.preemptions.push_back(*pending_preempt_);  // delay filled in at the end
@@ -573,6 +574,7 @@ class LiveRun {
     bool preempt;
     int stream;
     uint32_t seq;
+    Ns detect;  // host time the scheduler saw the completion
   };
   struct LpSample {
     Ns raise;  // -1: not a preemption we raised
@@ -584,6 +586,7 @@ class LiveRun {
   std::vector<LpSample> lp_samples_;
   Ns now_ = 0;
   std::priority_queue<Timer, std::vector<Timer>, std::greater<Timer>> timers_;
+  std::vector<Ns> timer_late_, detect_lag_;
   long timer_seq_ = 0;
   std::vector<HpTask> hp_;
   std::vector<LpTask> lp_;
@@ -653,7 +656,10 @@ json LiveRun::run() {
       timers_.pop();
       switch (t.kind) {
         case kArrival: request_arrival(t.a, static_cast<std::size_t>(t.b)); break;
-        case kBubbleOver: bubble_over(t.a); break;
+        case kBubbleOver:
+          timer_late_.push_back(now_ - t.t);
+          bubble_over(t.a);
+          break;
         case kLargeBubble: large_bubble_check(t.b); break;
         case kReefRefill: relaunch_if_allowed(); break;  // flag checked before the first wave
       }
@@ -705,6 +711,7 @@ json LiveRun::run() {
     ring_to_first_.push_back(first - smp.ring);
     if (smp.gate) gate_to_first_.push_back(static_cast<Ns>(smp.first) - static_cast<Ns>(smp.gate));
     chain_durations_.push_back(done - first);
+    detect_lag_.push_back(smp.detect - done);
     if (smp.preempt && pi < art_.preemptions.size()) {
       art_.preemptions[pi].delay = first - smp.ring;
       preempt_delays_.push_back(first - smp.ring);
@@ -757,6 +764,9 @@ json LiveRun::run() {
   out["requests"]["rows"] = std::move(reqs);  // [arrival, ttft, tpot, iterations, completed]
   out["preempt_ring_to_first_hp_cta"] = summarize(preempt_delays_);
   out["ring_to_first_hp_cta_all"] = summarize(ring_to_first_);
+  // host-side HP path: chain done (device) -> scheduler saw it; bubble end due -> handled
+  out["hp_done_detect_lag"] = summarize(detect_lag_);
+  out["bubble_timer_late"] = summarize(timer_late_);
   out["preempt_flag_to_last_lp_exit"] = summarize(lp_exit_lat_);
   out["preempt_flag_to_first_lp_seen"] = summarize(lp_seen_lat_);
   out["preempt_flag_to_exit_of_queued_lp_runs"] = summarize(lp_queued_exit_lat_);
