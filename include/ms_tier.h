@@ -20,8 +20,9 @@
  *                "eviction": "contention_first" | "round_robin", "score_threshold": 1.5,
  *                "probe_mb": 4, "probe_cache_us": 1000, "numa": host NUMA node (default:
  *                the GPU's)}
- * Relocation (an HP allocation displacing LP chunks) remaps LP memory: the caller must
- * have LP work on this tier's buffers drained (ms_preempt_raise + ms_lp_wait) first.
+ * Relocation (an HP allocation displacing LP chunks) remaps LP memory: it waits for the
+ * LP stream (preempt first — ms_preempt_raise — to keep that short); ms_tier_free waits
+ * for the LP stream too.  A buffer an ARMED HP chain uses must not be freed.
  * Threading: one owner thread per tier.  Errors as in ms_b200.h (ms_last_error).
  */
 #ifndef MS_TIER_H_

@@ -806,6 +806,11 @@ extern "C" {
 
 const char* ms_last_error(void) { return g_err.c_str(); }
 int ms_internal_fail(int code, const char* what) { return fail(code, what ? what : ""); }
+// Memory tier: wait for LP work only (an armed HP gate keeps the HP stream busy until rung).
+int ms_internal_lp_sync(ms_dev* d) {
+  MS_CUDA(cudaStreamSynchronize(d->lp));
+  return 0;
+}
 int64_t ms_host_now_ns(void) { return now_ns(); }
 
 int ms_dev_open(int ordinal, ms_dev** out) {

@@ -28,6 +28,7 @@
 #include "ms_tier.h"
 
 extern "C" int ms_internal_fail(int code, const char* what);  // ms_b200.cu: sets ms_last_error
+extern "C" int ms_internal_lp_sync(ms_dev* dev);                 // ms_b200.cu: LP stream only
 
 namespace microslice {
 namespace {
@@ -322,7 +323,9 @@ extern "C" int ms_tier_alloc(ms_tier* t, int task, int high_priority, uint64_t b
     std::vector<std::int64_t> ids =
         t->mm->allocate(task, prio, static_cast<std::int64_t>(bytes), mono_ns(), &moves);
     if (!moves.empty()) {
-      ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize (before relocation)");
+      // LP kernels may read the chunks being moved; HP chains never own LP chunks (and an
+      // armed HP gate must not be waited on)
+      if (ms_internal_lp_sync(t->dev) < 0) throw TierError{MS_E_CUDA, "LP stream sync before relocation"};
       t->relocate(moves);
     }
     Buffer b;
@@ -396,7 +399,8 @@ extern "C" int ms_tier_free(ms_tier* t, uint64_t dptr) {
   if (it == t->buffers.end()) return ms_internal_fail(MS_E_ARG, "ms_tier_free: unknown buffer");
   return guarded([&]() -> int {
     ck(cudaSetDevice(t->ordinal), "cudaSetDevice");
-    ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+    if (ms_internal_lp_sync(t->dev) < 0) throw TierError{MS_E_CUDA, "LP stream sync before free"};
+    ck(cudaStreamSynchronize(t->probe_stream), "probe stream sync");
     t->free_buffer(it->second);
     t->buffers.erase(it);
     return 0;
