@@ -410,7 +410,8 @@ extern "C" int ms_tier_free(ms_tier* t, uint64_t dptr) {
 extern "C" int ms_tier_close(ms_tier* t) {
   if (!t) return 0;
   cudaSetDevice(t->ordinal);
-  cudaDeviceSynchronize();
+  if (t->dev) ms_internal_lp_sync(t->dev);
+  if (t->probe_stream) cudaStreamSynchronize(t->probe_stream);
   for (auto& kv : t->buffers) t->free_buffer(kv.second);
   const size_t pb = (t->probe_bytes + kChunkBytes - 1) / kChunkBytes * kChunkBytes;
   std::vector<CUdeviceptr> ranges = t->probe_dst;
