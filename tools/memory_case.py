@@ -15,7 +15,7 @@ from paper_2601_04071_b200 import microslice as M  # noqa: E402
 from paper_2601_04071_b200 import scenarios as S  # noqa: E402
 
 
-RATE = 10.0
+RATE = float(sys.argv[3]) if len(sys.argv) > 3 else 10.0
 
 
 def row(sc, pol):
