@@ -1,5 +1,7 @@
 """In-process A/B of the bs=1 decode chain's consumer layout (MS_GEMV_W, read per launch):
-1 warp per ring stage vs 2 warps splitting each unit.  CUDA-event time per decode step."""
+1 warp per ring stage vs 2 warps splitting each unit.  CUDA-event time per decode step.
+(The W = 2 kernel was reverted after this A/B — profiles/r01_gemv_w_ab.json,
+profiles/r01_gemv_decode.txt — so on the current build both arms run W = 1.)"""
 import json
 import os
 import sys
