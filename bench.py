@@ -177,67 +177,78 @@ def run_reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def aggregate_ranks(allr, horizon_total):
-    """Whole-job aggregation of the per-rank (per-GPU replica) results: preemption samples
-    are pooled (p99 over all ranks), SLO attainment = sum met / sum requests, LP rates
-    add up."""
-    slo = allr[0]["slo"]
-
-    def att(rows_key):
+def aggregate_ranks(allr, H: float, Hb: float) -> dict:
+    """Whole-job aggregation of the per-rank (per-GPU replica) config-1 results: preemption
+    samples are pooled (p99 over all ranks), SLO attainment = sum met / sum requests against
+    each rank's own exclusive SLO, LP rates add up.  H / Hb = timed
+    seconds of the splitkernel windows / of the side-run windows per rank."""
+    def att(rows_of):
         met = tot = 0
         for r in allr:
-            rows = r[rows_key]
-            s_ = r.get("slo", slo)
-            met += sum(1 for x in rows if x[4] and x[1] <= s_["ttft_ns"] and x[2] <= s_["tpot_ns"])
-            tot += len(rows)
-        return met / max(1, tot)
+            rws = rows_of(r)
+            met += sum(1 for x in rws if x[4] and x[1] <= r["slo"]["ttft_ns"] and x[2] <= r["slo"]["tpot_ns"])
+            tot += len(rws)
+        return round(met / max(1, tot), 4)
 
-    return {"S": [x for r in allr for x in r["samples"]], "LX": [x for r in allr for x in r["lp_exit"]],
-            "E2E": [x for r in allr for x in r["e2e"]],
-            "lp_rate": sum(r["tiles"] for r in allr) / horizon_total,
-            "kb_rate": sum(r["kb_tiles"] for r in allr) / horizon_total,
-            "kbr_rate": sum(r.get("kbr_tiles", 0) for r in allr) / horizon_total,
+    pool = lambda k: [x for r in allr for x in r[k]]  # noqa: E731
+    kb = lambda p_, k: [x for r in allr for x in r["kb"][p_][k]]  # noqa: E731
+    return {"S": pool("samples"), "INF": pool("inflight"), "IDL": pool("idle"), "LX": pool("lp_exit"),
+            "E2E": pool("e2e"),
             "ex_rate": sum(r["exlp_rate"] for r in allr),
-            "pb_rate": sum(r.get("pb_tiles", 0) for r in allr) / horizon_total,
-            "att_pb": att("pb_rows") if all("pb_rows" in r for r in allr) else None,
-            "att": att("rows"), "att_ex": att("ex_rows"), "att_kb": att("kb_rows"),
-            "att_kbr": att("kbr_rows") if all("kbr_rows" in r for r in allr) else None}
+            "lp_rate": sum(r["tiles"] for r in allr) / H,
+            "kb_rate": {p_: sum(r["kb"][p_]["tiles"] for r in allr) / Hb for p_ in ("reef", "reef_req")},
+            "kb_samples": {p_: kb(p_, "samples") for p_ in ("reef", "reef_req")},
+            "pb_rate": sum(r["pb"]["tiles"] for r in allr) / Hb,
+            "pb_samples": [x for r in allr for x in r["pb"]["samples"]],
+            "pb_inflight": [x for r in allr for x in r["pb"]["inflight"]],
+            "pb_gov": [x for r in allr for x in r["pb"]["gov"] if x],
+            "att": att(lambda r: r["rows"]), "att_ex": att(lambda r: r["ex_rows"]),
+            "att_kb": {p_: att(lambda r, p_=p_: r["kb"][p_]["rows"]) for p_ in ("reef", "reef_req")},
+            "att_pb": att(lambda r: r["pb"]["rows"])}
 
 
-# ----------------------------------------------------------------------------- config-4 leg
-CFG4_POLICIES = ("splitkernel", "reef_req", "reef")
+# ----------------------------------------------------------------------------- policy legs
+LEG_POLICIES = ("splitkernel", "reef_req", "reef")
 
 
-def run_config4_leg(dev, horizon_s: float, seed: int) -> dict:
-    """Config 4 (BASELINE configs[3]): Llama-3.2-1B-geometry bs=1 decode HP at 80% HP load
-    (GEMV chain) + LP GEMM and HBM-streamer tenants.  Every LP-running policy runs under the
-    power governor (the same LP power budget for all), so the comparison isolates the
-    scheduling policy: splitkernel vs the kernel-boundary baselines."""
-    from paper_2601_04071_b200.live import Config4, live_run
-    w = Config4(dev)
-    time.sleep(0.5)  # let the part leave the power cap the config-1 GEMM runs put it in
-    w.calibrate()
-    sc = w.scenario(seed=seed, horizon_s=horizon_s, rate=w.hp_rate(0.8))
+def run_policy_leg(dev, w, horizon_s: float, seed: int, rate: float, exlp_s: float = 5.0,
+                   reef_s: float | None = None) -> dict:
+    """One config's policy comparison on the live GPU: exclusive (HP alone -> its own p99
+    TTFT/TPOT = the SLO, metrics.hpp:78-92), exclusive_lp (LP alone -> the LP throughput
+    reference), then splitkernel / reef_req / reef on the SAME trace window.  Every
+    LP-running policy runs under the power governor (same LP power budget for all), so the
+    comparison isolates the scheduling policy."""
+    from paper_2601_04071_b200.live import live_run
+    sc = w.scenario(seed=seed, horizon_s=horizon_s, rate=rate)
     ex = live_run(dev, sc, "exclusive", w.binding(), w.options(timeline=False))
     slo = {"ttft_ns": ex["own_p99"]["ttft_ns"], "tpot_ns": ex["own_p99"]["tpot_ns"]}
     gov = {"power_governor": True}
-    exlp = live_run(dev, sc, "exclusive_lp", w.binding(), w.options(timeline=False, **gov))
-    out = {"slo": slo, "ex_rows": ex["requests"]["rows"], "exlp_tiles": exlp["lp"]["tiles_done"],
-           "rate": sc["traces"][0]["bursty"]["rate"], "step_ms": w.calib["hp_step_ms"]}
-    for pol in CFG4_POLICIES:
-        r = live_run(dev, sc, pol, w.binding(), w.options(timeline=False, **gov))
-        out[pol] = {"rows": r["requests"]["rows"], "tiles": r["lp"]["tiles_done"],
-                    "ring": r["samples"]["ring_to_first_hp_cta_all"],
-                    "lp_exit": r["samples"]["preempt_flag_to_last_lp_exit"],
+    exlp = live_run(dev, w.scenario(seed=seed, horizon_s=exlp_s, rate=rate), "exclusive_lp", w.binding(),
+                    w.options(timeline=False, **gov))
+    out = {"slo": slo, "ex_rows": ex["requests"]["rows"], "exlp_rate": exlp["lp"]["tiles_per_s"],
+           "rate": rate, "calib": w.calib, "ex_step_p50_us": ex["hp_chain_duration"].get("p50_ns", 0) / 1e3}
+    for pol in LEG_POLICIES:
+        h = reef_s if (pol == "reef" and reef_s) else horizon_s
+        scp = sc if h == horizon_s else w.scenario(seed=seed, horizon_s=h, rate=rate)
+        r = live_run(dev, scp, pol, w.binding(), w.options(timeline=False, **gov))
+        smp = r["samples"]
+        out[pol] = {"rows": r["requests"]["rows"], "tiles_per_s": r["lp"]["tiles_per_s"],
+                    "ring": smp["ring_to_first_hp_cta_all"],
+                    "inflight": smp.get("preempt_ring_to_first_hp_cta_lp_in_flight", []),
+                    "lp_exit": smp["preempt_flag_to_last_lp_exit"],
                     "step_p50_us": r["hp_chain_duration"].get("p50_ns", 0) / 1e3,
-                    "lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms")}
-    out["ex_step_p50_us"] = ex["hp_chain_duration"].get("p50_ns", 0) / 1e3
+                    "lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms"),
+                    "launches": r["lp"]["launches"] + 6 * r["hp_chains"]}
     return out
 
 
-def aggregate_config4(parts: list) -> dict:
-    """Pool the per-rank config-4 legs: attainment = sum met / sum requests against each
-    rank's own exclusive p99 SLO; LP throughput = sum tiles / sum exclusive-LP tiles."""
+def _us(v):
+    return None if v is None else round(v / 1e3, 3)
+
+
+def aggregate_leg(parts: list, workload: str) -> dict:
+    """Pool one leg over ranks (replicas): attainment = sum met / sum requests against each
+    rank's own exclusive SLO; LP throughput = sum rate / sum exclusive-LP rate."""
     def att(key):
         met = tot = 0
         for p_ in parts:
@@ -246,25 +257,77 @@ def aggregate_config4(parts: list) -> dict:
             tot += len(rows)
         return met / max(1, tot)
 
-    exlp = sum(p_["exlp_tiles"] for p_ in parts)
-    res = {"workload": "cfg4 (BASELINE configs[3]) live: HP Llama-3.2-1B-geometry bs=1 decode (GEMV chain, "
-                       "2.47 GB/token) at 80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 "
-                       "axpy streamer; power governor on every LP-running policy",
-           "rate_req_s": parts[0]["rate"], "hp_step_ms": parts[0]["step_ms"],
-           "requests": sum(len(p_["ex_rows"]) for p_ in parts), "slo_attainment_exclusive": att(None),
-           "exclusive_step_p50_us": parts[0].get("ex_step_p50_us")}
-    for pol in CFG4_POLICIES:
+    exlp = sum(p_["exlp_rate"] for p_ in parts)
+    res = {"workload": workload, "rate_req_s": round(parts[0]["rate"], 3),
+           "requests": sum(len(p_["ex_rows"]) for p_ in parts),
+           "slo_attainment_exclusive": round(att(None), 4)}
+    for pol in LEG_POLICIES:
         ring = [x for p_ in parts for x in p_[pol]["ring"]]
-        res[pol] = {"slo_attainment": att(pol),
-                    "lp_throughput_vs_exclusive": sum(p_[pol]["tiles"] for p_ in parts) / max(1, exlp),
-                    "ring_to_first_hp_cta_p99_us": percentile(ring, 0.99) / 1e3 if ring else None,
-                    "flag_to_last_lp_exit_p99_us": (percentile(lx, 0.99) / 1e3) if (lx := [
-                        x for p_ in parts for x in p_[pol].get("lp_exit", [])]) else None,
-                    "hp_step_p50_us": parts[0][pol].get("step_p50_us"),
-                    "mean_lp_sms": parts[0][pol]["lp_sms"]}
-    res["lp_splitkernel_vs_reef_req"] = res["splitkernel"]["lp_throughput_vs_exclusive"] / max(
-        1e-9, res["reef_req"]["lp_throughput_vs_exclusive"])
+        infl = [x for p_ in parts for x in p_[pol]["inflight"]]
+        lx = [x for p_ in parts for x in p_[pol]["lp_exit"]]
+        res[pol] = {"slo_attainment": round(att(pol), 4),
+                    "lp_throughput_vs_exclusive": round(sum(p_[pol]["tiles_per_s"] for p_ in parts) / max(1e-9, exlp), 4),
+                    "ring_to_first_hp_cta_p99_us": _us(percentile(ring, 0.99)),
+                    "preempt_lp_in_flight_p99_us": _us(percentile(infl, 0.99)), "preempt_lp_in_flight_n": len(infl),
+                    "flag_to_last_lp_exit_p99_us": _us(percentile(lx, 0.99)),
+                    "hp_step_p50_us": round(parts[0][pol]["step_p50_us"], 1),
+                    "mean_lp_sms": round(parts[0][pol]["lp_sms"] or 0, 1)}
+    sk, kb = res["splitkernel"], res["reef_req"]
+    res["lp_splitkernel_vs_reef_req"] = round(sk["lp_throughput_vs_exclusive"] / max(1e-9, kb["lp_throughput_vs_exclusive"]), 3)
+    res["exclusive_step_p50_us"] = round(parts[0]["ex_step_p50_us"], 1)
+    p99 = sk["preempt_lp_in_flight_p99_us"] if sk["preempt_lp_in_flight_p99_us"] is not None else sk["ring_to_first_hp_cta_p99_us"]
+    res["targets"] = {"p99_le_10us": p99 is not None and p99 <= 10.0,
+                      "slo_within_1pt": sk["slo_attainment"] >= res["slo_attainment_exclusive"] - 0.01,
+                      "lp_ge_2x_kernel_boundary": res["lp_splitkernel_vs_reef_req"] >= 2.0}
     return res
+
+
+CFG4_WORKLOAD = ("cfg4 (BASELINE configs[3]): HP Llama-3.2-1B-geometry bs=1 decode (GEMV chain, 2.47 GB/token) at "
+                 "80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 axpy streamer; governed")
+
+
+# ----------------------------------------------------------------------------- host facts
+def host_info() -> dict:
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
+
+
+def numa_core_for(ordinal: int) -> int:
+    """A host core on the NUMA node of GPU `ordinal` (sysfs local_cpulist of its PCI
+    function), distinct per GPU on the same node; -1 if unknown."""
+    try:
+        import pynvml as N
+        N.nvmlInit()
+        buses = []
+        for i in range(N.nvmlDeviceGetCount()):
+            bid = N.nvmlDeviceGetPciInfo(N.nvmlDeviceGetHandleByIndex(i)).busId
+            bid = bid.decode() if isinstance(bid, bytes) else bid
+            buses.append(bid.lower()[-12:])
+        N.nvmlShutdown()
+
+        def cpus(bus):
+            txt = Path(f"/sys/bus/pci/devices/{bus}/local_cpulist").read_text().strip()
+            out = []
+            for part in txt.split(","):
+                a, _, b = part.partition("-")
+                out += list(range(int(a), int(b or a) + 1))
+            return out
+        mine = cpus(buses[ordinal])
+        allowed = os.sched_getaffinity(0)
+        mine = [c for c in mine if c in allowed] or sorted(allowed)
+        same = [i for i, b in enumerate(buses) if cpus(b) == cpus(buses[ordinal])]
+        # spread replicas over the node's cores; keep core 0 of the node for the OS / helpers
+        idx = 1 + same.index(ordinal) * max(1, (len(mine) - 1) // max(1, len(same)))
+        return mine[min(idx, len(mine) - 1)]
+    except Exception:
+        return -1
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -277,16 +340,19 @@ def main():
     ap.add_argument("--step-s", type=float, default=2.5)
     ap.add_argument("--warmup-s", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cfg4-s", type=float, default=10.0,
-                    help="config-4 leg (decode HP at 80%% load, governed): trace seconds; 0 skips it")
+    ap.add_argument("--baseline-windows", type=int, default=8,
+                    help="config-1 trace windows for the side runs (kernel-boundary baselines, governed variant)")
+    ap.add_argument("--cfg4-s", type=float, default=26.0,
+                    help="config-4 leg (decode HP at 80%% load, governed): trace seconds (>= 300 requests); 0 skips")
+    ap.add_argument("--detail", default=str(ROOT / "gpurun_out" / "bench_detail.json"),
+                    help="full per-leg results (the printed line is the compact summary)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if ws > 1:
+        # Replicas only: the process group is host plumbing for the final
+        # gather of per-GPU results — gloo, no NCCL, no data-path collective.
         import torch.distributed as dist
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
-        import torch
-        if args.impl == "ours":
-            torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
     if args.impl == "reference":
         run_reference_arm(args, ws, rank)
         if ws > 1:
@@ -297,31 +363,33 @@ def main():
     import torch
     from paper_2601_04071_b200.device import Device
     from paper_2601_04071_b200.live import Config1, live_run
+    torch.cuda.set_device(local)
 
     # Under ncu (kernel serialisation) the doorbell gates and the clock echo would wait on
     # host stores that are blocked behind them: run the same workload with direct HP
     # launches and no calibration.  Numbers printed in this mode are not bench values.
     profiling = "CUDA_INJECTION64_PATH" in os.environ or "NV_NSIGHT_INJECTION_TRANSPORT_TYPE" in os.environ
+    core = numa_core_for(local)  # this replica's scheduler thread: a core on its GPU's NUMA node
     dev = Device(local)
     w = Config1(dev)
-    if profiling:
-        _opts = w.options
-        w.options = lambda **kw: _opts(direct_hp=True, calibrate=False, **kw)  # noqa: E731
+    base_opts = w.options
+    w.options = lambda **kw: base_opts(pin_core=core, **(dict(direct_hp=True, calibrate=False) if profiling else {}),
+                                       **kw)  # noqa: E731
     calib = w.calibrate(reps=5)
     if rank == 0 and not profiling:  # a calibration taken under ncu replay is not a B200 timing
         (ROOT / "gpurun_out").mkdir(exist_ok=True)
         (ROOT / "gpurun_out" / "calib_b200.json").write_text(json.dumps(calib, indent=1))
     base_seed = 1000 + 10_000 * rank
     sc = lambda i, h: w.scenario(seed=base_seed + i, horizon_s=h)  # noqa: E731
+    nb = min(args.steps, args.baseline_windows)
 
     # --- reference runs for the other two metrics (same trace windows as the timed steps)
-    ex_rows, exlp_tiles, exlp_s = [], 0, 0.0
+    ex_rows = []
     for i in range(args.steps):
         ex = live_run(dev, sc(i, args.step_s), "exclusive", w.binding(), w.options(timeline=False))
         ex_rows += ex["requests"]["rows"]
-    ttft = percentile([r[1] for r in ex_rows if r[4]], 0.99)
-    tpot = percentile([r[2] for r in ex_rows if r[4]], 0.99)
-    slo = {"ttft_ns": ttft, "tpot_ns": tpot}
+    slo = {"ttft_ns": percentile([r[1] for r in ex_rows if r[4]], 0.99),
+           "tpot_ns": percentile([r[2] for r in ex_rows if r[4]], 0.99)}
     exlp = live_run(dev, sc(0, args.step_s), "exclusive_lp", w.binding(), w.options(timeline=False))
     exlp_rate = exlp["lp"]["tiles_per_s"]
 
@@ -332,17 +400,21 @@ def main():
     # --- timed steps
     torch.cuda.synchronize(local)
     barrier(ws)
-    samples, lp_exit, rows, tiles, launches, chains = [], [], [], 0, 0, 0
+    samples, inflight, idle, lp_exit, rows, tiles, launches, chains, pinned = [], [], [], [], [], 0, 0, 0, -1
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         for i in range(args.steps):
             r = live_run(dev, sc(i, args.step_s), "splitkernel", w.binding(), w.options(timeline=False, slo=slo))
-            samples += r["samples"]["preempt_ring_to_first_hp_cta"]
-            lp_exit += r["samples"]["preempt_flag_to_last_lp_exit"]
+            smp = r["samples"]
+            samples += smp["preempt_ring_to_first_hp_cta"]
+            inflight += smp["preempt_ring_to_first_hp_cta_lp_in_flight"]
+            idle += smp["preempt_ring_to_first_hp_cta_lp_idle"]
+            lp_exit += smp["preempt_flag_to_last_lp_exit"]
             rows += r["requests"]["rows"]
             tiles += r["lp"]["tiles_done"]
             launches += r["lp"]["launches"]
             chains += r["hp_chains"]
+            pinned = r.get("pinned_core", -1)
         torch.cuda.synchronize(local)
         wall = time.perf_counter() - t0
     barrier(ws)
@@ -351,54 +423,62 @@ def main():
     # --- kernel-boundary temporal-sharing baselines on the same windows: "reef" = the
     # reference's Reef policy (LP relaunched whenever HP drains, non-preemptible), and the
     # request-level variant (LP only between HP requests)
-    kb_rows, kb_tiles, kb_samples = [], 0, []
-    kbr_rows, kbr_tiles, kbr_samples = [], 0, []
-    for i in range(args.steps):
-        r = live_run(dev, sc(i, args.step_s), "reef", w.binding(), w.options(timeline=False))
-        kb_rows += r["requests"]["rows"]
-        kb_tiles += r["lp"]["tiles_done"]
-        kb_samples += r["samples"]["ring_to_first_hp_cta_all"]
-        r = live_run(dev, sc(i, args.step_s), "reef_req", w.binding(), w.options(timeline=False))
-        kbr_rows += r["requests"]["rows"]
-        kbr_tiles += r["lp"]["tiles_done"]
-        kbr_samples += r["samples"]["ring_to_first_hp_cta_all"]
+    kb = {"reef": {"rows": [], "tiles": 0, "samples": []}, "reef_req": {"rows": [], "tiles": 0, "samples": []}}
+    for i in range(nb):
+        for pol in kb:
+            r = live_run(dev, sc(i, args.step_s), pol, w.binding(), w.options(timeline=False))
+            kb[pol]["rows"] += r["requests"]["rows"]
+            kb[pol]["tiles"] += r["lp"]["tiles_done"]
+            kb[pol]["samples"] += r["samples"]["ring_to_first_hp_cta_all"]
 
     # --- power-governed variant: the same policy with the NVML clock-feedback governor
     # sizing LP's SM footprint so the GPU stays off its 1 kW cap and the HP chain keeps max
     # clocks (power; live.cpp PowerGovernor)
-    pb_rows, pb_tiles, pb_samples, pb_gov = [], 0, [], []
+    pb = {"rows": [], "tiles": 0, "samples": [], "inflight": [], "gov": []}
     with ClockSampler(local) as pclk:
-        for i in range(args.steps):
+        for i in range(nb):
             r = live_run(dev, sc(i, args.step_s), "splitkernel", w.binding(),
                          w.options(timeline=False, power_governor=True))
-            pb_gov.append(r.get("power_governor", {}).get("mean_lp_sms"))
-            pb_rows += r["requests"]["rows"]
-            pb_tiles += r["lp"]["tiles_done"]
-            pb_samples += r["samples"]["preempt_ring_to_first_hp_cta"]
+            pb["gov"].append(r.get("power_governor", {}).get("mean_lp_sms"))
+            pb["rows"] += r["requests"]["rows"]
+            pb["tiles"] += r["lp"]["tiles_done"]
+            pb["samples"] += r["samples"]["preempt_ring_to_first_hp_cta"]
+            pb["inflight"] += r["samples"]["preempt_ring_to_first_hp_cta_lp_in_flight"]
 
     # --- e2e: same metric through the C-ABI with the HP request buffers in pinned host
-    # memory (H2D of the input after the doorbell, D2H of the output before completion)
+    # memory (H2D of the input at admission, D2H of the output before completion)
     e2e = live_run(dev, sc(0, args.step_s), "splitkernel", w.binding(e2e=True), w.options(timeline=False))
     e2e_samples = e2e["samples"]["preempt_ring_to_first_hp_cta"]
 
-    cfg4 = run_config4_leg(dev, args.cfg4_s, 7 + 10_000 * rank) if args.cfg4_s > 0 and not profiling else None
+    cfg4 = None
+    if args.cfg4_s > 0 and not profiling:
+        from paper_2601_04071_b200.live import Config4
+        w4 = Config4(dev)
+        w4.options = (lambda f: (lambda **kw: f(pin_core=core, **kw)))(w4.options)
+        time.sleep(0.5)  # let the part leave the power cap the config-1 GEMM runs put it in
+        w4.calibrate()
+        cfg4 = run_policy_leg(dev, w4, args.cfg4_s, 7 + 10_000 * rank, w4.hp_rate(0.8), reef_s=min(args.cfg4_s, 8.0))
 
-    mine = {"cfg4": cfg4, "samples": samples, "lp_exit": lp_exit, "rows": rows, "tiles": tiles, "kb_rows": kb_rows,
-            "kb_tiles": kb_tiles, "kb_samples": kb_samples, "kbr_rows": kbr_rows, "kbr_tiles": kbr_tiles,
-            "kbr_samples": kbr_samples, "exlp_rate": exlp_rate, "ex_rows": ex_rows,
-            "step_ms": step_ms, "wall": wall, "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"],
-            "launches": launches, "chains": chains, "clocks": clk.summary(), "calib": calib,
-            "slo": slo, "pb_rows": pb_rows, "pb_tiles": pb_tiles, "pb_samples": pb_samples,
-            "pb_clocks": pclk.summary(), "pb_gov": pb_gov}
+    mine = {"cfg4": cfg4, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "rows": rows,
+            "tiles": tiles, "kb": kb, "exlp_rate": exlp_rate, "ex_rows": ex_rows, "step_ms": step_ms, "wall": wall,
+            "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"], "launches": launches,
+            "chains": chains, "clocks": clk.summary(), "calib": calib, "slo": slo, "pb": pb,
+            "pb_clocks": pclk.summary(), "core": pinned, "nb": nb}
     allr = gather(mine, ws)
     if rank != 0:
         dev.close()
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
 
-    agg = aggregate_ranks(allr, args.steps * args.step_s)
-    S_, LX, E2E = agg['S'], agg['LX'], agg['E2E']
-    lp_rate, kb_rate, ex_rate = agg['lp_rate'], agg['kb_rate'], agg['ex_rate']
-    att, att_ex, att_kb = agg['att'], agg['att_ex'], agg['att_kb']
+    H = args.steps * args.step_s
+    Hb = nb * args.step_s
+
+    agg = aggregate_ranks(allr, H, Hb)
+    S_, INF, IDL, LX, E2E = agg["S"], agg["INF"], agg["IDL"], agg["LX"], agg["E2E"]
+    ex_rate, lp_rate, kb_rate, pb_rate = agg["ex_rate"], agg["lp_rate"], agg["kb_rate"], agg["pb_rate"]
+    att_sk, att_ex = agg["att"], agg["att_ex"]
 
     # roofline of the dominant kernel (LP tcgen05 GEMM, 2*8192^3 per launch), timed alone
     # with CUDA events on its stream (ms_lp_time_full); peak = measured burst bf16.
@@ -410,59 +490,76 @@ def main():
     traffic = None
     if ncu.exists():
         traffic = json.loads(ncu.read_text()).get("tc_gemm_kernel<256>", {}).get("dram_bytes_per_launch")
-
+    cfg4_agg = aggregate_leg([r["cfg4"] for r in allr], CFG4_WORKLOAD) if allr[0]["cfg4"] else None
+    cb = None
+    if not args.no_cpu_baseline:
+        from paper_2601_04071_b200 import scenarios as S
+        cb = cpu_reference([S.config1(seed=1000 + i, horizon_s=args.step_s, calib=calib) for i in range(2)], 1)
+    p99 = _us(percentile(S_, 0.99))
+    p99_inf = _us(percentile(INF, 0.99))
+    kbr_lp = kb_rate["reef_req"] / max(1e-9, ex_rate)
     line = {
-        "metric": METRIC, "value": percentile(S_, 0.99) / 1e3, "unit": "us", "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": max(r["step_ms"] for r in allr), "higher_is_better": False,
+        "metric": METRIC, "value": p99, "unit": "us", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(max(r["step_ms"] for r in allr), 1), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": WORKLOAD, "step": f"one live {args.step_s}s trace window (fresh Poisson trace)",
                    "l2": "LP operands 384 MB > 126 MB L2 (no flush needed)", "parallelism": f"replicas x{ws}",
                    "preemption_latency_def": "HP doorbell ring -> first HP CTA (%globaltimer, drift-corrected)"},
-        "p50_us": percentile(S_, 0.50) / 1e3,
-        "preempt_samples": len(S_),
-        "lp_exit_p50_us": percentile(LX, 0.50) / 1e3 if LX else None,
-        "lp_exit_p99_us": percentile(LX, 0.99) / 1e3 if LX else None,
-        "slo_attainment": att, "slo_attainment_exclusive": att_ex,
-        "lp_throughput_vs_exclusive": lp_rate / max(1e-9, ex_rate),
-        "kernel_boundary_baseline": {"policy": "reef (reference Reef: LP relaunched whenever HP drains, "
-                                               "non-preemptible; HP waits at the LP kernel boundary)",
-                                     "slo_attainment": att_kb, "lp_throughput_vs_exclusive": kb_rate / max(1e-9, ex_rate),
-                                     "p99_us": percentile([x for r in allr for x in r["kb_samples"]], 0.99) / 1e3},
+        "p50_us": _us(percentile(S_, 0.50)), "preempt_samples": len(S_),
+        "preempt_lp_in_flight": {"p50_us": _us(percentile(INF, 0.5)), "p99_us": p99_inf, "n": len(INF)},
+        "preempt_lp_idle": {"p50_us": _us(percentile(IDL, 0.5)), "p99_us": _us(percentile(IDL, 0.99)), "n": len(IDL)},
+        "lp_exit_p50_us": _us(percentile(LX, 0.50)), "lp_exit_p99_us": _us(percentile(LX, 0.99)),
+        "slo_attainment": att_sk, "slo_attainment_exclusive": att_ex,
+        "lp_throughput_vs_exclusive": round(lp_rate / max(1e-9, ex_rate), 4),
+        "lp_vs_kernel_boundary": round(lp_rate / max(1e-9, kb_rate["reef"]), 3),
+        "lp_vs_kernel_boundary_request_level": round(lp_rate / max(1e-9, kb_rate["reef_req"]), 3),
+        "kernel_boundary_baseline": {"policy": "reef (reference Reef: non-preemptible LP relaunched when HP drains)",
+                                     "slo_attainment": agg["att_kb"]["reef"],
+                                     "lp_throughput_vs_exclusive": round(kb_rate["reef"] / max(1e-9, ex_rate), 4),
+                                     "p99_us": _us(percentile(agg["kb_samples"]["reef"], 0.99))},
         "kernel_boundary_request_level": {"policy": "reef_req (LP only between HP requests)",
-                                          "slo_attainment": agg["att_kbr"],
-                                          "lp_throughput_vs_exclusive": agg["kbr_rate"] / max(1e-9, ex_rate),
-                                          "p99_us": percentile([x for r in allr for x in r.get("kbr_samples", [])], 0.99) / 1e3
-                                          if any(r.get("kbr_samples") for r in allr) else None},
-        "lp_vs_kernel_boundary": lp_rate / max(1e-9, kb_rate),
-        "power_governed_variant": {"policy": "splitkernel + NVML clock-feedback power governor sizing LP's SM "
-                                             "footprint (live option power_governor)",
-                                 "mean_lp_sms": [x for r in allr for x in r["pb_gov"]],
-                                 "slo_attainment": agg["att_pb"],
-                                 "lp_throughput_vs_exclusive": agg["pb_rate"] / max(1e-9, ex_rate),
-                                 "p99_us": percentile([x for r in allr for x in r["pb_samples"]], 0.99) / 1e3,
-                                 "clocks": allr[0]["pb_clocks"]},
-        "slo_ns": allr[0]["slo"],
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                                          "slo_attainment": agg["att_kb"]["reef_req"],
+                                          "lp_throughput_vs_exclusive": round(kbr_lp, 4),
+                                          "p99_us": _us(percentile(agg["kb_samples"]["reef_req"], 0.99))},
+        "power_governed_variant": {"policy": "splitkernel + NVML clock-feedback governor sizing LP's SM footprint",
+                                   "mean_lp_sms": round(statistics.mean(agg["pb_gov"] or [0]), 1),
+                                   "slo_attainment": agg["att_pb"],
+                                   "lp_throughput_vs_exclusive": round(pb_rate / max(1e-9, ex_rate), 4),
+                                   "p99_us": _us(percentile(agg["pb_samples"], 0.99)),
+                                   "preempt_lp_in_flight_p99_us": _us(percentile(agg["pb_inflight"], 0.99)),
+                                   "clocks": {k: allr[0]["pb_clocks"].get(k) for k in ("sm_mhz", "reasons")}},
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": "tc_gemm_kernel<256> (LP 8192^3 bf16, 2048 128x256 tiles)",
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
-        "e2e": {"value": percentile(E2E, 0.99) / 1e3 if E2E else None, "unit": "us",
+        "e2e": {"value": _us(percentile(E2E, 0.99)), "unit": "us",
                 "h2d_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),
                 "d2h_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),
-                "what": "same metric, HP request input H2D from pinned host after the doorbell, output D2H"},
+                "what": "same metric through ms_live_run with the request input H2D (pinned host) at admission and "
+                        "the output D2H before completion"},
         "gpu_launches": int(sum(r["launches"] + 6 * r["chains"] for r in allr)),
         "clocks": allr[0]["clocks"],
-        "calib": allr[0]["calib"],
-        "config4_decode_high_load": aggregate_config4([r["cfg4"] for r in allr]) if allr[0]["cfg4"] else None,
+        "host": dict(host_info(), scheduler_cores=[r["core"] for r in allr]),
+        "config4_decode_high_load": cfg4_agg,
     }
-    if not args.no_cpu_baseline:
-        from paper_2601_04071_b200 import scenarios as S
-        cb = cpu_reference([S.config1(seed=1000 + i, horizon_s=args.step_s, calib=calib) for i in range(2)], 1)
+    if cb:
         line["cpu_baseline"] = {"value": cb["p99_us"], "unit": "us", "cores": 1, "kind": "reference",
                                 "sample": f"reference Engine::run() replay of 2 x {args.step_s}s config-1 windows "
                                           f"(splitkernel+exclusive+exclusive_lp), {cb['events']} events in "
                                           f"{cb['wall_s']:.2f}s; modelled delay floor = launch_overhead",
-                                "lp_throughput_vs_exclusive": cb["lp_norm"]}
+                                "lp_throughput_vs_exclusive": round(cb["lp_norm"], 4)}
+    line["targets"] = {
+        "cfg1": {"p99_le_10us": (p99_inf if p99_inf is not None else p99) <= 10.0,
+                 "slo_within_1pt": att_sk >= att_ex - 0.01,
+                 "lp_ge_2x_kernel_boundary": round(lp_rate / max(1e-9, kb_rate["reef_req"]), 3) >= 2.0},
+        "cfg4": cfg4_agg["targets"] if cfg4_agg else None}
+    try:
+        Path(args.detail).parent.mkdir(parents=True, exist_ok=True)
+        Path(args.detail).write_text(json.dumps({"line": line, "calib": calib, "slo_ns": allr[0]["slo"],
+                                                 "cfg4_raw_slo": [r["cfg4"]["slo"] for r in allr if r["cfg4"]]},
+                                                indent=1))
+    except OSError:
+        pass
     print(json.dumps(line), flush=True)
     dev.close()
     if ws > 1:

@@ -107,6 +107,12 @@ int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint6
 }
 
 constexpr int kRedoCap = 8192;
+
+// FFI callers may pass any id: every entry point that indexes a slot checks it first.
+#define MS_CHECK_LP(d, id) \
+  if (!(d) || (id) < 0 || (id) >= MS_MAX_LP || !(d)->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id")
+#define MS_CHECK_CHAIN(d, cid) \
+  if (!(d) || (cid) < 0 || (cid) >= MS_MAX_HP_CHAINS || !(d)->chains[cid].used) return fail(MS_E_ARG, "bad chain")
 constexpr int kAxpyMaxPad = 200 * 1024;  // residency-capping dynamic smem of the HBM streamer
 constexpr int kGateSmem = 40 * 1024;
 
@@ -165,6 +171,10 @@ struct HpChain {
   GemvOpDesc* gemv_descs_d = nullptr;  // device copy (bulk-loaded by every CTA)
   uint32_t* wire_d = nullptr;       // tagged op->op handoff words
   mutable uint32_t launches = 0;    // wire tag source (one tag per launch, stream-ordered)
+  // Leading H2D ops (e2e request input) run on the hpcopy stream when armed; the chain
+  // kernels wait for this event.
+  int lead_copies = 0;
+  cudaEvent_t in_ev = nullptr;
 };
 
 }  // namespace
@@ -174,6 +184,10 @@ struct ms_dev {
   cudaDeviceProp prop{};
   int prio_low = 0, prio_high = 0;
   cudaStream_t lp = nullptr, hp = nullptr, aux = nullptr;
+  // e2e request input: an armed chain whose first op is an H2D copy gets a second gate on
+  // this stream, so the copy engine starts at the ring, concurrent with the LP drain; the
+  // chain on `hp` waits for the copy's event instead of queueing the copy itself.
+  cudaStream_t hpcopy = nullptr;
   MsHostPage* page = nullptr;    // host view
   MsHostPage* page_d = nullptr;  // device view of the same page
   MsDevMirror* mirror = nullptr;
@@ -784,10 +798,10 @@ int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool 
 }
 
 // Enqueue a chain's work on the HP stream (after its gate when `after_gate`).
-int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after_gate) {
+int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after_gate, size_t first_op = 0) {
   // batch-1 chains have no per-op kernels: the GEMV chain is their only implementation
   const bool fused = (d->hp_fused && ch.fusable) || ch.gemv;
-  for (size_t i = 0; i < ch.ops.size(); ++i) {
+  for (size_t i = first_op; i < ch.ops.size(); ++i) {
     if (fused && static_cast<int>(i) >= ch.fused_first && static_cast<int>(i) <= ch.fused_last) {
       if (static_cast<int>(i) == ch.fused_first) {
         const bool pdl = after_gate && i == 0;
@@ -828,6 +842,7 @@ int ms_dev_open(int ordinal, ms_dev** out) {
   MS_CUDA(cudaStreamCreateWithPriority(&d->lp, cudaStreamNonBlocking, d->prio_low));
   MS_CUDA(cudaStreamCreateWithPriority(&d->hp, cudaStreamNonBlocking, d->prio_high));
   MS_CUDA(cudaStreamCreateWithPriority(&d->aux, cudaStreamNonBlocking, d->prio_low));
+  MS_CUDA(cudaStreamCreateWithPriority(&d->hpcopy, cudaStreamNonBlocking, d->prio_high));
   MS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&d->page), sizeof(MsHostPage),
                         cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(d->page, 0, sizeof(MsHostPage));
@@ -865,6 +880,7 @@ int ms_dev_close(ms_dev* d) {
   cudaStreamDestroy(d->lp);
   cudaStreamDestroy(d->hp);
   cudaStreamDestroy(d->aux);
+  cudaStreamDestroy(d->hpcopy);
   delete d;
   return 0;
 }
@@ -1030,7 +1046,7 @@ int ms_lp_run(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget) 
 }
 
 int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budget, int flags) {
-  if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
+  MS_CHECK_LP(d, id);
   LpSlot& s = d->lp_slots[id];
   if (end > s.total_tiles || begin > end) return fail(MS_E_ARG, "tile range out of bounds");
   if (budget > end) budget = end;
@@ -1189,14 +1205,16 @@ int ms_debug_stamps(ms_dev* d, int enable, unsigned long long* out, size_t n) {
 }
 
 uint64_t ms_lp_total_tiles(ms_dev* d, int id) {
-  return (id >= 0 && id < MS_MAX_LP && d->lp_slots[id].used) ? d->lp_slots[id].total_tiles : 0;
+  return (d && id >= 0 && id < MS_MAX_LP && d->lp_slots[id].used) ? d->lp_slots[id].total_tiles : 0;
 }
 
 uint64_t ms_lp_progress(ms_dev* d, int id) {
+  if (!d || id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return 0;
   return __atomic_load_n(&d->page->progress[id], __ATOMIC_ACQUIRE);
 }
 
 int ms_lp_set_budget(ms_dev* d, int id, uint64_t budget) {
+  MS_CHECK_LP(d, id);
   LpSlot& s = d->lp_slots[id];
   if (budget > s.last_end) budget = s.last_end;
   __atomic_store_n(&d->page->lp_line[id].budget, ((s.run_id & 0xFFFFFFull) << 40) | budget, __ATOMIC_RELEASE);
@@ -1204,6 +1222,8 @@ int ms_lp_set_budget(ms_dev* d, int id, uint64_t budget) {
 }
 
 int ms_lp_poll(ms_dev* d, int id, ms_lp_status* st) {
+  MS_CHECK_LP(d, id);
+  if (!st) return fail(MS_E_ARG, "null status");
   LpSlot& s = d->lp_slots[id];
   const MsLpExit& e = d->page->lp_exit[id];
   const uint64_t rid = __atomic_load_n(&e.run_id, __ATOMIC_ACQUIRE);
@@ -1227,9 +1247,12 @@ int ms_lp_poll(ms_dev* d, int id, ms_lp_status* st) {
 }
 
 int ms_lp_wait(ms_dev* d, int id, int64_t timeout_ns, ms_lp_status* st) {
+  MS_CHECK_LP(d, id);
+  if (!d->lp_slots[id].launched) return fail(MS_E_ARG, "LP kernel has no run to wait for");
   const int64_t t0 = now_ns();
   for (;;) {
     const int r = ms_lp_poll(d, id, st);
+    if (r < 0) return r;
     if (r) return 0;
     if (timeout_ns >= 0 && now_ns() - t0 > timeout_ns) {
       const cudaError_t e = cudaStreamQuery(d->lp);
@@ -1241,7 +1264,14 @@ int ms_lp_wait(ms_dev* d, int id, int64_t timeout_ns, ms_lp_status* st) {
 }
 
 int ms_lp_reset(ms_dev* d, int id) {
-  d->lp_slots[id].redo_carry = 0;
+  MS_CHECK_LP(d, id);
+  LpSlot& s = d->lp_slots[id];
+  // A run still in flight would publish a carry after the reset: refuse.
+  if (s.launched && __atomic_load_n(&d->page->lp_exit[id].run_id, __ATOMIC_ACQUIRE) != s.run_id)
+    return fail(MS_E_ARG, "ms_lp_reset: an LP run is still in flight");
+  s.redo_carry = 0;
+  // The last exit record is consumed: a later ms_lp_poll must not restore its carry.
+  s.launched = false;
   return 0;
 }
 
@@ -1364,6 +1394,10 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
   } else if (int rc = plan_fused(d, ch)) {
     return rc;
   }
+  while (ch.lead_copies < static_cast<int>(ch.ops.size()) && ch.ops[ch.lead_copies].op.kind == MS_HP_H2D)
+    ++ch.lead_copies;
+  if (ch.lead_copies == static_cast<int>(ch.ops.size())) ch.lead_copies = 0;  // copy-only chain: plain path
+  if (ch.lead_copies) MS_CUDA(cudaEventCreateWithFlags(&ch.in_ev, cudaEventDisableTiming));
   ch.used = true;
   d->chains[cid] = ch;
   *chain_id = cid;
@@ -1373,7 +1407,9 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
 int ms_hp_unregister_chain(ms_dev* d, int cid) {
   if (cid < 0 || cid >= MS_MAX_HP_CHAINS || !d->chains[cid].used) return fail(MS_E_ARG, "bad chain");
   MS_CUDA(cudaStreamSynchronize(d->hp));
+  MS_CUDA(cudaStreamSynchronize(d->hpcopy));
   HpChain& ch = d->chains[cid];
+  if (ch.in_ev) cudaEventDestroy(ch.in_ev);
   for (HpOpRt& o : ch.ops) {
     if (o.ws) cudaFree(o.ws);
     if (o.tile_cnt) cudaFree(o.tile_cnt);
@@ -1404,35 +1440,63 @@ int ms_hp_chain_info(ms_dev* d, int cid, int* fused_grid, int* cluster) {
 }
 
 int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
+  MS_CHECK_CHAIN(d, cid);
   const HpChain& ch = d->chains[cid];
-  if (!ch.used) return fail(MS_E_ARG, "bad chain");
   // 40 KB of (unused) shared memory keeps a 193 KB LP GEMM CTA off the gate's SM: an LP
   // CTA co-resident with the spinning gate observed preemptions ~5 us late.
   static const int gate_smem = [] {
     const char* e = std::getenv("MS_GATE_SMEM");
     return e ? std::max(0, std::min(atoi(e), kGateSmem)) : kGateSmem;
   }();
+  if (ch.lead_copies > 0) {
+    // e2e input: its own gate on the copy stream, so the H2D starts at the ring (no SM
+    // work needed, it overlaps the LP drain); the chain waits for the copy's event.
+    gate_kernel<<<1, 32, gate_smem, d->hpcopy>>>(&d->page_d->doorbell, seq, nullptr, nullptr);  // (smem: stays off LP SMs)
+    MS_CUDA(cudaGetLastError());
+    for (int i = 0; i < ch.lead_copies; ++i) {
+      const ms_hp_op& op = ch.ops[i].op;
+      MS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(op.c), reinterpret_cast<const void*>(op.a),
+                              static_cast<size_t>(op.m), cudaMemcpyDefault, d->hpcopy));
+    }
+    MS_CUDA(cudaEventRecord(ch.in_ev, d->hpcopy));
+  }
   gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
+  if (ch.lead_copies > 0) {
+    MS_CUDA(cudaStreamWaitEvent(d->hp, ch.in_ev, 0));
+    return launch_chain(d, cid, ch, seq, false, static_cast<size_t>(ch.lead_copies));
+  }
   return launch_chain(d, cid, ch, seq, true);
 }
 
 uint32_t ms_hp_next_seq(ms_dev* d) { return ++d->hp_seq; }
 
 int ms_hp_ring(ms_dev* d, uint32_t seq, int64_t* t_host) {
+  if (!d) return fail(MS_E_ARG, "null device");
   const uint64_t e = __atomic_load_n(&d->page->epoch, __ATOMIC_ACQUIRE);
-  __atomic_store_n(&d->page->doorbell, (e << 32) | seq, __ATOMIC_RELEASE);
+  // The doorbell only moves forward (serial-number order on the seq): ringing an older seq
+  // must not re-close a gate a newer ring already opened.
+  uint64_t cur = __atomic_load_n(&d->page->doorbell, __ATOMIC_ACQUIRE);
+  for (;;) {
+    const uint32_t s_cur = static_cast<uint32_t>(cur);
+    const uint32_t s_new = static_cast<int32_t>(seq - s_cur) >= 0 ? seq : s_cur;
+    if (__atomic_compare_exchange_n(&d->page->doorbell, &cur, (e << 32) | s_new, false, __ATOMIC_RELEASE,
+                                    __ATOMIC_ACQUIRE))
+      break;
+  }
   if (t_host) *t_host = now_ns();
   return 0;
 }
 
 int ms_hp_launch_direct(ms_dev* d, int cid, uint32_t seq) {
+  MS_CHECK_CHAIN(d, cid);
   const HpChain& ch = d->chains[cid];
-  if (!ch.used) return fail(MS_E_ARG, "bad chain");
   return launch_chain(d, cid, ch, seq, false);
 }
 
 int ms_hp_poll(ms_dev* d, int cid, uint32_t seq, ms_hp_times* t) {
+  MS_CHECK_CHAIN(d, cid);
+  if (!t) return fail(MS_E_ARG, "null times");
   const MsHpRecord& r = d->page->hp[cid];
   // 16-byte atomic read of the completion pair (aligned SSE load; written by one PCIe write).
   const __m128i v = _mm_load_si128(reinterpret_cast<const __m128i*>(&r.done_first));
@@ -1449,9 +1513,12 @@ int ms_hp_poll(ms_dev* d, int cid, uint32_t seq, ms_hp_times* t) {
 }
 
 int ms_hp_wait(ms_dev* d, int cid, uint32_t seq, int64_t timeout_ns, ms_hp_times* t) {
+  MS_CHECK_CHAIN(d, cid);
   const int64_t t0 = now_ns();
   for (;;) {
-    if (ms_hp_poll(d, cid, seq, t)) return 0;
+    const int r = ms_hp_poll(d, cid, seq, t);
+    if (r < 0) return r;
+    if (r) return 0;
     if (timeout_ns >= 0 && now_ns() - t0 > timeout_ns) {
       const cudaError_t e = cudaStreamQuery(d->hp);
       if (e != cudaSuccess && e != cudaErrorNotReady)
@@ -1496,6 +1563,8 @@ int ms_clock_calibrate(ms_dev* d, int rounds, int64_t* offset_ns, int64_t* rtt_m
 }
 
 int ms_lp_time_full(ms_dev* d, int id, int reps, float* ms_per_run) {
+  MS_CHECK_LP(d, id);
+  if (reps < 1) return fail(MS_E_ARG, "reps must be >= 1");
   LpSlot& s = d->lp_slots[id];
   cudaEvent_t a, b;
   MS_CUDA(cudaEventCreate(&a));
@@ -1519,7 +1588,7 @@ int ms_lp_time_full(ms_dev* d, int id, int reps, float* ms_per_run) {
 }
 
 int ms_lp_time_range(ms_dev* d, int id, uint64_t begin, uint64_t end, int reps, float* ms_per_run) {
-  if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
+  MS_CHECK_LP(d, id);
   LpSlot& s = d->lp_slots[id];
   if (begin >= end || end > s.total_tiles || reps < 1) return fail(MS_E_ARG, "bad tile range");
   cudaEvent_t a, b;
@@ -1530,10 +1599,8 @@ int ms_lp_time_range(ms_dev* d, int id, uint64_t begin, uint64_t end, int reps, 
   if (int rc = ms_lp_run(d, id, begin, end, end)) return rc;  // warm-up
   if (int rc = ms_lp_wait(d, id, 20000000000ll, &st)) return rc;
   MS_CUDA(cudaEventRecord(a, d->lp));
-  for (int i = 0; i < reps; ++i) {
-    ms_lp_reset(d, id);
+  for (int i = 0; i < reps; ++i)  // unpreempted runs leave no redo carry
     if (int rc = ms_lp_run(d, id, begin, end, end)) return rc;
-  }
   MS_CUDA(cudaEventRecord(b, d->lp));
   MS_CUDA(cudaEventSynchronize(b));
   float ms = 0;
@@ -1546,6 +1613,8 @@ int ms_lp_time_range(ms_dev* d, int id, uint64_t begin, uint64_t end, int reps, 
 }
 
 int ms_hp_time_chain(ms_dev* d, int cid, int reps, float* ms_per_chain) {
+  MS_CHECK_CHAIN(d, cid);
+  if (reps < 1) return fail(MS_E_ARG, "reps must be >= 1");
   cudaEvent_t a, b;
   MS_CUDA(cudaEventCreate(&a));
   MS_CUDA(cudaEventCreate(&b));

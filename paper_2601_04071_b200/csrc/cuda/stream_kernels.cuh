@@ -286,12 +286,16 @@ __global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpReco
         if (atomicExch(&rung, 1u) == 0) {
           word = v;
           const uint32_t epoch = static_cast<uint32_t>(v >> 32);
+          if (mirror) {
 #pragma unroll
-          for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&mirror->epoch[c * MS_MIRROR_STRIDE], epoch);
+            for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&mirror->epoch[c * MS_MIRROR_STRIDE], epoch);
+          }
           pdl_launch_dependents();
-          const unsigned long long t = globaltimer();
-          st_relaxed_sys_u64(&rec->t_gate, t);
-          st_release_sys_u32(&rec->seq_gate, seq);
+          if (rec) {  // (the e2e input-copy gate carries no record)
+            const unsigned long long t = globaltimer();
+            st_relaxed_sys_u64(&rec->t_gate, t);
+            st_release_sys_u32(&rec->seq_gate, seq);
+          }
         }
         break;
       }

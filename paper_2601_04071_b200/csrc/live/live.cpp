@@ -15,6 +15,8 @@
 // see the same arrivals, iteration counts and bubble lengths.
 #include <cuda_runtime_api.h>
 #include <dlfcn.h>
+#include <pthread.h>
+#include <sched.h>
 #include <nvml.h>
 #include <time.h>
 
@@ -151,6 +153,12 @@ class LiveRun {
         lp_.push_back(std::move(l));
       }
     }
+    // One HP doorbell lane per device: every armed gate sits on the one HP stream and opens
+    // for doorbell >= its seq, so a second HP task's ring would release the first task's
+    // pre-armed chain.  The replay core models any number of HP streams; live runs refuse.
+    if (hp_.size() > 1)
+      throw ValidationError("tasks", "live B200 runtime supports one high-priority task per device (got " +
+                                         std::to_string(hp_.size()) + ")");
     lp_bind_ = binding.contains("lp") ? binding.at("lp") : json::object();
     if (opts.contains("tile_ns")) tile_ns_ = opts.at("tile_ns");
     art_.policy = policy_ == "splitkernel" ? Policy::SplitKernel
@@ -291,8 +299,8 @@ class LiveRun {
   void hp_chain_done(HpTask& h, const ms_hp_times& tm) {
     h.inflight = false;
     // Device timestamps are converted after the run with a drift-corrected clock fit.
-    HpSample smp{h.ring_t, tm.t_first_cta, tm.t_done, tm.t_gate, pending_preempt_.has_value(), h.index, tm.seq,
-                 now_};
+    HpSample smp{h.ring_t, tm.t_first_cta, tm.t_done, tm.t_gate, pending_preempt_.has_value(),
+                 pending_preempt_.has_value() && pending_preempt_->lp_in_flight, h.index, tm.seq, now_};
     hp_samples_.push_back(smp);
     if (pending_preempt_) {
       art_.preemptions.push_back(*pending_preempt_);  // delay filled in at the end
@@ -413,8 +421,6 @@ class LiveRun {
     l.dev_id = lp_bind_.at(l.kernel).get<int>();
     l.tile_ns = tile_ns_.contains(l.kernel) ? tile_ns_.at(l.kernel).get<Ns>() : 50000;
     check(ms_lp_reset(dev_, l.dev_id), "ms_lp_reset");
-    ms_lp_status st{};
-    ms_lp_poll(dev_, l.dev_id, &st);
     l.total = ms_lp_total_tiles(dev_, l.dev_id);
     l.cursor = 0;
     l.redo = 0;
@@ -572,6 +578,7 @@ class LiveRun {
     Ns ring;
     uint64_t first, done, gate;
     bool preempt;
+    bool lp_in_flight;  // an LP run was resident when HP turned active (engine.hpp:954-960)
     int stream;
     uint32_t seq;
     Ns detect;  // host time the scheduler saw the completion
@@ -604,7 +611,8 @@ class LiveRun {
   uint64_t lp_budget_ = 0, run_begin_ = 0, run_redo_in_ = 0;
   uint64_t lp_tiles_done_ = 0, lp_launches_ = 0, lp_preemptions_ = 0, budget_extensions_ = 0;
   std::vector<Ns> ring_to_first_, preempt_delays_, lp_exit_lat_, lp_seen_lat_, gate_to_first_, chain_durations_;
-  std::vector<Ns> lp_queued_exit_lat_;  // preempted runs that had not started at the raise
+  std::vector<Ns> lp_queued_exit_lat_;
+  std::vector<Ns> preempt_inflight_, preempt_idle_;  // HP activations with / without LP resident  // preempted runs that had not started at the raise
   RunArtifacts art_;
 
 };
@@ -627,6 +635,27 @@ json summarize(const std::vector<Ns>& v) {
 }
 
 json LiveRun::run() {
+  // Optional: pin the scheduler thread (the caller's) to one host core for the run — the
+  // multi-GPU replicas each get a core on their GPU's NUMA node.  Helper threads created
+  // before this point (power governor) keep the process mask.
+  cpu_set_t saved;
+  bool pinned = false;
+  if (opts_.contains("pin_core") && opts_.at("pin_core").get<int>() >= 0) {
+    const int core = opts_.at("pin_core").get<int>();
+    if (pthread_getaffinity_np(pthread_self(), sizeof saved, &saved) == 0) {
+      cpu_set_t one;
+      CPU_ZERO(&one);
+      CPU_SET(core, &one);
+      pinned = pthread_setaffinity_np(pthread_self(), sizeof one, &one) == 0;
+    }
+  }
+  struct Unpin {
+    bool on;
+    cpu_set_t* mask;
+    ~Unpin() {
+      if (on) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), mask);
+    }
+  } unpin{pinned, &saved};
   // Clock calibration: device %globaltimer -> host monotonic.
   int64_t rtt = 0, rtt1 = 0;
   {
@@ -715,6 +744,7 @@ json LiveRun::run() {
     if (smp.preempt && pi < art_.preemptions.size()) {
       art_.preemptions[pi].delay = first - smp.ring;
       preempt_delays_.push_back(first - smp.ring);
+      (smp.lp_in_flight ? preempt_inflight_ : preempt_idle_).push_back(first - smp.ring);
       emit(first, EventKind::PreemptEnd, smp.stream, hp_[smp.stream].spec->name,
            "delay_ns=" + std::to_string(first - smp.ring));
       ++pi;
@@ -742,6 +772,7 @@ json LiveRun::run() {
   out["scenario"] = json(sc_.name);
   out["horizon_ns"] = json(static_cast<long long>(sc_.horizon));
   out["loops"] = json(static_cast<unsigned long long>(loops));
+  out["pinned_core"] = json(pinned ? opts_.at("pin_core").get<int>() : -1);
   out["clock"] = json::object();
   out["clock"]["offset_ns"] = json(static_cast<long long>(off0_));
   out["clock"]["drift_ppm"] = json(c1_ > c0_ ? 1e6 * static_cast<double>(off1_ - off0_) / static_cast<double>(c1_ - c0_) : 0.0);
@@ -764,6 +795,9 @@ json LiveRun::run() {
   out["requests"]["rows"] = std::move(reqs);  // [arrival, ttft, tpot, iterations, completed]
   out["preempt_ring_to_first_hp_cta"] = summarize(preempt_delays_);
   out["ring_to_first_hp_cta_all"] = summarize(ring_to_first_);
+  // true preemptions (LP resident when HP turned active) vs activations on an LP-idle GPU
+  out["preempt_ring_to_first_hp_cta_lp_in_flight"] = summarize(preempt_inflight_);
+  out["preempt_ring_to_first_hp_cta_lp_idle"] = summarize(preempt_idle_);
   // host-side HP path: chain done (device) -> scheduler saw it; bubble end due -> handled
   out["hp_done_detect_lag"] = summarize(detect_lag_);
   out["bubble_timer_late"] = summarize(timer_late_);
@@ -781,6 +815,12 @@ json LiveRun::run() {
   for (const Ns x : lp_exit_lat_) b.push_back(json(static_cast<long long>(x)));
   raw["preempt_ring_to_first_hp_cta"] = std::move(a);
   raw["preempt_flag_to_last_lp_exit"] = std::move(b);
+  json fi = json::array();
+  for (const Ns x : preempt_inflight_) fi.push_back(json(static_cast<long long>(x)));
+  raw["preempt_ring_to_first_hp_cta_lp_in_flight"] = std::move(fi);
+  json fid = json::array();
+  for (const Ns x : preempt_idle_) fid.push_back(json(static_cast<long long>(x)));
+  raw["preempt_ring_to_first_hp_cta_lp_idle"] = std::move(fid);
   json c = json::array();
   for (const Ns x : ring_to_first_) c.push_back(json(static_cast<long long>(x)));
   raw["ring_to_first_hp_cta_all"] = std::move(c);

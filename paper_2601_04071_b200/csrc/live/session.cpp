@@ -187,8 +187,10 @@ struct ms_session {
           }
           samples.push_back({ring, t.t_gate, t.t_first_cta, t.t_done});
           last_armed_chain = chain;
-          running.store(0, std::memory_order_release);
+          // hp_pending first: once running reads 0 a submit may proceed and set
+          // hp_pending = 1 for the next chain, which a later clear would wipe.
           hp_pending.store(0, std::memory_order_seq_cst);
+          running.store(0, std::memory_order_release);
           last_hp = now_mono();
           harvesting = false;
         }
@@ -205,7 +207,8 @@ struct ms_session {
       }
       // Arm the next chain at the start of the tenant's bubble (it is on the GPU long before
       // the next submit), or right away when a submit is waiting for it.
-      if ((hint > 0 || want_arm.load(std::memory_order_acquire)) && !armed.load() && !running.load()) {
+      if ((hint > 0 || want_arm.load(std::memory_order_acquire)) && !armed.load() && !running.load() &&
+          !hp_pending.load(std::memory_order_seq_cst)) {
         const int nc = next_chain.load();
         arm_next(nc >= 0 ? nc : last_armed_chain);
         want_arm.store(0, std::memory_order_release);

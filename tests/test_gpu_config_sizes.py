@@ -1,0 +1,180 @@
+"""Tenant-kernel parity at the EXACT config sizes, against the C
+restatement in oracle/tenant_ref.c, through the C-ABI:
+  * config-1 HP chain: 4 x [128 x 4096] x [4096 x 4096] + bias/GELU (fused launch);
+  * config-4 HP step: the full 16-layer Llama-3.2-1B-geometry bs=1 decode step with the
+    128,256-row LM head (GEMV chain), oracle logits on every vocab row;
+  * config-4 LP2 streamer: axpy over 2^30 bf16 elements, bit-exact.
+Both error measures are asserted and recorded (gpurun_out/parity_config_sizes.json):
+normwise = max|got - want| / max|want| (north_star bf16 <= 1e-2), and elementwise =
+max |got - want| / max(|want|, 1e-2 * max|want|) (per element, floored at 1% of the
+output's range so exact zeros do not divide)."""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = 1e-2
+SEED = 4242
+OUT = Path(__file__).resolve().parents[1] / "gpurun_out" / "parity_config_sizes.json"
+RESULTS = {}
+
+
+def errs(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    err = np.abs(got - want)
+    scale = np.max(np.abs(want))
+    return float(np.max(err) / scale), float(np.max(err / np.maximum(np.abs(want), 1e-2 * scale)))
+
+
+def record(name, **kw):
+    RESULTS[name] = kw
+    OUT.parent.mkdir(exist_ok=True)
+    OUT.write_text(json.dumps(RESULTS, indent=1))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2601_04071_b200.device import Device
+    d = Device(0)
+    yield d
+    d.close()
+
+
+@pytest.fixture(scope="module")
+def T():
+    from oracle import tenant
+    return tenant
+
+
+def d2h(dev, ptr, n):
+    out = np.empty(n, np.uint16)
+    dev.d2h(out.ctypes.data, ptr, n * 2)
+    return out
+
+
+def rnd(y):  # fp32 -> bf16 bits (RNE), like the device epilogues
+    u = np.ascontiguousarray(y, dtype=np.float32).view(np.uint32)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def test_config1_hp_chain_full_size(dev, T):
+    """The config-1 HP segment exactly as Config1 registers it (H = 4096, fused cluster
+    launch), every output element of every op against the oracle chain."""
+    M, H = 128, 4096
+    act = [dev.alloc(M * H * 2) for _ in range(5)]
+    ws = [dev.alloc(H * H * 2) for _ in range(4)]
+    bias, out = dev.alloc(H * 2), dev.alloc(M * H * 2)
+    s = float(np.float32(1 / math.sqrt(H)))
+    dev.fill_synth(act[0], M * H, SEED, 100, 1.0)
+    for i, w in enumerate(ws):
+        dev.fill_synth(w, H * H, SEED, 101 + i, s)
+    dev.fill_synth(bias, H, SEED, 110, 0.1)
+    ops = [dict(kind=1, block_n=128, a=act[i], b=ws[i], c=act[i + 1], bias=0, m=M, n=H, k=H) for i in range(4)]
+    ops.append(dict(kind=2, block_n=0, a=act[4], b=0, c=out, bias=bias, m=M, n=H, k=0))
+    chain = dev.hp_register_chain(ops)
+    assert dev.hp_chain_info(chain)["cluster"] == 4  # the fused DSMEM plan the bench runs
+    dev.hp_launch_direct(chain, dev.hp_next_seq())
+    dev.sync()
+    x = T.synth_bf16(M * H, SEED, 100, 1.0)
+    per_op = []
+    for i in range(4):
+        want = T.gemm_rows(x, T.synth_bf16(H * H, SEED, 101 + i, s), list(range(M)), H, H).reshape(-1)
+        got_b = d2h(dev, act[i + 1], M * H)
+        nw, ew = errs(T.bf16_to_f32(got_b), want)
+        per_op.append((nw, ew))
+        assert nw <= BF16_TOL, (i, nw)
+        x = rnd(want)  # the next op consumes the bf16-rounded oracle output
+    want = T.bf16_to_f32(T.bias_gelu(d2h(dev, act[4], M * H), T.synth_bf16(H, SEED, 110, 0.1), M, H))
+    nw, ew = errs(T.bf16_to_f32(d2h(dev, out, M * H)), want)
+    assert nw <= BF16_TOL
+    per_op.append((nw, ew))
+    record("config1_hp_chain_128x4096x4096x4", per_op_normwise=[p[0] for p in per_op],
+           per_op_elementwise=[p[1] for p in per_op], elements_checked=5 * M * H)
+    for p in per_op:
+        assert p[1] <= 0.1, per_op
+    dev.hp_unregister_chain(chain)
+    for p_ in act + ws + [bias, out]:
+        dev.free(p_)
+
+
+def test_config4_full_decode_step(dev, T):
+    """The full config-4 HP step (16 layers + 128,256-row LM head, bs=1 GEMV chain) with
+    Config4's geometry; the oracle restates every layer with bf16 rounding between ops and
+    checks all 128,256 logits."""
+    from paper_2601_04071_b200.live import Config4, decode_step_ops
+    M, H, Q, F, V, L = 1, Config4.H, Config4.Q, Config4.F, Config4.V, Config4.LAYERS
+    bufs = [dev.alloc(M * n * 2) for n in (H, Q, H, 2 * F, F, V)]
+    sc = lambda k: float(np.float32(1 / math.sqrt(k)))  # noqa: E731
+    ws, host_w = [], []
+    for l in range(L):
+        ptrs, hw = [], []
+        for j, (n, k) in enumerate([(Q, H), (H, H), (2 * F, H), (H, F)]):
+            p = dev.alloc(n * k * 2)
+            dev.fill_synth(p, n * k, SEED, 600 + 10 * l + j, sc(k))
+            ptrs.append(p)
+            hw.append(T.synth_bf16(n * k, SEED, 600 + 10 * l + j, sc(k)))
+        ws.append(ptrs)
+        host_w.append(hw)
+    lm = dev.alloc(V * H * 2)
+    dev.fill_synth(lm, V * H, SEED, 799, sc(H))
+    dev.fill_synth(bufs[0], M * H, SEED, 598, 1.0)
+    chain = dev.hp_register_chain(decode_step_ops(M, H, Q, F, V, L, bufs, ws, lm))
+    dev.hp_launch_direct(chain, dev.hp_next_seq())
+    dev.sync()
+    rows = [0]
+    h = T.synth_bf16(M * H, SEED, 598, 1.0)
+    for l in range(L):
+        wq, wo, wg, wd = host_w[l]
+        qkv = rnd(T.gemm_rows(h, wq, rows, Q, H).reshape(-1))
+        o = rnd(T.gemm_rows(np.ascontiguousarray(qkv[:H]), wo, rows, H, H).reshape(-1))
+        gu = T.gemm_rows(o, wg, rows, 2 * F, H)
+        g, u = gu[:, :F], gu[:, F:]
+        act = rnd((g / (1.0 + np.exp(-g)) * u).reshape(-1))
+        h = rnd(T.gemm_rows(act, wd, rows, H, F).reshape(-1))
+    want = T.gemm_rows(h, T.synth_bf16(V * H, SEED, 799, sc(H)), rows, V, H).reshape(-1)
+    got = T.bf16_to_f32(d2h(dev, bufs[5], V))
+    nw, ew = errs(got, want)
+    h_dev = T.bf16_to_f32(d2h(dev, bufs[0], H))
+    nh, eh = errs(h_dev, T.bf16_to_f32(h))
+    record("config4_decode_step_16L_V128256", logits_normwise=nw, logits_elementwise=ew, final_h_normwise=nh,
+           final_h_elementwise=eh, elements_checked=V + H)
+    assert nw <= BF16_TOL and nh <= BF16_TOL, (nw, nh)
+    assert ew <= 0.1
+    dev.hp_unregister_chain(chain)
+    for p_ in bufs + [p for l in ws for p in l] + [lm]:
+        dev.free(p_)
+
+
+def test_config4_axpy_2e30_bit_exact(dev, T):
+    """LP2 of config 4 at its real size: y <- a x + y over 2^30 bf16 elements (6 GiB of HBM
+    traffic), preempted twice mid-pass and resumed from its cursor, bit-exact vs the C
+    restatement (fmaf + RNE) on every element."""
+    n = 1 << 30
+    x, y = dev.alloc(2 * n), dev.alloc(2 * n)
+    dev.fill_synth(x, n, SEED, 21, 1.0)
+    dev.fill_synth(y, n, SEED, 22, 1.0)
+    k = dev.lp_register_axpy(x, y, n, 0.5, tile_elems=8192)
+    runs, begin = 0, 0
+    import time
+    while True:
+        dev.lp_run(k, begin, k.total_tiles)
+        runs += 1
+        if runs <= 2:
+            time.sleep(0.0003)
+            dev.preempt_raise()
+        st = dev.lp_wait(k, 60)
+        begin = st["cursor"]
+        if begin >= k.total_tiles and st["redo_count"] == 0:
+            break
+        assert runs < 100
+    got = d2h(dev, y, n)
+    want = T.axpy(T.synth_bf16(n, SEED, 22, 1.0), T.synth_bf16(n, SEED, 21, 1.0), 0.5)
+    mism = int(np.count_nonzero(got != want))
+    record("config4_axpy_2^30", elements_checked=n, mismatches=mism, runs=runs)
+    assert mism == 0
+    dev.lp_unregister(k)
+    dev.free(x)
+    dev.free(y)

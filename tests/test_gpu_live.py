@@ -141,3 +141,43 @@ def test_session_external_tenant():
     dev.d2h(want.ctypes.data, w.act[0], M * H * 2)
     assert np.array_equal(got, want)
     dev.close()
+
+
+def test_live_preemption_latency_targets():
+    """Regression guard on the north_star latency target (config 1, 1.5 s live window):
+    ring -> first HP CTA p99 <= 10 us over true preemptions (LP resident when HP turned
+    active, engine.hpp:954-960) and over all HP activations; the LP drain (flag -> last LP
+    CTA exit) stays within 2x of the target."""
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config1, live_run
+    dev = Device(0)
+    w = Config1(dev)
+    w.calibrate(reps=2)
+    sk = live_run(dev, w.scenario(seed=21, horizon_s=1.5), "splitkernel", w.binding(), w.options(timeline=False))
+    infl = sk["preempt_ring_to_first_hp_cta_lp_in_flight"]
+    idle = sk["preempt_ring_to_first_hp_cta_lp_idle"]
+    assert infl["n"] >= 10 and infl["n"] + idle["n"] == sk["preempt_ring_to_first_hp_cta"]["n"]
+    assert infl["p99_ns"] <= 10_000, infl
+    assert sk["preempt_ring_to_first_hp_cta"]["p99_ns"] <= 10_000
+    assert sk["preempt_flag_to_last_lp_exit"]["p99_ns"] <= 20_000
+    dev.close()
+
+
+def test_live_rejects_second_hp_task():
+    """One HP doorbell lane per device: a scenario with two HP tasks is refused (the replay
+    core runs it; the live runtime would let one task's ring release the other's gate)."""
+    import copy
+    import pytest as _pytest
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config1, live_run
+    dev = Device(0)
+    w = Config1(dev)
+    sc = copy.deepcopy(w.scenario(seed=3, horizon_s=0.1))
+    t2 = copy.deepcopy(sc["tasks"][0])
+    t2["name"] = "hp_infer_2"
+    sc["tasks"].append(t2)
+    b = w.binding()
+    b["hp"]["hp_infer_2"] = b["hp"]["hp_infer"]
+    with _pytest.raises(RuntimeError, match="rc=-2"):
+        live_run(dev, sc, "splitkernel", b, w.options())
+    dev.close()
