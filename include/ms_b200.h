@@ -67,10 +67,16 @@ int ms_memcpy_d2h(ms_dev* dev, void* dst, uint64_t src, size_t bytes);
 int ms_memset(ms_dev* dev, uint64_t dst, int value, size_t bytes);
 /* deterministic synthetic bf16 tensor (generator of oracle/tenant_ref.c) */
 int ms_fill_synth_bf16(ms_dev* dev, uint64_t dst, uint64_t n, uint64_t seed, uint64_t tensor, float scale);
+/* fp32 tensor holding the same synthetic values (widened from bf16): optimizer state */
+int ms_fill_synth_f32(ms_dev* dev, uint64_t dst, uint64_t n, uint64_t seed, uint64_t tensor, float scale);
 
 /* ---- LP (preemptible) kernels ------------------------------------------------------ */
 #define MS_LP_GEMM 1 /* C[m,n] = A[m,k] * B[n,k]^T, bf16 in/out, fp32 accumulate (tcgen05) */
 #define MS_LP_AXPY 2 /* y = alpha * x + y over n_elems bf16 (HBM streamer) */
+#define MS_LP_OPTIM 3 /* optimizer step over n_elems parameters (HBM streamer): a = fp32 params, b = fp32
+                         first moment, c = fp32 second moment (AdamW only), x = bf16 gradients;
+                         opt_mode 0 = AdamW, 1 = SGD momentum (opt[1] = momentum); tile_elems multiple
+                         of 1024 (default 4096) */
 
 typedef struct ms_lp_desc {
   int32_t kind;
@@ -87,6 +93,8 @@ typedef struct ms_lp_desc {
   float alpha;
   float pad2;
   int64_t n_elems;
+  int32_t opt_mode;   /* MS_LP_OPTIM: 0 = AdamW, 1 = SGD momentum */
+  float opt[7];       /* MS_LP_OPTIM: lr, beta1 (momentum), beta2, eps, weight decay, bias corrections c1, c2 */
 } ms_lp_desc;
 
 typedef struct ms_lp_status {
@@ -154,6 +162,24 @@ uint32_t ms_preempt_epoch(ms_dev* dev);
                                (m == 1: GEMV chain, k <= 4096) */
 #define MS_HP_H2D 3       /* copy m bytes: pinned host a -> device c (e2e request input) */
 #define MS_HP_D2H 4       /* copy m bytes: device a -> pinned host c (e2e request output) */
+/* Config-2 / config-3 tenants (ResNet-50 bs=1, BERT-base bs=1): per-op chain kernels,
+ * hp_ops.cuh.  Geometry in ms_hp_op.geo (NHWC, batch 1). */
+#define MS_HP_IM2COL 7    /* c[m x n] = conv patches of the NHWC input a [h*w x cin]: row = output pixel
+                             (oy * wo + ox, rows >= ho*wo zero), column = (ky, kx, ch) (cols >= kh*kw*cin
+                             zero); m, n padded to the GEMM tile (128, 64) */
+#define MS_HP_BIAS_ACT 8  /* c = act(a + bias[col] (+ b when b != 0)) over m x n; geo.flags bit 0 = ReLU */
+#define MS_HP_MAXPOOL 9   /* c[m x cin] = geo.kh x geo.kw / stride / pad max pooling of NHWC a [h*w x cin] */
+#define MS_HP_AVGPOOL 10  /* c[0, :] = mean of the h*w rows of a [h*w x n]; rows 1 .. m-1 of c = 0 */
+#define MS_HP_ATTN 11     /* c[m x n] = per head softmax(Q K^T / 8) V, a = [m x 3n] = [Q | K | V], head dim 64,
+                             m <= 256 and a multiple of 16 (no mask) */
+#define MS_HP_ADD_LN 12   /* c = LayerNorm(a + b) * gamma + beta over rows of n (eps 1e-12), bias = [gamma | beta] */
+
+typedef struct ms_hp_geo {
+  int32_t h, w, cin;      /* input spatial size and channels */
+  int32_t kh, kw;         /* window */
+  int32_t stride, pad;
+  int32_t flags;          /* MS_HP_BIAS_ACT: bit 0 = ReLU */
+} ms_hp_geo;
 
 typedef struct ms_hp_op {
   int32_t kind;
@@ -166,6 +192,7 @@ typedef struct ms_hp_op {
                         [K/64][N][64] */
   int64_t lda;       /* GEMM: row stride of a in elements (0: k) — e.g. a column slice of a wider
                         activation */
+  ms_hp_geo geo;     /* IM2COL / MAXPOOL / AVGPOOL geometry, BIAS_ACT flags (zero otherwise) */
 } ms_hp_op;
 
 typedef struct ms_hp_times {

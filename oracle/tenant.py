@@ -25,6 +25,13 @@ def lib():
         L.tr_axpy_bf16.argtypes = [P, P, F, S, S]
         L.tr_bias_gelu.argtypes = [P, P, P, I, I]
         L.tr_silu_mul.argtypes = [P, P, I, I]
+        L.tr_im2col.argtypes = [P, P, I, I, I, I, I, I, I, I, I]
+        L.tr_bias_act.argtypes = [P, P, P, P, I, I, I]
+        L.tr_maxpool.argtypes = [P, P, I, I, I, I, I, I, I]
+        L.tr_avgpool.argtypes = [P, P, I, I, I]
+        L.tr_attention.argtypes = [P, P, I, I]
+        L.tr_add_ln.argtypes = [P, P, P, P, I, I]
+        L.tr_optim.argtypes = [P, P, P, P, S, S, I, F, F, F, F, F, F, F]
         _lib = L
     return _lib
 
@@ -67,3 +74,53 @@ def silu_mul(x: np.ndarray, M: int, N: int) -> np.ndarray:
     out = np.empty(M * N, dtype=np.uint16)
     lib().tr_silu_mul(_p(x), _p(out), M, N)
     return out
+
+
+# ---- config-2 / config-3 glue ops (oracle/tenant_ref.c; device: hp_ops.cuh) -------------
+def im2col(x: np.ndarray, h: int, w: int, cin: int, kh: int, kw: int, stride: int, pad: int,
+           m_pad: int, n_pad: int) -> np.ndarray:
+    out = np.empty(m_pad * n_pad, dtype=np.uint16)
+    lib().tr_im2col(_p(np.ascontiguousarray(x)), _p(out), h, w, cin, kh, kw, stride, pad, m_pad, n_pad)
+    return out
+
+
+def bias_act(x: np.ndarray, bias: np.ndarray, resid, m: int, n: int, relu: bool) -> np.ndarray:
+    out = np.empty(m * n, dtype=np.uint16)
+    r = None if resid is None else np.ascontiguousarray(resid)
+    lib().tr_bias_act(_p(np.ascontiguousarray(x)), _p(bias), None if r is None else _p(r), _p(out), m, n, int(relu))
+    return out
+
+
+def maxpool(x: np.ndarray, h: int, w: int, c: int, k: int, stride: int, pad: int, m_pad: int) -> np.ndarray:
+    out = np.empty(m_pad * c, dtype=np.uint16)
+    lib().tr_maxpool(_p(np.ascontiguousarray(x)), _p(out), h, w, c, k, stride, pad, m_pad)
+    return out
+
+
+def avgpool(x: np.ndarray, rows: int, n: int, m_pad: int) -> np.ndarray:
+    out = np.empty(m_pad * n, dtype=np.uint16)
+    lib().tr_avgpool(_p(np.ascontiguousarray(x)), _p(out), rows, n, m_pad)
+    return out
+
+
+def attention(qkv: np.ndarray, s: int, d: int) -> np.ndarray:
+    out = np.empty(s * d, dtype=np.uint16)
+    lib().tr_attention(_p(np.ascontiguousarray(qkv)), _p(out), s, d)
+    return out
+
+
+def add_ln(x: np.ndarray, resid: np.ndarray, gb: np.ndarray, m: int, n: int) -> np.ndarray:
+    out = np.empty(m * n, dtype=np.uint16)
+    lib().tr_add_ln(_p(np.ascontiguousarray(x)), _p(np.ascontiguousarray(resid)), _p(gb), _p(out), m, n)
+    return out
+
+
+def synth_f32(n: int, seed: int, tensor: int, scale: float = 1.0) -> np.ndarray:
+    """fp32 tensor of the bf16 synthetic values (device: ms_fill_synth_f32)."""
+    return bf16_to_f32(synth_bf16(n, seed, tensor, scale)).copy()
+
+
+def optim(p, m, v, g, mode, lr, b1, b2, eps, wd, c1, c2, begin=0, end=None):
+    """In-place optimizer step over fp32 p / m / v (v ignored by SGD) and bf16 g."""
+    end = len(p) if end is None else end
+    lib().tr_optim(_p(p), _p(m), _p(v), _p(g), begin, end, mode, lr, b1, b2, eps, wd, c1, c2)

@@ -96,3 +96,141 @@ void tr_bias_gelu(const uint16_t* x, const uint16_t* bias, uint16_t* out, int M,
       out[(size_t)m * N + n] = f32_to_bf16(g);
     }
 }
+
+/* ---- config-2 / config-3 tenant glue ops (hp_ops.cuh), NHWC batch 1, fp32 math, RNE out ---- */
+
+/* conv patch matrix: out[m_pad x n_pad], row = output pixel oy*wo+ox, col = (ky*kw+kx)*cin+ch */
+void tr_im2col(const uint16_t* in, uint16_t* out, int h, int w, int cin, int kh, int kw, int stride, int pad,
+               int m_pad, int n_pad) {
+  const int ho = (h + 2 * pad - kh) / stride + 1, wo = (w + 2 * pad - kw) / stride + 1;
+  const int kvalid = kh * kw * cin;
+  for (int r = 0; r < m_pad; ++r)
+    for (int k = 0; k < n_pad; ++k) {
+      uint16_t v = 0;
+      if (r < ho * wo && k < kvalid) {
+        const int oy = r / wo, ox = r % wo, tap = k / cin, ch = k % cin;
+        const int iy = oy * stride - pad + tap / kw, ix = ox * stride - pad + tap % kw;
+        if (iy >= 0 && iy < h && ix >= 0 && ix < w) v = in[((size_t)iy * w + ix) * cin + ch];
+      }
+      out[(size_t)r * n_pad + k] = v;
+    }
+}
+
+/* out = act(x + bias[col] (+ resid)), relu when relu != 0; resid may be NULL */
+void tr_bias_act(const uint16_t* x, const uint16_t* bias, const uint16_t* resid, uint16_t* out, int m, int n,
+                 int relu) {
+  for (int r = 0; r < m; ++r)
+    for (int c = 0; c < n; ++c) {
+      const size_t i = (size_t)r * n + c;
+      float v = bf16_to_f32(x[i]) + bf16_to_f32(bias[c]);
+      if (resid) v = v + bf16_to_f32(resid[i]);
+      if (relu && v < 0.0f) v = 0.0f;
+      out[i] = f32_to_bf16(v);
+    }
+}
+
+void tr_maxpool(const uint16_t* in, uint16_t* out, int h, int w, int c, int k, int stride, int pad, int m_pad) {
+  const int ho = (h + 2 * pad - k) / stride + 1, wo = (w + 2 * pad - k) / stride + 1;
+  for (int r = 0; r < m_pad; ++r)
+    for (int ch = 0; ch < c; ++ch) {
+      float mx = -INFINITY;
+      if (r < ho * wo) {
+        const int oy = r / wo, ox = r % wo;
+        for (int ky = 0; ky < k; ++ky)
+          for (int kx = 0; kx < k; ++kx) {
+            const int iy = oy * stride - pad + ky, ix = ox * stride - pad + kx;
+            if (iy < 0 || iy >= h || ix < 0 || ix >= w) continue;
+            const float v = bf16_to_f32(in[((size_t)iy * w + ix) * c + ch]);
+            if (v > mx) mx = v;
+          }
+      } else {
+        mx = 0.0f;
+      }
+      out[(size_t)r * c + ch] = f32_to_bf16(mx);
+    }
+}
+
+/* out[0, :] = mean over rows of in [rows x n] (fp32 sum in row order); rows 1..m_pad-1 = 0 */
+void tr_avgpool(const uint16_t* in, uint16_t* out, int rows, int n, int m_pad) {
+  for (int c = 0; c < n; ++c) {
+    float s = 0.0f;
+    for (int q = 0; q < rows; ++q) s += bf16_to_f32(in[(size_t)q * n + c]);
+    out[c] = f32_to_bf16(s * (1.0f / (float)rows));
+  }
+  for (size_t i = (size_t)n; i < (size_t)m_pad * n; ++i) out[i] = 0;
+}
+
+/* ctx[s x d] = per head softmax(Q K^T / 8) V; qkv = [s x 3d] = [Q | K | V], head dim 64;
+   fp64 math (the device uses fp32 + __expf: agreement within the bf16 tolerance) */
+void tr_attention(const uint16_t* qkv, uint16_t* ctx, int s, int d) {
+  const int heads = d / 64;
+  const size_t ld = (size_t)3 * d;
+#pragma omp parallel for schedule(static)
+  for (int hq = 0; hq < heads * s; ++hq) {
+    const int hd = hq / s, q = hq % s;
+    double p[1024];
+    double mx = -1e300, sum = 0.0;
+    for (int j = 0; j < s; ++j) {
+      double acc = 0.0;
+      for (int e = 0; e < 64; ++e)
+        acc += (double)bf16_to_f32(qkv[q * ld + hd * 64 + e]) * (double)bf16_to_f32(qkv[j * ld + d + hd * 64 + e]);
+      p[j] = acc * 0.125;
+      if (p[j] > mx) mx = p[j];
+    }
+    for (int j = 0; j < s; ++j) {
+      p[j] = exp(p[j] - mx);
+      sum += p[j];
+    }
+    for (int e = 0; e < 64; ++e) {
+      double acc = 0.0;
+      for (int j = 0; j < s; ++j) acc += p[j] * (double)bf16_to_f32(qkv[j * ld + 2 * d + hd * 64 + e]);
+      ctx[(size_t)q * d + hd * 64 + e] = f32_to_bf16((float)(acc / sum));
+    }
+  }
+}
+
+/* out = LayerNorm(x + resid) * gamma + beta over rows of n, eps 1e-12 (gb = [gamma | beta]) */
+void tr_add_ln(const uint16_t* x, const uint16_t* resid, const uint16_t* gb, uint16_t* out, int m, int n) {
+  for (int r = 0; r < m; ++r) {
+    double mean = 0.0, var = 0.0;
+    for (int c = 0; c < n; ++c)
+      mean += (double)(bf16_to_f32(x[(size_t)r * n + c]) + bf16_to_f32(resid[(size_t)r * n + c]));
+    mean /= n;
+    for (int c = 0; c < n; ++c) {
+      const double v = (double)(bf16_to_f32(x[(size_t)r * n + c]) + bf16_to_f32(resid[(size_t)r * n + c])) - mean;
+      var += v * v;
+    }
+    const double rstd = 1.0 / sqrt(var / n + 1e-12);
+    for (int c = 0; c < n; ++c) {
+      const double v = (double)(bf16_to_f32(x[(size_t)r * n + c]) + bf16_to_f32(resid[(size_t)r * n + c]));
+      out[(size_t)r * n + c] =
+          f32_to_bf16((float)((v - mean) * rstd * bf16_to_f32(gb[c]) + bf16_to_f32(gb[n + c])));
+    }
+  }
+}
+
+/* Optimizer streamers (LP, config 2/3 training steps), element-wise over [begin, end):
+   mode 0 = AdamW (fp32 p, m, v; bf16 g): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+            p -= lr * (m * c1 / (sqrt(v * c2) + eps) + wd * p)   (c1, c2 = bias corrections)
+   mode 1 = SGD momentum: m = mu m + g; p -= lr * (m + wd * p)   (v unused)
+   Float math in this exact order (the device kernel uses the same operations, no FMA
+   contraction: bit-exact). */
+void tr_optim(float* p, float* m, float* v, const uint16_t* g, size_t begin, size_t end, int mode, float lr,
+              float b1, float b2, float eps, float wd, float c1, float c2) {
+#pragma omp parallel for schedule(static)
+  for (size_t i = begin; i < end; ++i) {
+    const float gi = bf16_to_f32(g[i]);
+    if (mode == 0) {
+      const float mi = b1 * m[i] + (1.0f - b1) * gi;
+      const float vi = b2 * v[i] + (1.0f - b2) * (gi * gi);
+      const float upd = (mi * c1) / (sqrtf(vi * c2) + eps) + wd * p[i];
+      m[i] = mi;
+      v[i] = vi;
+      p[i] = p[i] - lr * upd;
+    } else {
+      const float mi = b1 * m[i] + gi;
+      m[i] = mi;
+      p[i] = p[i] - lr * (mi + wd * p[i]);
+    }
+  }
+}

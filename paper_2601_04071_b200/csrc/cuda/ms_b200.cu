@@ -23,6 +23,8 @@
 #include "hp_fused.cuh"
 #include "hp_gemv.cuh"
 #include "tc_gemm2.cuh"
+#include "hp_ops.cuh"
+#include "lp_optim.cuh"
 
 using namespace msdev;
 
@@ -107,6 +109,7 @@ int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint6
 }
 
 constexpr int kRedoCap = 8192;
+constexpr int kMaxChainOps = 512;  // per-op chains (config-2 ResNet-50: ~160 ops); fused / GEMV plans are shorter
 
 // FFI callers may pass any id: every entry point that indexes a slot checks it first.
 #define MS_CHECK_LP(d, id) \
@@ -226,6 +229,7 @@ int set_smem_attrs() {
   MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                FusedCfg<1, 32>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
@@ -297,6 +301,95 @@ int launch_gemm(ms_dev* d, int block_n, const CUtensorMap& ta, const CUtensorMap
 }
 
 bool is_copy(const ms_hp_op& op) { return op.kind == MS_HP_H2D || op.kind == MS_HP_D2H; }
+// Config-2/3 glue ops (hp_ops.cuh): per-op kernels only (never fused / GEMV-planned).
+bool is_glue(int kind) {
+  return kind == MS_HP_IM2COL || kind == MS_HP_BIAS_ACT || kind == MS_HP_MAXPOOL || kind == MS_HP_AVGPOOL ||
+         kind == MS_HP_ATTN || kind == MS_HP_ADD_LN;
+}
+
+int launch_glue(ms_dev* d, const HpOpRt& o, const TileRun& r, bool pdl) {
+  HpOpParams q{};
+  q.run = r;
+  q.a = reinterpret_cast<const __nv_bfloat16*>(o.op.a);
+  q.b = reinterpret_cast<const __nv_bfloat16*>(o.op.b);
+  q.bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
+  q.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+  q.m = static_cast<int>(o.op.m);
+  q.n = static_cast<int>(o.op.n);
+  const ms_hp_geo& g = o.op.geo;
+  q.h = g.h;
+  q.w = g.w;
+  q.cin = g.cin;
+  q.kh = g.kh;
+  q.kw = g.kw;
+  q.stride = g.stride;
+  q.pad = g.pad;
+  q.flags = g.flags;
+  if (g.stride > 0) {
+    q.ho = (g.h + 2 * g.pad - g.kh) / g.stride + 1;
+    q.wo = (g.w + 2 * g.pad - g.kw) / g.stride + 1;
+  }
+  const int sms = d->prop.multiProcessorCount;
+  auto grid_for = [&](long long vecs) {
+    return static_cast<int>(std::max<long long>(1, std::min<long long>((vecs + kHpOpThreads - 1) / kHpOpThreads, 4ll * sms)));
+  };
+  switch (o.op.kind) {
+    case MS_HP_IM2COL:
+      MS_CUDA(launch_k(im2col_kernel, grid_for(o.op.m * (o.op.n / 8)), kHpOpThreads, 0, d->hp, pdl, q));
+      break;
+    case MS_HP_BIAS_ACT:
+      MS_CUDA(launch_k(bias_act_kernel, grid_for(o.op.m * (o.op.n / 8)), kHpOpThreads, 0, d->hp, pdl, q));
+      break;
+    case MS_HP_MAXPOOL:
+      MS_CUDA(launch_k(maxpool_kernel, grid_for(o.op.m * (g.cin / 8)), kHpOpThreads, 0, d->hp, pdl, q));
+      break;
+    case MS_HP_AVGPOOL:
+      MS_CUDA(launch_k(avgpool_kernel, grid_for(o.op.m * (o.op.n / 8)), kHpOpThreads, 0, d->hp, pdl, q));
+      break;
+    case MS_HP_ATTN:
+      MS_CUDA(launch_k(attn_kernel, static_cast<int>((o.op.n / 64) * (o.op.m / 16)), 128, kAttnSmemBytes, d->hp, pdl, q));
+      break;
+    case MS_HP_ADD_LN:
+      MS_CUDA(launch_k(add_ln_kernel, static_cast<int>(std::min<int64_t>(o.op.m, sms)), kHpOpThreads, 0, d->hp, pdl, q));
+      break;
+    default:
+      return fail(MS_E_ARG, "not a glue op");
+  }
+  return 0;
+}
+
+// Registration checks of a glue op (shapes the kernels above assume).
+int check_glue(const ms_hp_op& op) {
+  const ms_hp_geo& g = op.geo;
+  if (op.m <= 0 || op.n <= 0 || op.n % 8 || !op.a || !op.c) return fail(MS_E_ARG, "glue op: m, n > 0, n % 8 == 0, a, c");
+  if ((op.a | op.b | op.c | op.bias) % 16) return fail(MS_E_ARG, "glue op operands must be 16-byte aligned");
+  switch (op.kind) {
+    case MS_HP_IM2COL:
+    case MS_HP_MAXPOOL: {
+      if (g.h <= 0 || g.w <= 0 || g.cin <= 0 || g.kh <= 0 || g.kw <= 0 || g.stride <= 0 || g.pad < 0)
+        return fail(MS_E_ARG, "im2col / maxpool geometry");
+      const int64_t ho = (g.h + 2 * g.pad - g.kh) / g.stride + 1, wo = (g.w + 2 * g.pad - g.kw) / g.stride + 1;
+      if (op.m < ho * wo) return fail(MS_E_ARG, "im2col / maxpool: m < output pixels");
+      if (op.kind == MS_HP_IM2COL && op.n < static_cast<int64_t>(g.kh) * g.kw * g.cin)
+        return fail(MS_E_ARG, "im2col: n < kh * kw * cin");
+      if (op.kind == MS_HP_MAXPOOL && (g.cin % 8 || op.n != g.cin)) return fail(MS_E_ARG, "maxpool: n == cin, cin % 8 == 0");
+      return 0;
+    }
+    case MS_HP_BIAS_ACT:
+      if (!op.bias) return fail(MS_E_ARG, "bias_act needs a bias");
+      return 0;
+    case MS_HP_AVGPOOL:
+      if (g.h <= 0 || g.w <= 0) return fail(MS_E_ARG, "avgpool: h, w");
+      return 0;
+    case MS_HP_ATTN:
+      if (op.n % 64 || op.m % 16 || op.m > kAttnMaxS) return fail(MS_E_ARG, "attn: n % 64 == 0, m % 16 == 0, m <= 256");
+      return 0;
+    case MS_HP_ADD_LN:
+      if (!op.b || !op.bias || op.n > 8 * kHpOpThreads) return fail(MS_E_ARG, "add_ln: b, bias, n <= 2048");
+      return 0;
+  }
+  return fail(MS_E_ARG, "not a glue op");
+}
 
 int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq, bool after_gate) {
   const HpOpRt& o = ch.ops[i];
@@ -324,6 +417,7 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   // the chain's first kernel does not depend on the gate's output, later ones wait.
   const bool prev_is_kernel = i > 0 ? !is_copy(ch.ops[i - 1].op) : after_gate;
   r.pdl_wait = i > 0 && prev_is_kernel;
+  if (is_glue(o.op.kind)) return launch_glue(d, o, r, prev_is_kernel);
   if (o.op.kind == MS_HP_GEMM_SWIGLU) {
     // GEMM into tmp ([gate | up] halves), then the SwiGLU kernel (PDL) writes c.
     const bool last = r.hp_last;
@@ -433,6 +527,8 @@ int plan_fused(ms_dev* d, HpChain& ch) {
   for (int i = first; i <= last; ++i) {
     const ms_hp_op& op = ch.ops[i].op;
     if (is_copy(op)) return 0;  // copies between kernels: keep per-op launches
+    if (is_glue(op.kind)) return 0;
+    if (last - first + 1 > kFusedMaxOps) return 0;
     if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % 32 || op.k % kBK)) return 0;
     if (op.kind == MS_HP_GEMM && op.n % kFusedBN && !(op.m == kBM && d->hp_fused == 1)) return 0;
     if (op.kind == MS_HP_GEMM_SWIGLU && (op.m % kBM || op.n % 64 || op.k % kBK)) return 0;
@@ -943,6 +1039,13 @@ int ms_memset(ms_dev* d, uint64_t dst, int value, size_t bytes) {
   MS_CUDA(cudaStreamSynchronize(d->aux));
   return 0;
 }
+int ms_fill_synth_f32(ms_dev* d, uint64_t dst, uint64_t n, uint64_t seed, uint64_t tensor, float scale) {
+  synth_fill_f32_kernel<<<d->prop.multiProcessorCount * 8, 256, 0, d->aux>>>(reinterpret_cast<float*>(dst), n, seed,
+                                                                             tensor, scale);
+  MS_CUDA(cudaGetLastError());
+  MS_CUDA(cudaStreamSynchronize(d->aux));
+  return 0;
+}
 int ms_fill_synth_bf16(ms_dev* d, uint64_t dst, uint64_t n, uint64_t seed, uint64_t tensor, float scale) {
   synth_fill_kernel<<<d->prop.multiProcessorCount * 8, 256, 0, d->aux>>>(reinterpret_cast<__nv_bfloat16*>(dst), n,
                                                                          seed, tensor, scale);
@@ -991,6 +1094,15 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     if (s.desc.tile_elems % (kStreamThreads * 8) || s.desc.tile_elems > kStreamThreads * 8 * 8)
       return fail(MS_E_ARG, "tile_elems must be a multiple of 2048 and <= 16384");
     if (desc->n_elems % 8) return fail(MS_E_ARG, "n_elems must be a multiple of 8");
+    s.total_tiles = (static_cast<uint64_t>(desc->n_elems) + s.desc.tile_elems - 1) / s.desc.tile_elems;
+  } else if (desc->kind == MS_LP_OPTIM) {
+    s.desc.tile_elems = desc->tile_elems ? desc->tile_elems : 4096;
+    if (s.desc.tile_elems % (kStreamThreads * 4) || s.desc.tile_elems > kStreamThreads * 4 * 8)
+      return fail(MS_E_ARG, "optimizer tile_elems must be a multiple of 1024 and <= 8192");
+    if (desc->n_elems % 4 || desc->n_elems <= 0) return fail(MS_E_ARG, "n_elems must be a positive multiple of 4");
+    if (desc->opt_mode != 0 && desc->opt_mode != 1) return fail(MS_E_ARG, "opt_mode must be 0 (AdamW) or 1 (SGD)");
+    if (!desc->a || !desc->b || !desc->x || (desc->opt_mode == 0 && !desc->c)) return fail(MS_E_ARG, "optimizer buffers");
+    if ((desc->a | desc->b | desc->c) % 16 || desc->x % 8) return fail(MS_E_ARG, "optimizer buffers must be aligned");
     s.total_tiles = (static_cast<uint64_t>(desc->n_elems) + s.desc.tile_elems - 1) / s.desc.tile_elems;
   } else {
     return fail(MS_E_ARG, "unknown LP kernel kind");
@@ -1131,6 +1243,36 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
       return 0;
     }
     return launch_gemm(d, s.desc.block_n, s.tma_a, s.tma_b, s.tma_c, p, grid, d->lp);
+  }
+  if (s.desc.kind == MS_LP_OPTIM) {
+    OptimParams q{};
+    q.run = r;
+    q.p = reinterpret_cast<float*>(s.desc.a);
+    q.m = reinterpret_cast<float*>(s.desc.b);
+    q.v = reinterpret_cast<float*>(s.desc.c);
+    q.g = reinterpret_cast<const __nv_bfloat16*>(s.desc.x);
+    q.n = static_cast<unsigned long long>(s.desc.n_elems);
+    q.tile_elems = s.desc.tile_elems;
+    q.mode = s.desc.opt_mode;
+    q.lr = s.desc.opt[0];
+    q.b1 = s.desc.opt[1];
+    q.b2 = s.desc.opt[2];
+    q.eps = s.desc.opt[3];
+    q.wd = s.desc.opt[4];
+    q.c1 = s.desc.opt[5];
+    q.c2 = s.desc.opt[6];
+    const uint64_t cap = static_cast<uint64_t>(std::max(1, d->prop.multiProcessorCount - d->lp_sm_reserve));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((work + kAxpyGroups - 1) / kAxpyGroups, cap)));
+    const int threads = kAxpyGroups * kStreamThreads + 64;
+    switch (s.desc.tile_elems / (kStreamThreads * 4)) {
+      case 1: optim_kernel<1><<<grid, threads, 0, d->lp>>>(q); break;
+      case 2: optim_kernel<2><<<grid, threads, 0, d->lp>>>(q); break;
+      case 4: optim_kernel<4><<<grid, threads, 0, d->lp>>>(q); break;
+      case 8: optim_kernel<8><<<grid, threads, 0, d->lp>>>(q); break;
+      default: return fail(MS_E_ARG, "optimizer tile_elems must be 1024 * {1,2,4,8}");
+    }
+    MS_CUDA(cudaGetLastError());
+    return 0;
   }
   StreamParams p{};
   p.run = r;
@@ -1293,7 +1435,7 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       cid = i;
       break;
     }
-  if (cid < 0 || n_ops < 1 || n_ops > kFusedMaxOps) return fail(MS_E_ARG, "bad HP chain");
+  if (cid < 0 || n_ops < 1 || n_ops > kMaxChainOps) return fail(MS_E_ARG, "bad HP chain");
   // Batch-1 (m == 1) GEMM ops run as one HBM-streaming GEMV chain; they cannot share a
   // chain with tcgen05 (m >= 128) GEMMs.  Checked before anything is allocated.
   bool any_gemv = false, any_mat = false;
@@ -1303,9 +1445,12 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
     any_mat |= mm && ops[i].m != 1;
   }
   if (any_gemv && any_mat) return fail(MS_E_ARG, "an HP chain cannot mix m == 1 and m >= 128 GEMM ops");
-  for (int i = 0; i < n_ops && any_gemv; ++i)
+  for (int i = 0; i < n_ops && any_gemv; ++i) {
     if ((ops[i].kind == MS_HP_BIAS_GELU || ops[i].kind == MS_HP_SILU_MUL) && ops[i].m != 1)
       return fail(MS_E_ARG, "batch-1 chain: elementwise ops must have m == 1");
+    if (is_glue(ops[i].kind)) return fail(MS_E_ARG, "batch-1 chain: conv / attention glue ops need m >= 16 rows");
+  }
+  if (any_gemv && n_ops > kGemvMaxOps) return fail(MS_E_ARG, "batch-1 chain too long");
   HpChain ch;
   for (int i = 0; i < n_ops; ++i) {
     HpOpRt o;
@@ -1384,6 +1529,8 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       if (o.op.n % 8) return fail(MS_E_ARG, "elementwise cols must be a multiple of 8");
     } else if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
       if (o.op.m <= 0) return fail(MS_E_ARG, "copy size must be > 0");
+    } else if (is_glue(o.op.kind)) {
+      if (int rc = check_glue(o.op)) return rc;
     } else {
       return fail(MS_E_ARG, "unknown HP op");
     }
@@ -1448,7 +1595,11 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
     const char* e = std::getenv("MS_GATE_SMEM");
     return e ? std::max(0, std::min(atoi(e), kGateSmem)) : kGateSmem;
   }();
-  if (ch.lead_copies > 0) {
+  const bool overlap = ch.lead_copies > 0 && [] {
+    const char* e = std::getenv("MS_E2E_OVERLAP");  // A/B: 0 = copy queued behind the HP gate
+    return !e || atoi(e) != 0;
+  }();
+  if (overlap) {
     // e2e input: its own gate on the copy stream, so the H2D starts at the ring (no SM
     // work needed, it overlaps the LP drain); the chain waits for the copy's event.
     gate_kernel<<<1, 32, gate_smem, d->hpcopy>>>(&d->page_d->doorbell, seq, nullptr, nullptr);  // (smem: stays off LP SMs)
@@ -1462,7 +1613,7 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   }
   gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
-  if (ch.lead_copies > 0) {
+  if (overlap) {
     MS_CUDA(cudaStreamWaitEvent(d->hp, ch.in_ev, 0));
     return launch_chain(d, cid, ch, seq, false, static_cast<size_t>(ch.lead_copies));
   }

@@ -15,7 +15,7 @@
 #pragma once
 #include <stdint.h>
 
-#define MS_MAX_LP 16
+#define MS_MAX_LP 96  /* config-2 LP: the ~63 distinct GEMM shapes of a ResNet-50 training step */
 #define MS_MAX_HP_CHAINS 64
 #define MS_N_CTL (MS_MAX_LP + 8192)  // control blocks: LP slots, then HP chain kernels
 #define MS_MIRROR_COPIES 8

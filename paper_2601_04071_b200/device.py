@@ -11,8 +11,10 @@ from dataclasses import dataclass
 
 from . import _native
 
-MS_LP_GEMM, MS_LP_AXPY = 1, 2
+MS_LP_GEMM, MS_LP_AXPY, MS_LP_OPTIM = 1, 2, 3
 MS_HP_GEMM, MS_HP_BIAS_GELU, MS_HP_H2D, MS_HP_D2H = 1, 2, 3, 4
+MS_HP_SILU_MUL, MS_HP_GEMM_SWIGLU = 5, 6
+MS_HP_IM2COL, MS_HP_BIAS_ACT, MS_HP_MAXPOOL, MS_HP_AVGPOOL, MS_HP_ATTN, MS_HP_ADD_LN = 7, 8, 9, 10, 11, 12
 
 
 class DeviceError(RuntimeError):
@@ -31,7 +33,7 @@ class LpDesc(C.Structure):
                 ("a", C.c_uint64), ("b", C.c_uint64), ("c", C.c_uint64),
                 ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
                 ("x", C.c_uint64), ("y", C.c_uint64), ("alpha", C.c_float), ("pad2", C.c_float),
-                ("n_elems", C.c_int64)]
+                ("n_elems", C.c_int64), ("opt_mode", C.c_int32), ("opt", C.c_float * 7)]
 
 
 class LpStatus(C.Structure):
@@ -45,10 +47,25 @@ class LpStatus(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class HpGeo(C.Structure):
+    _fields_ = [("h", C.c_int32), ("w", C.c_int32), ("cin", C.c_int32), ("kh", C.c_int32), ("kw", C.c_int32),
+                ("stride", C.c_int32), ("pad", C.c_int32), ("flags", C.c_int32)]
+
+
 class HpOp(C.Structure):
     _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("a", C.c_uint64), ("b", C.c_uint64),
                 ("c", C.c_uint64), ("bias", C.c_uint64), ("m", C.c_int64), ("n", C.c_int64),
-                ("k", C.c_int64), ("split_k", C.c_int32), ("b_layout", C.c_int32), ("lda", C.c_int64)]
+                ("k", C.c_int64), ("split_k", C.c_int32), ("b_layout", C.c_int32), ("lda", C.c_int64),
+                ("geo", HpGeo)]
+
+    @classmethod
+    def from_dict(cls, o: dict) -> "HpOp":
+        o = dict(o)
+        geo = o.pop("geo", None)
+        op = cls(**o)
+        if geo:
+            op.geo = HpGeo(**geo)
+        return op
 
 
 class HpTimes(C.Structure):
@@ -77,6 +94,7 @@ def lib() -> C.CDLL:
             "ms_memcpy_h2d": (I, [P, U64, P, C.c_size_t]), "ms_memcpy_d2h": (I, [P, P, U64, C.c_size_t]),
             "ms_memset": (I, [P, U64, I, C.c_size_t]),
             "ms_fill_synth_bf16": (I, [P, U64, U64, U64, U64, F]),
+            "ms_fill_synth_f32": (I, [P, U64, U64, U64, U64, F]),
             "ms_lp_register": (I, [P, C.POINTER(LpDesc), C.POINTER(I), C.POINTER(U64)]),
             "ms_lp_run": (I, [P, I, U64, U64, U64]), "ms_lp_set_budget": (I, [P, I, U64]),
             "ms_lp_set_slow_tiles": (I, [P, I, C.c_char_p, U64, I, I]),
@@ -174,6 +192,9 @@ class Device:
     def fill_synth(self, dst: int, n: int, seed: int, tensor: int, scale: float = 1.0):
         _ck(lib().ms_fill_synth_bf16(self._h, dst, n, seed, tensor, scale))
 
+    def fill_synth_f32(self, dst: int, n: int, seed: int, tensor: int, scale: float = 1.0):
+        _ck(lib().ms_fill_synth_f32(self._h, dst, n, seed, tensor, scale))
+
     def sync(self):
         _ck(lib().ms_dev_sync(self._h))
 
@@ -187,6 +208,17 @@ class Device:
                          ctas_per_sm: int = 1) -> LpKernel:
         d = LpDesc(kind=MS_LP_AXPY, tile_elems=tile_elems, ctas_per_sm=ctas_per_sm, x=x, y=y,
                    alpha=alpha, n_elems=n_elems)
+        return self._lp_register(d)
+
+    def lp_register_optim(self, params: int, m1: int, m2: int, grads: int, n_elems: int, mode: int = 0,
+                          lr: float = 1e-4, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                          wd: float = 0.01, c1: float = 1.0, c2: float = 1.0, tile_elems: int = 4096) -> LpKernel:
+        """Optimizer step streamer (MS_LP_OPTIM): mode 0 AdamW over fp32 params / moments and
+        bf16 grads, mode 1 SGD momentum (beta1 = momentum, m2 unused)."""
+        d = LpDesc(kind=MS_LP_OPTIM, tile_elems=tile_elems, a=params, b=m1, c=m2, x=grads, n_elems=n_elems,
+                   opt_mode=mode)
+        for i, v in enumerate((lr, beta1, beta2, eps, wd, c1, c2)):
+            d.opt[i] = v
         return self._lp_register(d)
 
     def _lp_register(self, d: LpDesc) -> LpKernel:
@@ -273,7 +305,7 @@ class Device:
 
     # ---- HP
     def hp_register_chain(self, ops: list[dict]) -> int:
-        arr = (HpOp * len(ops))(*[HpOp(**o) for o in ops])
+        arr = (HpOp * len(ops))(*[HpOp.from_dict(o) for o in ops])
         cid = C.c_int()
         _ck(lib().ms_hp_register_chain(self._h, arr, len(ops), C.byref(cid)))
         return cid.value

@@ -234,3 +234,80 @@ class Config4:
                          "lp_axpy_1g": c.get("lp_ew_tile_ns", 4000)}, "timeline": True}
         o.update(kw)
         return o
+
+
+class _TrainInferConfig:
+    """Shared shape of configs 2 and 3: one HP inference tenant (a per-op chain of one
+    request, 1 iteration, Poisson arrivals) + one LP training-step tenant (TrainStepLP)."""
+
+    HP_TASK = LP_TASK = NAME = ""
+    RATE = 100.0
+    THRESHOLD_MS = 0.5  # large-bubble threshold (scheduler.threshold_ms): the gaps are a few ms
+
+    def _finish(self, dev: Device, hp, lp):
+        self.dev, self.hp, self.lp = dev, hp, lp
+        self.chain = dev.hp_register_chain(hp.ops)
+        self.calib = None
+
+    def calibrate(self, reps: int = 2) -> dict:
+        c = self.lp.calibrate(reps)
+        time.sleep(0.2)
+        ms_chain = min(self.dev.hp_time_chain(self.chain, 10) for _ in range(3))
+        self.calib = dict(c, hp_chain_ms=ms_chain, hp_gemm_tflops=self.hp.gemm_flops / (ms_chain * 1e-3) / 1e12,
+                          hp_ops=len(self.hp.ops), lp_tile_ns=dict(self.lp.tile_ns))
+        return self.calib
+
+    def hp_rate(self, max_util: float = 0.8) -> float:
+        """The config's request rate, capped so HP alone stays <= max_util."""
+        ms = (self.calib or {}).get("hp_chain_ms", 1.0)
+        return min(self.RATE, max_util / (ms * 1e-3))
+
+    def scenario(self, seed: int, horizon_s: float, rate: float | None = None) -> dict:
+        c = self.calib or {}
+        return scenarios.train_infer(self.NAME, seed=seed, horizon_s=horizon_s, hp_task=self.HP_TASK,
+                                     hp_ops=len(self.hp.ops), hp_chain_ns=int(c.get("hp_chain_ms", 1.0) * 1e6),
+                                     lp_task=self.LP_TASK, lp_specs=self.lp.kernel_specs(),
+                                     lp_sequence=self.lp.sequence, rate=rate or self.hp_rate(),
+                                     threshold_ms=self.THRESHOLD_MS)
+
+    def binding(self) -> dict:
+        return {"lp": self.lp.binding(), "hp": {self.HP_TASK: [self.chain]}}
+
+    def options(self, **kw) -> dict:
+        o = {"tile_ns": dict(self.lp.tile_ns), "timeline": True}
+        o.update(kw)
+        return o
+
+    def close(self):
+        self.dev.hp_unregister_chain(self.chain)
+        self.hp.free()
+        self.lp.free()
+
+
+class Config2(_TrainInferConfig):
+    """Config 2 (BASELINE configs[1]): HP ResNet-50 bs=1 inference (~160-op chain: im2col +
+    tcgen05 conv GEMMs + folded-BN/ReLU/residual + pools + FC) at 200 req/s, LP ResNet-50
+    training step at bs=64 (48 distinct conv/FC GEMM shapes fwd/dgrad/wgrad + SGD)."""
+
+    HP_TASK, LP_TASK, NAME, RATE = "hp_resnet50", "lp_resnet50_train", "cfg2_resnet50", 200.0
+
+    def __init__(self, dev: Device, seed: int = SEED):
+        from .tenants import RESNET50_PARAMS, ResNet50HP, TrainStepLP, resnet50_train_gemms
+        hp = ResNet50HP(dev, seed)
+        lp = TrainStepLP(dev, "rn50", resnet50_train_gemms(64), RESNET50_PARAMS, optim_mode=1, seed=seed,
+                         tensor_base=2900)
+        self._finish(dev, hp, lp)
+
+
+class Config3(_TrainInferConfig):
+    """Config 3 (BASELINE configs[2]): HP BERT-base bs=1 seq-128 encoder (96-op chain) at
+    100 req/s, LP BERT-base training step at bs=32 (9 distinct GEMM shapes x 144 GEMMs +
+    AdamW over 110 M parameters)."""
+
+    HP_TASK, LP_TASK, NAME, RATE = "hp_bert", "lp_bert_train", "cfg3_bert_base", 100.0
+
+    def __init__(self, dev: Device, seed: int = SEED):
+        from .tenants import BERT_PARAMS, BertHP, TrainStepLP, bert_train_gemms
+        hp = BertHP(dev, seed)
+        lp = TrainStepLP(dev, "bert", bert_train_gemms(32), BERT_PARAMS, optim_mode=0, seed=seed, tensor_base=3900)
+        self._finish(dev, hp, lp)

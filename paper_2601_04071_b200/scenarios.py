@@ -145,3 +145,31 @@ def dumps(sc: dict) -> str:
 
 def save(sc: dict, path: str | Path) -> None:
     Path(path).write_text(json.dumps(sc, indent=2, sort_keys=True) + "\n")
+
+
+def train_infer(name: str, seed: int, horizon_s: float, hp_task: str, hp_ops: int, hp_chain_ns: int, lp_task: str,
+                lp_specs: list, lp_sequence: list, rate: float, threshold_ms: float = 0.5,
+                calib: dict | None = None) -> dict:
+    """Configs 2 / 3 (ResNet-50, BERT-base): one HP serving task whose request is ONE
+    iteration of `hp_ops` chain kernels (point block time = measured chain time / ops, one
+    wave each), Poisson arrivals at `rate`; one LP batch task whose kernel sequence is the
+    training step (lp_sequence = [(kernel, repeat)], specs from TrainStepLP.kernel_specs)."""
+    c = dict(DEFAULT_CALIB, **(calib or {}))
+    op_ns = max(1000, hp_chain_ns // max(1, hp_ops))
+    hp_kernel = _kernel(f"{hp_task}_op", N_SM, op_ns, 1 << 20, False)
+    return {
+        "name": name,
+        "seed": seed,
+        "horizon": _dur(int(horizon_s * 1e9)),
+        "gpu": gpu_b200(c),
+        "scheduler": {"threshold_ms": threshold_ms},
+        "kernels": [hp_kernel] + list(lp_specs),
+        "tasks": [
+            {"name": hp_task, "priority": "high", "kind": "serving", "trace": "hp_trace",
+             "kernels": [{"kernel": f"{hp_task}_op", "repeat": int(hp_ops)}], "bubble_hints": []},
+            {"name": lp_task, "priority": "low", "kind": "batch",
+             "kernels": [{"kernel": k, "repeat": int(r)} for k, r in lp_sequence]},
+        ],
+        "traces": [{"name": "hp_trace", "bursty": {"rate": rate, "burstiness": 1.0},
+                    "iterations": {"dist": "point", "value": 1}}],
+    }

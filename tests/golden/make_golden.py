@@ -97,6 +97,15 @@ def digests() -> dict:
         cases[f"mem{seed}"] = random_memory_scenario(2000 + seed)
     for ev in ("contention_first", "round_robin"):
         cases[f"memory_{ev}_0p3s"] = S.config_memory(seed=1, horizon_s=0.3, eviction=ev)
+    # configs 2 / 3 (ResNet-50, BERT-base): training-step LP tasks, device-free specs
+    from paper_2601_04071_b200 import tenants as TN
+    for nm, g, n_par, mode, ops, rate in (("cfg2", TN.resnet50_train_gemms(64), TN.RESNET50_PARAMS, 1, 160, 200.0),
+                                          ("cfg3", TN.bert_train_gemms(32), TN.BERT_PARAMS, 0, 96, 100.0)):
+        specs, seq = TN.step_specs(nm, g, n_par, mode)
+        for seed in (1, 2):
+            cases[f"{nm}_seed{seed}_0p3s"] = S.train_infer(nm, seed=seed, horizon_s=0.3, hp_task=f"hp_{nm}", hp_ops=ops,
+                                                          hp_chain_ns=900_000, lp_task=f"lp_{nm}", lp_specs=specs,
+                                                          lp_sequence=seq, rate=rate)
     for name, sc in cases.items():
         out[name] = {"scenario": sc, "policies": {}}
         for pol in ("exclusive", "exclusive_lp", "splitkernel", "spatial", "reef"):

@@ -78,23 +78,30 @@ def test_config1_hp_chain_full_size(dev, T):
     assert dev.hp_chain_info(chain)["cluster"] == 4  # the fused DSMEM plan the bench runs
     dev.hp_launch_direct(chain, dev.hp_next_seq())
     dev.sync()
-    x = T.synth_bf16(M * H, SEED, 100, 1.0)
+    # (1) every op in isolation: the oracle op applied to the DEVICE's input of that op
+    # (elementwise agreement is then bf16 output rounding + fp32-vs-fp64 accumulation);
+    # (2) the whole chain: the oracle chain from the synthetic input, bf16 rounding between
+    # ops like the device (normwise; elementwise differences compound over 4 ops).
     per_op = []
+    x_dev = T.synth_bf16(M * H, SEED, 100, 1.0)
+    x_chain = x_dev
     for i in range(4):
-        want = T.gemm_rows(x, T.synth_bf16(H * H, SEED, 101 + i, s), list(range(M)), H, H).reshape(-1)
-        got_b = d2h(dev, act[i + 1], M * H)
-        nw, ew = errs(T.bf16_to_f32(got_b), want)
-        per_op.append((nw, ew))
-        assert nw <= BF16_TOL, (i, nw)
-        x = rnd(want)  # the next op consumes the bf16-rounded oracle output
-    want = T.bf16_to_f32(T.bias_gelu(d2h(dev, act[4], M * H), T.synth_bf16(H, SEED, 110, 0.1), M, H))
-    nw, ew = errs(T.bf16_to_f32(d2h(dev, out, M * H)), want)
-    assert nw <= BF16_TOL
-    per_op.append((nw, ew))
+        w_i = T.synth_bf16(H * H, SEED, 101 + i, s)
+        got_f = T.bf16_to_f32(d2h(dev, act[i + 1], M * H))
+        want = T.gemm_rows(x_dev, w_i, list(range(M)), H, H).reshape(-1)
+        per_op.append(errs(got_f, want))
+        x_chain = rnd(T.gemm_rows(x_chain, w_i, list(range(M)), H, H).reshape(-1))
+        x_dev = d2h(dev, act[i + 1], M * H)
+    want = T.bf16_to_f32(T.bias_gelu(x_dev, T.synth_bf16(H, SEED, 110, 0.1), M, H))
+    got_out = T.bf16_to_f32(d2h(dev, out, M * H))
+    per_op.append(errs(got_out, want))
+    chain_nw, chain_ew = errs(got_out, T.bf16_to_f32(T.bias_gelu(x_chain, T.synth_bf16(H, SEED, 110, 0.1), M, H)))
     record("config1_hp_chain_128x4096x4096x4", per_op_normwise=[p[0] for p in per_op],
-           per_op_elementwise=[p[1] for p in per_op], elements_checked=5 * M * H)
-    for p in per_op:
-        assert p[1] <= 0.1, per_op
+           per_op_elementwise=[p[1] for p in per_op], chain_normwise=chain_nw, chain_elementwise=chain_ew,
+           elements_checked=5 * M * H)
+    for nw, ew in per_op:
+        assert nw <= BF16_TOL and ew <= 2e-2, per_op
+    assert chain_nw <= BF16_TOL, chain_nw
     dev.hp_unregister_chain(chain)
     for p_ in act + ws + [bias, out]:
         dev.free(p_)
@@ -134,15 +141,19 @@ def test_config4_full_decode_step(dev, T):
         g, u = gu[:, :F], gu[:, F:]
         act = rnd((g / (1.0 + np.exp(-g)) * u).reshape(-1))
         h = rnd(T.gemm_rows(act, wd, rows, H, F).reshape(-1))
-    want = T.gemm_rows(h, T.synth_bf16(V * H, SEED, 799, sc(H)), rows, V, H).reshape(-1)
+    lm_h = T.synth_bf16(V * H, SEED, 799, sc(H))
     got = T.bf16_to_f32(d2h(dev, bufs[5], V))
-    nw, ew = errs(got, want)
-    h_dev = T.bf16_to_f32(d2h(dev, bufs[0], H))
-    nh, eh = errs(h_dev, T.bf16_to_f32(h))
-    record("config4_decode_step_16L_V128256", logits_normwise=nw, logits_elementwise=ew, final_h_normwise=nh,
-           final_h_elementwise=eh, elements_checked=V + H)
+    # the LM head in isolation (oracle applied to the device's final hidden state) ...
+    h_dev_b = d2h(dev, bufs[0], H)
+    iso_nw, iso_ew = errs(got, T.gemm_rows(h_dev_b, lm_h, rows, V, H).reshape(-1))
+    # ... and the whole 16-layer chain from the synthetic input
+    nw, ew = errs(got, T.gemm_rows(h, lm_h, rows, V, H).reshape(-1))
+    nh, eh = errs(T.bf16_to_f32(h_dev_b), T.bf16_to_f32(h))
+    record("config4_decode_step_16L_V128256", lm_head_isolated_normwise=iso_nw, lm_head_isolated_elementwise=iso_ew,
+           chain_logits_normwise=nw, chain_logits_elementwise=ew, chain_final_h_normwise=nh,
+           chain_final_h_elementwise=eh, elements_checked=V + H)
+    assert iso_nw <= BF16_TOL and iso_ew <= 2e-2, (iso_nw, iso_ew)
     assert nw <= BF16_TOL and nh <= BF16_TOL, (nw, nh)
-    assert ew <= 0.1
     dev.hp_unregister_chain(chain)
     for p_ in bufs + [p for l in ws for p in l] + [lm]:
         dev.free(p_)
