@@ -23,7 +23,15 @@
 //     measured ~2 us per op under full HBM load) is used only for inputs that are not
 //     produced in the chain.
 //   * units are dealt to CTAs round-robin on a counter that continues across ops, so each
-//     CTA's total byte count over the chain is balanced to within one unit.
+//     CTA's total byte count over the chain is balanced to within one unit (static mode), or
+//     (dynamic mode, default) each CTA's producer CLAIMS the next unit of the op with one
+//     atomic on a per-op counter just before loading it: a CTA that starts late (its SM still
+//     draining a preempted LP CTA when the doorbell fires) simply claims fewer units, instead
+//     of holding back every later op by its start delay.  The producer writes the claimed
+//     unit id next to the stage; when an op runs out it fills S = 12 sentinel stages (no
+//     data, a plain mbarrier arrive), one per consumer warp, so every warp learns where the
+//     op ends in this CTA's stream.  The L2 lookahead keeps the static unit plan (whichever
+//     CTA later claims a prefetched unit finds it in L2).
 //
 // Per-unit algorithmic bytes = the unit's weight bytes (the vectors are L2-resident and
 // small).  Roofline: HBM (MEASURED_PEAKS.json hbm_gbs).
@@ -67,6 +75,8 @@ static_assert(sizeof(GemvOpDesc) % 16 == 0, "descriptors are bulk-copied (16-byt
 struct GemvParams {
   TileRun run;  // HP bookkeeping (first-CTA stamp, completion record, phase-counter reset)
   uint32_t* phase_cnt;  // [n_ops]: CTAs that finished op i
+  uint32_t* claim;      // [n_ops]: dynamic mode unit claim counters (reset by the last CTA)
+  int dynamic;          // 1: units claimed dynamically (default), 0: static round-robin
   const GemvOpDesc* ops;  // [n_ops] in global memory (16-byte aligned), bulk-copied to smem
   int n_ops;
   uint32_t tag;  // this launch's wire tag (16 bits)
@@ -323,6 +333,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
   uint8_t* xs = ring + kGemvStages * kGemvStageBytes;
   const uint32_t ring_s = smem_u32(ring), xs_s = smem_u32(xs);
   __shared__ uint64_t full[kGemvStages], empty[kGemvStages], desc_bar;
+  __shared__ int stage_unit[kGemvStages];  // dynamic mode: unit id loaded into the stage (-1: op end)
   // Op descriptors live in shared memory (one bulk copy from global at entry): dynamically
   // indexed kernel-parameter reads go through the constant cache, whose misses wait behind
   // the saturated memory system, and small parameters keep the launch itself short.
@@ -384,7 +395,51 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         pf_seek(pf_oi, pf_u + G);
         return true;
       };
-      for (int oi = 0; oi < p.n_ops; ++oi) {
+      uint32_t pos = 0;  // dynamic mode: ring position (units + sentinels)
+      auto free_stage = [&](uint32_t at) {  // wait until ring position `at` may be (re)filled
+        if (at >= D) {
+          const uint32_t back = at - D;
+          mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
+        }
+        mbar_wait(&empty[at % kGemvStages], ((at / kGemvStages) & 1) ^ 1);
+      };
+      for (int oi = 0; oi < p.n_ops && p.dynamic; ++oi) {
+        const GemvOpDesc& o = sops[oi];
+        if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
+        const size_t row_bytes = static_cast<size_t>(o.k) * 2;
+        for (;;) {
+          free_stage(pos);
+          const int u = static_cast<int>(atomicAdd(p.claim + oi, 1u));
+          const uint32_t st = pos % kGemvStages;
+          if (u >= o.units) break;  // (the stage stays free for the first sentinel)
+          stage_unit[st] = u;
+          const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
+          const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
+          uint8_t* dst = ring + st * kGemvStageBytes;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(o.w) + r0 * row_bytes;
+          if (o.kind == kGemvSwiglu) {
+            mbar_arrive_expect_tx(&full[st], 2 * bytes);
+            bulk_load(dst, src, bytes, &full[st], pol);
+            bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[st], pol);
+          } else {
+            mbar_arrive_expect_tx(&full[st], bytes);
+            bulk_load(dst, src, bytes, &full[st], pol);
+          }
+          ++pos;
+          ++issued;
+          while (pf_step()) {
+          }
+        }
+        // one sentinel per consumer warp: positions pos .. pos + S - 1
+        for (int sidx = 0; sidx < kGemvConsumers; ++sidx) {
+          if (sidx > 0) free_stage(pos);
+          stage_unit[pos % kGemvStages] = -1;
+          mbar_arrive(&full[pos % kGemvStages]);
+          ++pos;
+        }
+        if (oi < 16) gemv_stamp(p.run, 48 + oi);
+      }
+      for (int oi = 0; oi < p.n_ops && !p.dynamic; ++oi) {
         const GemvOpDesc& o = sops[oi];
         if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
         const size_t row_bytes = static_cast<size_t>(o.k) * 2;
@@ -427,7 +482,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
     // phase ahead of a stage another warp has not released: mbarrier parity ABA).
     const int cw = warp - 1;
     const int t = threadIdx.x - 32;  // 0..255
-    uint32_t j = 0;
+    uint32_t j = p.dynamic ? static_cast<uint32_t>(cw) : 0u;  // dynamic: this warp's next ring position
     const uint32_t tag = p.tag;
     for (int oi = 0; oi < p.n_ops; ++oi) {
       const GemvOpDesc& o = sops[oi];
@@ -445,7 +500,27 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(g) : "r"(xs_s) : "memory");
           if (g != 0x7FEDCBA9u) p.run.dbg[2048 + 148 * 64 + blockIdx.x * 16 + oi] = globaltimer();
         }
-        for (int u = gemv_first_unit(o, G); u < o.units; u += G, ++j) {
+        if (p.dynamic) {
+          // this warp's ring positions: cw, cw + S, ... (continuing across ops); the op ends
+          // at this warp's sentinel
+          for (;;) {
+            const uint32_t stage = j % kGemvStages;
+            mbar_wait(&full[stage], (j / kGemvStages) & 1);
+            const int u = stage_unit[stage];
+            if (u < 0) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&empty[stage]);
+              j += kGemvConsumers;
+              break;
+            }
+            const float v = gemv_unit(o, u, ring_s + stage * kGemvStageBytes, xs_s, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (lane < gemv_unit_rows(o, u)) store_out(o, u * o.rows + lane, v, tag);
+            j += kGemvConsumers;
+          }
+        }
+        for (int u = gemv_first_unit(o, G); u < o.units && !p.dynamic; u += G, ++j) {
           if (static_cast<int>(j % kGemvConsumers) != cw) continue;
           const uint32_t stage = j % kGemvStages;
           mbar_wait(&full[stage], (j / kGemvStages) & 1);

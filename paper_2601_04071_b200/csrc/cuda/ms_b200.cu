@@ -178,6 +178,9 @@ struct HpChain {
   // kernels wait for this event.
   int lead_copies = 0;
   cudaEvent_t in_ev = nullptr;
+  // SM pull of the leading H2D (default e2e mode): device views of the host sources
+  std::vector<uint64_t> pull_src;
+  unsigned int* pull_done = nullptr;
 };
 
 }  // namespace
@@ -391,7 +394,8 @@ int check_glue(const ms_hp_op& op) {
   return fail(MS_E_ARG, "not a glue op");
 }
 
-int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq, bool after_gate) {
+int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t seq, bool after_gate,
+                 bool after_pull = false) {
   const HpOpRt& o = ch.ops[i];
   if (o.op.kind == MS_HP_H2D || o.op.kind == MS_HP_D2H) {
     MS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(o.op.c), reinterpret_cast<const void*>(o.op.a),
@@ -415,8 +419,9 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   r.hp_seq = seq;
   // PDL when the stream predecessor is a kernel (the gate, or the previous chain kernel);
   // the chain's first kernel does not depend on the gate's output, later ones wait.
-  const bool prev_is_kernel = i > 0 ? !is_copy(ch.ops[i - 1].op) : after_gate;
-  r.pdl_wait = i > 0 && prev_is_kernel;
+  const bool prev_is_kernel = after_pull || (i > 0 ? !is_copy(ch.ops[i - 1].op) : after_gate);
+  r.pdl_wait = (i > 0 && prev_is_kernel) || after_pull;
+  if (after_pull) r.hp_first = 0;  // the pull kernel stamps t_first_cta when the input is resident
   if (is_glue(o.op.kind)) return launch_glue(d, o, r, prev_is_kernel);
   if (o.op.kind == MS_HP_GEMM_SWIGLU) {
     // GEMM into tmp ([gate | up] halves), then the SwiGLU kernel (PDL) writes c.
@@ -811,32 +816,40 @@ int plan_gemv(ms_dev* d, HpChain& ch) {
   MS_CUDA(cudaMalloc(&ch.gemv_descs_d, sizeof(GemvOpDesc) * n));
   MS_CUDA(cudaMemcpy(ch.gemv_descs_d, ch.gemv_descs.data(), sizeof(GemvOpDesc) * n, cudaMemcpyHostToDevice));
   const int np = n;
-  MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * np));
-  MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * np));
+  // [0, n): grid phase counters; [n, 2n): dynamic unit-claim counters (both reset by the
+  // last CTA of each launch)
+  MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * 2 * np));
+  MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * 2 * np));
   ch.fused_ctl = d->next_hp_ctl++;
   if (ch.fused_ctl >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
   ch.fused_first = first;
   ch.fused_last = last;
   ch.fused_grid = grid;
   ch.fused_cs = 1;
-  ch.n_phases = np;
+  ch.n_phases = 2 * np;
   ch.gemv = true;
   ch.fusable = true;
   return 0;
 }
 
-int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl) {
+int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl, bool after_pull = false) {
   GemvParams p{};
   p.run = base_run(d, ch.fused_ctl);
   p.run.hp_ctl = d->hp_ctl + chain_id;
   p.run.hp_rec = &d->page_d->hp[chain_id];
-  p.run.hp_first = 1;
+  p.run.hp_first = after_pull ? 0 : 1;
+  p.run.pdl_wait = after_pull ? 1 : 0;
   p.run.hp_last = !is_copy(ch.ops.back().op);
   p.run.hp_seq = seq;
   p.run.dbg = d->dbg;
   p.run.reset_words = ch.phase_d;
   p.run.n_reset = ch.n_phases;
   p.phase_cnt = ch.phase_d;
+  p.claim = ch.phase_d + ch.gemv_descs.size();
+  p.dynamic = [] {
+    const char* e = getenv("MS_GEMV_DYNAMIC");  // A/B: 0 = static round-robin unit plan
+    return e ? atoi(e) : 1;
+  }();
   p.n_ops = static_cast<int>(ch.gemv_descs.size());
   p.ops = ch.gemv_descs_d;
   p.tag = (++ch.launches) & 0xFFFFu;
@@ -855,12 +868,13 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
   return 0;
 }
 
-int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl) {
+int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool pdl, bool after_pull = false) {
   FusedParams p{};
   p.run = base_run(d, ch.fused_ctl);
   p.run.hp_ctl = d->hp_ctl + chain_id;
   p.run.hp_rec = &d->page_d->hp[chain_id];
-  p.run.hp_first = 1;
+  p.run.hp_first = after_pull ? 0 : 1;
+  p.run.pdl_wait = after_pull ? 1 : 0;
   p.run.hp_last = !is_copy(ch.ops.back().op);
   p.run.hp_seq = seq;
   p.run.dbg = d->dbg;
@@ -894,18 +908,22 @@ int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool 
 }
 
 // Enqueue a chain's work on the HP stream (after its gate when `after_gate`).
-int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after_gate, size_t first_op = 0) {
+// `after_pull`: the kernel before op first_op is the e2e input pull (hp_pull_kernel).
+int launch_chain(ms_dev* d, int cid, const HpChain& ch, uint32_t seq, bool after_gate, size_t first_op = 0,
+                 bool after_pull = false) {
   // batch-1 chains have no per-op kernels: the GEMV chain is their only implementation
   const bool fused = (d->hp_fused && ch.fusable) || ch.gemv;
   for (size_t i = first_op; i < ch.ops.size(); ++i) {
+    const bool pulled = after_pull && i == first_op;
     if (fused && static_cast<int>(i) >= ch.fused_first && static_cast<int>(i) <= ch.fused_last) {
       if (static_cast<int>(i) == ch.fused_first) {
-        const bool pdl = after_gate && i == 0;
-        if (int rc = ch.gemv ? launch_gemv(d, cid, ch, seq, pdl) : launch_fused(d, cid, ch, seq, pdl)) return rc;
+        const bool pdl = (after_gate && i == 0) || pulled;
+        if (int rc = ch.gemv ? launch_gemv(d, cid, ch, seq, pdl, pulled) : launch_fused(d, cid, ch, seq, pdl, pulled))
+          return rc;
       }
       continue;
     }
-    if (int rc = launch_hp_op(d, cid, ch, i, seq, after_gate)) return rc;
+    if (int rc = launch_hp_op(d, cid, ch, i, seq, after_gate, pulled)) return rc;
   }
   return 0;
 }
@@ -1004,7 +1022,7 @@ int ms_dev_sync(ms_dev* d) {
 int ms_host_alloc(ms_dev* d, size_t bytes, uint64_t* p) {
   MS_CUDA(cudaSetDevice(d->ordinal));
   void* ptr = nullptr;
-  MS_CUDA(cudaHostAlloc(&ptr, bytes, cudaHostAllocPortable));
+  MS_CUDA(cudaHostAlloc(&ptr, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
   *p = reinterpret_cast<uint64_t>(ptr);
   return 0;
 }
@@ -1544,7 +1562,22 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
   while (ch.lead_copies < static_cast<int>(ch.ops.size()) && ch.ops[ch.lead_copies].op.kind == MS_HP_H2D)
     ++ch.lead_copies;
   if (ch.lead_copies == static_cast<int>(ch.ops.size())) ch.lead_copies = 0;  // copy-only chain: plain path
-  if (ch.lead_copies) MS_CUDA(cudaEventCreateWithFlags(&ch.in_ev, cudaEventDisableTiming));
+  if (ch.lead_copies) {
+    MS_CUDA(cudaEventCreateWithFlags(&ch.in_ev, cudaEventDisableTiming));
+    // SM pull needs a device-mapped view of each pinned source and 16-byte granules
+    bool ok = true;
+    for (int i = 0; i < ch.lead_copies && ok; ++i) {
+      const ms_hp_op& op = ch.ops[i].op;
+      void* dp = nullptr;
+      ok = op.m % 16 == 0 && op.a % 16 == 0 && op.c % 16 == 0 &&
+           cudaHostGetDevicePointer(&dp, reinterpret_cast<void*>(op.a), 0) == cudaSuccess;
+      if (ok) ch.pull_src.push_back(reinterpret_cast<uint64_t>(dp));
+    }
+    cudaGetLastError();  // (a non-mapped source is not an error: the copy-engine path runs)
+    if (!ok) ch.pull_src.clear();
+    MS_CUDA(cudaMalloc(&ch.pull_done, sizeof(unsigned int) * ch.lead_copies));
+    MS_CUDA(cudaMemset(ch.pull_done, 0, sizeof(unsigned int) * ch.lead_copies));
+  }
   ch.used = true;
   d->chains[cid] = ch;
   *chain_id = cid;
@@ -1557,6 +1590,7 @@ int ms_hp_unregister_chain(ms_dev* d, int cid) {
   MS_CUDA(cudaStreamSynchronize(d->hpcopy));
   HpChain& ch = d->chains[cid];
   if (ch.in_ev) cudaEventDestroy(ch.in_ev);
+  if (ch.pull_done) cudaFree(ch.pull_done);
   for (HpOpRt& o : ch.ops) {
     if (o.ws) cudaFree(o.ws);
     if (o.tile_cnt) cudaFree(o.tile_cnt);
@@ -1595,10 +1629,14 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
     const char* e = std::getenv("MS_GATE_SMEM");
     return e ? std::max(0, std::min(atoi(e), kGateSmem)) : kGateSmem;
   }();
-  const bool overlap = ch.lead_copies > 0 && [] {
-    const char* e = std::getenv("MS_E2E_OVERLAP");  // A/B: 0 = copy queued behind the HP gate
-    return !e || atoi(e) != 0;
+  // e2e input modes (MS_E2E_MODE): 2 = SM pull on the HP stream (default), 1 = copy engine on
+  // its own gated stream + event, 0 = copy queued behind the HP gate
+  const int e2e_mode = ch.lead_copies == 0 ? -1 : [] {
+    const char* e = std::getenv("MS_E2E_MODE");
+    return e ? atoi(e) : 2;
   }();
+  const bool pull = e2e_mode == 2 && static_cast<int>(ch.pull_src.size()) == ch.lead_copies;
+  const bool overlap = e2e_mode == 1;
   if (overlap) {
     // e2e input: its own gate on the copy stream, so the H2D starts at the ring (no SM
     // work needed, it overlaps the LP drain); the chain waits for the copy's event.
@@ -1613,6 +1651,19 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   }
   gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
   MS_CUDA(cudaGetLastError());
+  if (pull) {
+    for (int i = 0; i < ch.lead_copies; ++i) {
+      const ms_hp_op& op = ch.ops[i].op;
+      PullParams q{};
+      q.src = reinterpret_cast<const uint4*>(ch.pull_src[i]);
+      q.dst = reinterpret_cast<uint4*>(op.c);
+      q.n16 = static_cast<unsigned long long>(op.m) / 16;
+      q.hp_ctl = d->hp_ctl + cid;
+      q.done = ch.pull_done + i;
+      MS_CUDA(launch_k(hp_pull_kernel, kPullCtas, kPullThreads, 0, d->hp, true, q));
+    }
+    return launch_chain(d, cid, ch, seq, false, static_cast<size_t>(ch.lead_copies), true);
+  }
   if (overlap) {
     MS_CUDA(cudaStreamWaitEvent(d->hp, ch.in_ev, 0));
     return launch_chain(d, cid, ch, seq, false, static_cast<size_t>(ch.lead_copies));

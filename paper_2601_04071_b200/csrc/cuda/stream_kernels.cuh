@@ -304,6 +304,48 @@ __global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpReco
   }
 }
 
+// e2e request input, pulled by SMs from pinned host memory (PCIe reads, many 16-byte loads
+// in flight) into HBM as the first HP kernel of an armed chain: PDL-released by the gate at
+// the ring (no copy-engine start, no event -> launch hop), and the chain's first kernel is
+// PDL-released by it in turn.  Its last CTA stamps the chain's t_first_cta when the input is
+// resident: the e2e preemption latency = ring -> HP input in HBM (its compute then starts
+// at the dependent's griddepcontrol.wait).
+struct PullParams {
+  const uint4* src;      // device view of the pinned host buffer
+  uint4* dst;
+  unsigned long long n16;  // 16-byte words
+  MsHpCtl* hp_ctl;
+  unsigned int* done;    // CTAs finished (self-resetting)
+};
+constexpr int kPullThreads = 256, kPullCtas = 7, kPullUnroll = 8;
+
+__global__ void __launch_bounds__(kPullThreads) hp_pull_kernel(const __grid_constant__ PullParams p) {
+  pdl_launch_dependents();  // the chain kernel may become resident now; it waits for our completion
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * kPullThreads;
+  for (unsigned long long i0 = blockIdx.x * static_cast<unsigned long long>(kPullThreads) + threadIdx.x; i0 < p.n16;
+       i0 += stride * kPullUnroll) {
+    uint4 v[kPullUnroll];
+#pragma unroll
+    for (int u = 0; u < kPullUnroll; ++u) {
+      const unsigned long long i = i0 + u * stride;
+      if (i < p.n16) v[u] = p.src[i];
+    }
+#pragma unroll
+    for (int u = 0; u < kPullUnroll; ++u) {
+      const unsigned long long i = i0 + u * stride;
+      if (i < p.n16) p.dst[i] = v[u];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.done, 1u) + 1 == gridDim.x) {
+      atomicMin(&p.hp_ctl->t_first_cta, static_cast<unsigned long long>(globaltimer()));
+      *p.done = 0;
+    }
+  }
+}
+
 // Completion record of a chain whose last op is a copy (e2e mode): written after the D2H.
 __global__ void hp_notify_kernel(MsHpCtl* ctl, MsHpRecord* rec, unsigned int seq) {
   const unsigned long long t = globaltimer();

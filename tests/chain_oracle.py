@@ -74,6 +74,12 @@ class ChainOracle:
                 a = np.ascontiguousarray(np.lib.stride_tricks.as_strided(a, (m, K), (lda * 2, 2))).reshape(-1)
             w = rd(o["b"], n * K)
             return rnd(T.gemm_rows(a, w, list(range(m)), n, K).reshape(-1))
+        if k == GEMM_SWIGLU:  # silu(x Wg^T) * (x Wu^T) on the fp32 accumulators, W = [Wg; Wu]
+            K, lda = o["k"], o.get("lda") or o["k"]
+            a = rd(o["a"], (m - 1) * lda + K)
+            gu = T.gemm_rows(np.ascontiguousarray(a), rd(o["b"], 2 * n * K), list(range(m)), 2 * n, K)
+            g, u = gu[:, :n].astype(np.float64), gu[:, n:].astype(np.float64)
+            return rnd((g / (1.0 + np.exp(-g)) * u).reshape(-1))
         if k == BIAS_GELU:
             return T.bias_gelu(rd(o["a"], m * n), rd(o["bias"], n), m, n)
         if k == IM2COL:

@@ -216,8 +216,11 @@ def test_train_step_gemm_shapes(dev, T, m, n, k):
     want = T.gemm_rows(A, T.synth_bf16(n * k, SEED, 12, s), rows, n, k)
     got = T.bf16_to_f32(d2h(dev, c, m * n).reshape(m, n)[rows].reshape(-1)).reshape(len(rows), n)
     nw, ew = errs(got, want)
-    record(f"train_gemm_{m}x{n}x{k}", normwise=nw, elementwise=ew, rows=len(rows))
-    assert nw <= 1e-2 and ew <= 2e-2, (nw, ew)
+    # fp32 accumulation (TMEM) vs the fp64 oracle: the rounding of the sum grows like
+    # sqrt(K); the element tolerance scales with it past K = 64k (wgrad over 802,816 rows)
+    ew_tol = 2e-2 * max(1.0, math.sqrt(k / 65536))
+    record(f"train_gemm_{m}x{n}x{k}", normwise=nw, elementwise=ew, elementwise_tol=ew_tol, rows=len(rows))
+    assert nw <= 1e-2 and ew <= ew_tol, (nw, ew)
     dev.lp_unregister(kern)
     for p_ in (a, b, c):
         dev.free(p_)
@@ -230,7 +233,7 @@ def test_optimizer_streamer_bit_exact_preempted(dev, T, mode):
     p, m1, m2, g = dev.alloc(4 * n), dev.alloc(4 * n), dev.alloc(4 * n), dev.alloc(2 * n)
     dev.fill_synth_f32(p, n, SEED, 20, 0.05)
     dev.fill_synth_f32(m1, n, SEED, 21, 0.01)
-    dev.fill_synth_f32(m2, n, SEED, 22, 0.01)
+    dev.memset(m2, 0, 4 * n)  # second moment starts at 0 (>= 0: sqrt defined)
     dev.fill_synth(g, n, SEED, 23, 0.01)
     hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.01, c1=10.0, c2=1000.0) if mode == 0 else \
         dict(lr=0.1, beta1=0.9, beta2=0.0, eps=0.0, wd=1e-4, c1=1.0, c2=1.0)
@@ -240,13 +243,14 @@ def test_optimizer_streamer_bit_exact_preempted(dev, T, mode):
         dev.lp_run(k, begin, k.total_tiles)
         runs += 1
         if runs <= 2:
-            time.sleep(0.0001)
+            time.sleep(0.00005 * runs)
             dev.preempt_raise()
         st = dev.lp_wait(k, 60)
         begin = st["cursor"]
         if begin >= k.total_tiles and st["redo_count"] == 0:
             break
-    P, M1, M2 = (T.synth_f32(n, SEED, t, sc) for t, sc in ((20, 0.05), (21, 0.01), (22, 0.01)))
+    P, M1 = (T.synth_f32(n, SEED, t, sc) for t, sc in ((20, 0.05), (21, 0.01)))
+    M2 = np.zeros(n, np.float32)
     T.optim(P, M1, M2, T.synth_bf16(n, SEED, 23, 0.01), mode, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
             hp["wd"], hp["c1"], hp["c2"])
 
@@ -254,10 +258,13 @@ def test_optimizer_streamer_bit_exact_preempted(dev, T, mode):
         out = np.empty(n, np.float32)
         dev.d2h(out.ctypes.data, ptr, 4 * n)
         return out
-    assert np.array_equal(f32(p), P) and np.array_equal(f32(m1), M1)
+    got_p = f32(p)
+    assert not np.isnan(P).any()
+    assert np.array_equal(got_p, P) and np.array_equal(f32(m1), M1)
     if mode == 0:
         assert np.array_equal(f32(m2), M2)
     record(f"optim_mode{mode}", elements=n, runs=runs, bit_exact=True)
+    assert runs > 1  # the step was preempted and resumed
     dev.lp_unregister(k)
     for x in (p, m1, m2, g):
         dev.free(x)
