@@ -46,6 +46,15 @@ $(LIB)/libms_b200.so: $(CUDA_OBJ) $(LIVE_OBJ) $(LIB)/libmicroslice.so
 oracle:
 	$(MAKE) -C oracle
 
+# Test infrastructure: the live scheduler (unchanged live.cpp) over a virtual-time CPU model
+# of the device C-ABI (tests/livemock/mock_device.cpp) -> tests/test_live_decisions.py.
+livemock: build/livemock/libms_livemock.so
+build/livemock/libms_livemock.so: tests/livemock/mock_device.cpp $(PKG)/csrc/live/live.cpp $(LIB)/libmicroslice.so \
+    $(wildcard include/microslice/*.hpp) include/ms_b200.h include/ms_live.h
+	@mkdir -p build/livemock
+	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -shared -o $@ tests/livemock/mock_device.cpp $(PKG)/csrc/live/live.cpp \
+	  -L$(LIB) -lmicroslice -Wl,-rpath,$(abspath $(LIB)) -ldl -lpthread
+
 clean:
 	rm -rf build $(LIB)
-.PHONY: all host cuda oracle clean
+.PHONY: all host cuda oracle livemock clean

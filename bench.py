@@ -286,6 +286,13 @@ CFG4_WORKLOAD = ("cfg4 (BASELINE configs[3]): HP Llama-3.2-1B-geometry bs=1 deco
                  "80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 axpy streamer; governed")
 
 
+CFG2_WORKLOAD = ("cfg2 (BASELINE configs[1]): HP ResNet-50 bs=1 224x224 inference (130-op chain: im2col + tcgen05 "
+                 "conv GEMMs + bias/ReLU/residual + pools + FC), Poisson; LP ResNet-50 bs=64 training step (161 "
+                 "GEMMs fwd/dgrad/wgrad, 48 shapes, + SGD-momentum 25.6 M params); governed")
+CFG3_WORKLOAD = ("cfg3 (BASELINE configs[2]): HP BERT-base bs=1 seq-128 encoder (96-op chain), Poisson; LP BERT-base "
+                 "bs=32 training step (144 GEMMs, 9 shapes, + AdamW 110 M params); governed")
+
+
 # ----------------------------------------------------------------------------- host facts
 def host_info() -> dict:
     model = None
@@ -344,6 +351,10 @@ def main():
                     help="config-1 trace windows for the side runs (kernel-boundary baselines, governed variant)")
     ap.add_argument("--cfg4-s", type=float, default=26.0,
                     help="config-4 leg (decode HP at 80%% load, governed): trace seconds (>= 300 requests); 0 skips")
+    ap.add_argument("--cfg2-s", type=float, default=6.0,
+                    help="config-2 leg (ResNet-50 bs=1 HP at 200 req/s + bs=64 training LP): trace seconds; 0 skips")
+    ap.add_argument("--cfg3-s", type=float, default=6.0,
+                    help="config-3 leg (BERT-base bs=1 HP at 100 req/s + bs=32 training LP): trace seconds; 0 skips")
     ap.add_argument("--detail", default=str(ROOT / "gpurun_out" / "bench_detail.json"),
                     help="full per-leg results (the printed line is the compact summary)")
     args = ap.parse_args()
@@ -459,7 +470,20 @@ def main():
         w4.calibrate()
         cfg4 = run_policy_leg(dev, w4, args.cfg4_s, 7 + 10_000 * rank, w4.hp_rate(0.8), reef_s=min(args.cfg4_s, 8.0))
 
-    mine = {"cfg4": cfg4, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "rows": rows,
+    legs23 = {}
+    for key, cls_name, secs in (("cfg2", "Config2", args.cfg2_s), ("cfg3", "Config3", args.cfg3_s)):
+        if secs <= 0 or profiling:
+            continue
+        from paper_2601_04071_b200 import live as L_
+        wx = getattr(L_, cls_name)(dev)
+        wx.options = (lambda f: (lambda **kw: f(pin_core=core, **kw)))(wx.options)
+        time.sleep(0.3)
+        wx.calibrate()
+        legs23[key] = run_policy_leg(dev, wx, secs, 11 + 10_000 * rank, wx.hp_rate(), exlp_s=3.0,
+                                     reef_s=min(secs, 4.0))
+        wx.close()
+
+    mine = {"cfg4": cfg4, "legs23": legs23, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "rows": rows,
             "tiles": tiles, "kb": kb, "exlp_rate": exlp_rate, "ex_rows": ex_rows, "step_ms": step_ms, "wall": wall,
             "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"], "launches": launches,
             "chains": chains, "clocks": clk.summary(), "calib": calib, "slo": slo, "pb": pb,
@@ -491,6 +515,8 @@ def main():
     if ncu.exists():
         traffic = json.loads(ncu.read_text()).get("tc_gemm_kernel<256>", {}).get("dram_bytes_per_launch")
     cfg4_agg = aggregate_leg([r["cfg4"] for r in allr], CFG4_WORKLOAD) if allr[0]["cfg4"] else None
+    legs_agg = {key: aggregate_leg([r["legs23"][key] for r in allr], wl) for key, wl in
+                (("cfg2", CFG2_WORKLOAD), ("cfg3", CFG3_WORKLOAD)) if key in allr[0]["legs23"]}
     cb = None
     if not args.no_cpu_baseline:
         from paper_2601_04071_b200 import scenarios as S
@@ -541,6 +567,8 @@ def main():
         "clocks": allr[0]["clocks"],
         "host": dict(host_info(), scheduler_cores=[r["core"] for r in allr]),
         "config4_decode_high_load": cfg4_agg,
+        "config2_resnet50": legs_agg.get("cfg2"),
+        "config3_bert_base": legs_agg.get("cfg3"),
     }
     if cb:
         line["cpu_baseline"] = {"value": cb["p99_us"], "unit": "us", "cores": 1, "kind": "reference",
@@ -552,7 +580,9 @@ def main():
         "cfg1": {"p99_le_10us": (p99_inf if p99_inf is not None else p99) <= 10.0,
                  "slo_within_1pt": att_sk >= att_ex - 0.01,
                  "lp_ge_2x_kernel_boundary": round(lp_rate / max(1e-9, kb_rate["reef_req"]), 3) >= 2.0},
-        "cfg4": cfg4_agg["targets"] if cfg4_agg else None}
+        "cfg4": cfg4_agg["targets"] if cfg4_agg else None,
+        "cfg2": legs_agg["cfg2"]["targets"] if "cfg2" in legs_agg else None,
+        "cfg3": legs_agg["cfg3"]["targets"] if "cfg3" in legs_agg else None}
     try:
         Path(args.detail).parent.mkdir(parents=True, exist_ok=True)
         Path(args.detail).write_text(json.dumps({"line": line, "calib": calib, "slo_ns": allr[0]["slo"],

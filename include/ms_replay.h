@@ -103,6 +103,8 @@ int ms_generate_bursty_arrivals(double rate, double burstiness, int64_t horizon_
 #define MS_RUN_NDJSON 1
 #define MS_RUN_REPORT 2
 #define MS_RUN_DELAYS 4
+#define MS_RUN_ROWS 8   /* per-request rows [arrival, ttft, tpot, iterations, completed] (the live
+                           runtime's ms_live_run row format), for decision-level comparisons */
 int ms_replay_run(const char* scenario_json, const char* policy, int flags, char** out_json, char* err,
                   size_t err_len);
 

@@ -17,7 +17,7 @@ _PKG = Path(__file__).resolve().parent
 LIB_DIR = _PKG / "lib"
 
 MS_OK, MS_E_ARG, MS_E_VALIDATION, MS_E_ENGINE, MS_E_CAPACITY = 0, -1, -2, -3, -4
-MS_RUN_NDJSON, MS_RUN_REPORT, MS_RUN_DELAYS = 1, 2, 4
+MS_RUN_NDJSON, MS_RUN_REPORT, MS_RUN_DELAYS, MS_RUN_ROWS = 1, 2, 4, 8
 
 
 class ValidationError(ValueError):

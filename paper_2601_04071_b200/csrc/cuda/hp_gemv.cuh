@@ -24,14 +24,13 @@
 //     produced in the chain.
 //   * units are dealt to CTAs round-robin on a counter that continues across ops, so each
 //     CTA's total byte count over the chain is balanced to within one unit (static mode), or
-//     (dynamic mode, default) each CTA's producer CLAIMS the next unit of the op with one
-//     atomic on a per-op counter just before loading it: a CTA that starts late (its SM still
-//     draining a preempted LP CTA when the doorbell fires) simply claims fewer units, instead
-//     of holding back every later op by its start delay.  The producer writes the claimed
-//     unit id next to the stage; when an op runs out it fills S = 12 sentinel stages (no
-//     data, a plain mbarrier arrive), one per consumer warp, so every warp learns where the
-//     op ends in this CTA's stream.  The L2 lookahead keeps the static unit plan (whichever
-//     CTA later claims a prefetched unit finds it in L2).
+//     (dynamic mode, default) each CTA's producer CLAIMS batches of units of the op from a
+//     per-op counter (the next batch's atomic in flight while the current one loads): a CTA
+//     that starts late (its SM still draining a preempted LP CTA when the doorbell fires)
+//     simply claims fewer units instead of holding back every later op by its start delay.
+//     The producer writes each stage's (op, unit) next to it; a consumer warp's op ends at
+//     the first of its positions that holds a later op's unit.  The L2 lookahead keeps the
+//     static unit plan (whichever CTA claims a prefetched unit finds it in L2).
 //
 // Per-unit algorithmic bytes = the unit's weight bytes (the vectors are L2-resident and
 // small).  Roofline: HBM (MEASURED_PEAKS.json hbm_gbs).
@@ -77,6 +76,7 @@ struct GemvParams {
   uint32_t* phase_cnt;  // [n_ops]: CTAs that finished op i
   uint32_t* claim;      // [n_ops]: dynamic mode unit claim counters (reset by the last CTA)
   int dynamic;          // 1: units claimed dynamically (default), 0: static round-robin
+  int claim_batch;      // dynamic: units per claim (one atomic per batch, the next in flight)
   const GemvOpDesc* ops;  // [n_ops] in global memory (16-byte aligned), bulk-copied to smem
   int n_ops;
   uint32_t tag;  // this launch's wire tag (16 bits)
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
   uint8_t* xs = ring + kGemvStages * kGemvStageBytes;
   const uint32_t ring_s = smem_u32(ring), xs_s = smem_u32(xs);
   __shared__ uint64_t full[kGemvStages], empty[kGemvStages], desc_bar;
-  __shared__ int stage_unit[kGemvStages];  // dynamic mode: unit id loaded into the stage (-1: op end)
+  __shared__ int2 stage_meta[kGemvStages];  // (op, unit) loaded into each stage; op == n_ops: end
   // Op descriptors live in shared memory (one bulk copy from global at entry): dynamically
   // indexed kernel-parameter reads go through the constant cache, whose misses wait behind
   // the saturated memory system, and small parameters keep the launch itself short.
@@ -395,83 +395,59 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         pf_seek(pf_oi, pf_u + G);
         return true;
       };
-      uint32_t pos = 0;  // dynamic mode: ring position (units + sentinels)
-      auto free_stage = [&](uint32_t at) {  // wait until ring position `at` may be (re)filled
-        if (at >= D) {
-          const uint32_t back = at - D;
-          mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
-        }
-        mbar_wait(&empty[at % kGemvStages], ((at / kGemvStages) & 1) ^ 1);
-      };
-      for (int oi = 0; oi < p.n_ops && p.dynamic; ++oi) {
+      // Ring position `pos` (counted across ops) holds one unit; the unit's (op, id) is
+      // written next to the stage before the load is issued (the full-barrier completion
+      // publishes it).  Unit source: dynamic = batches of B units claimed from the op's
+      // counter, the next batch's atomic in flight while the current one is issued; static
+      // = every G-th unit from this CTA's round-robin start.
+      uint32_t pos = 0;
+      const int B = p.claim_batch;
+      for (int oi = 0; oi < p.n_ops; ++oi) {
         const GemvOpDesc& o = sops[oi];
         if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
         const size_t row_bytes = static_cast<size_t>(o.k) * 2;
+        int next = p.dynamic ? static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)))
+                             : gemv_first_unit(o, G);
         for (;;) {
-          free_stage(pos);
-          const int u = static_cast<int>(atomicAdd(p.claim + oi, 1u));
-          const uint32_t st = pos % kGemvStages;
-          if (u >= o.units) break;  // (the stage stays free for the first sentinel)
-          stage_unit[st] = u;
-          const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
-          const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
-          uint8_t* dst = ring + st * kGemvStageBytes;
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(o.w) + r0 * row_bytes;
-          if (o.kind == kGemvSwiglu) {
-            mbar_arrive_expect_tx(&full[st], 2 * bytes);
-            bulk_load(dst, src, bytes, &full[st], pol);
-            bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[st], pol);
-          } else {
-            mbar_arrive_expect_tx(&full[st], bytes);
-            bulk_load(dst, src, bytes, &full[st], pol);
+          const int b0 = next;
+          if (b0 >= o.units) break;
+          const int b1 = p.dynamic ? min(b0 + B, o.units) : b0 + 1;
+          next = p.dynamic ? static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B))) : b0 + G;
+          for (int u = b0; u < b1; ++u, ++pos, ++issued) {
+            // Bound the loads in flight: a full 12-stage queue on every SM inflates HBM latency
+            // (and the op->op handoff traffic behind it); landed units may still fill the
+            // whole ring while the consumers wait for an op's input.
+            if (pos >= D) {
+              const uint32_t back = pos - D;
+              mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
+            }
+            const uint32_t st = pos % kGemvStages;
+            mbar_wait(&empty[st], ((pos / kGemvStages) & 1) ^ 1);
+            stage_meta[st] = make_int2(oi, u);
+            const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
+            const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
+            uint8_t* dst = ring + st * kGemvStageBytes;
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(o.w) + r0 * row_bytes;
+            if (o.kind == kGemvSwiglu) {
+              mbar_arrive_expect_tx(&full[st], 2 * bytes);
+              bulk_load(dst, src, bytes, &full[st], pol);  // gate rows
+              bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[st], pol);
+            } else {
+              mbar_arrive_expect_tx(&full[st], bytes);
+              bulk_load(dst, src, bytes, &full[st], pol);
+            }
+            while (pf_step()) {
+            }  // keep the L2 lookahead P units past the issue point
           }
-          ++pos;
-          ++issued;
-          while (pf_step()) {
-          }
-        }
-        // one sentinel per consumer warp: positions pos .. pos + S - 1
-        for (int sidx = 0; sidx < kGemvConsumers; ++sidx) {
-          if (sidx > 0) free_stage(pos);
-          stage_unit[pos % kGemvStages] = -1;
-          mbar_arrive(&full[pos % kGemvStages]);
-          ++pos;
-        }
-        if (oi < 16) gemv_stamp(p.run, 48 + oi);
-      }
-      for (int oi = 0; oi < p.n_ops && !p.dynamic; ++oi) {
-        const GemvOpDesc& o = sops[oi];
-        if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
-        const size_t row_bytes = static_cast<size_t>(o.k) * 2;
-        for (int u = gemv_first_unit(o, G); u < o.units; u += G, ++issued) {
-          const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
-          const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
-          // Bound the loads in flight: a full 12-stage queue on every SM inflates HBM latency
-          // (and the op->op handoff traffic behind it); landed units may still fill the
-          // whole ring while the consumers wait for an op's input.
-          if (issued >= D) {
-            const uint32_t back = issued - D;
-            mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
-          }
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* dst = ring + stage * kGemvStageBytes;
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(o.w) + r0 * row_bytes;
-          if (o.kind == kGemvSwiglu) {
-            mbar_arrive_expect_tx(&full[stage], 2 * bytes);
-            bulk_load(dst, src, bytes, &full[stage], pol);  // gate rows
-            bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[stage], pol);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], bytes);
-            bulk_load(dst, src, bytes, &full[stage], pol);
-          }
-          if (++stage == kGemvStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-          while (pf_step()) {
-          }  // keep the L2 lookahead P units past the issue point
         }
         if (oi < 16) gemv_stamp(p.run, 48 + oi);  // last unit of op oi issued
+      }
+      // end of the chain: one terminal entry per consumer warp (no data)
+      for (int w = 0; w < kGemvConsumers; ++w, ++pos) {
+        const uint32_t st = pos % kGemvStages;
+        mbar_wait(&empty[st], ((pos / kGemvStages) & 1) ^ 1);
+        stage_meta[st] = make_int2(p.n_ops, 0);
+        mbar_arrive(&full[st]);
       }
     }
   } else {
@@ -482,7 +458,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
     // phase ahead of a stage another warp has not released: mbarrier parity ABA).
     const int cw = warp - 1;
     const int t = threadIdx.x - 32;  // 0..255
-    uint32_t j = p.dynamic ? static_cast<uint32_t>(cw) : 0u;  // dynamic: this warp's next ring position
+    uint32_t j = static_cast<uint32_t>(cw);  // this warp's next ring position
     const uint32_t tag = p.tag;
     for (int oi = 0; oi < p.n_ops; ++oi) {
       const GemvOpDesc& o = sops[oi];
@@ -500,34 +476,20 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(g) : "r"(xs_s) : "memory");
           if (g != 0x7FEDCBA9u) p.run.dbg[2048 + 148 * 64 + blockIdx.x * 16 + oi] = globaltimer();
         }
-        if (p.dynamic) {
-          // this warp's ring positions: cw, cw + S, ... (continuing across ops); the op ends
-          // at this warp's sentinel
-          for (;;) {
-            const uint32_t stage = j % kGemvStages;
-            mbar_wait(&full[stage], (j / kGemvStages) & 1);
-            const int u = stage_unit[stage];
-            if (u < 0) {
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&empty[stage]);
-              j += kGemvConsumers;
-              break;
-            }
-            const float v = gemv_unit(o, u, ring_s + stage * kGemvStageBytes, xs_s, lane);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (lane < gemv_unit_rows(o, u)) store_out(o, u * o.rows + lane, v, tag);
-            j += kGemvConsumers;
-          }
-        }
-        for (int u = gemv_first_unit(o, G); u < o.units && !p.dynamic; u += G, ++j) {
-          if (static_cast<int>(j % kGemvConsumers) != cw) continue;
+        // This warp's ring positions: cw, cw + S, ... (counted across ops).  The op ends for
+        // this warp at the first position holding a later op's unit (or the terminal entry):
+        // that stage is kept (not released) and consumed when the warp reaches that op.
+        for (;;) {
           const uint32_t stage = j % kGemvStages;
           mbar_wait(&full[stage], (j / kGemvStages) & 1);
+          const int2 meta = stage_meta[stage];
+          if (meta.x != oi) break;
+          const int u = meta.y;
           const float v = gemv_unit(o, u, ring_s + stage * kGemvStageBytes, xs_s, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[stage]);  // release the stage before any global store
           if (lane < gemv_unit_rows(o, u)) store_out(o, u * o.rows + lane, v, tag);
+          j += kGemvConsumers;
         }
       } else {
         gemv_elementwise(o, t, G, tag);

@@ -850,6 +850,10 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
     const char* e = getenv("MS_GEMV_DYNAMIC");  // A/B: 0 = static round-robin unit plan
     return e ? atoi(e) : 1;
   }();
+  p.claim_batch = [] {
+    const char* e = getenv("MS_GEMV_CLAIM_BATCH");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
   p.n_ops = static_cast<int>(ch.gemv_descs.size());
   p.ops = ch.gemv_descs_d;
   p.tag = (++ch.launches) & 0xFFFFu;

@@ -338,6 +338,19 @@ int ms_replay_run_opts(const char* scenario_json, const char* policy, const char
       for (const PreemptionRecord& p : art.preemptions) delays.push_back(json(static_cast<long long>(p.delay)));
       d["delays"] = std::move(delays);
     }
+    if (flags & MS_RUN_ROWS) {
+      json rows = json::array();
+      for (const RequestStat& r : art.requests) {
+        json e = json::array();
+        e.push_back(json(static_cast<long long>(r.arrival)));
+        e.push_back(json(static_cast<long long>(r.ttft())));
+        e.push_back(json(static_cast<long long>(r.tpot())));
+        e.push_back(json(r.iterations));
+        e.push_back(json(r.completed));
+        rows.push_back(std::move(e));
+      }
+      d["request_rows"] = std::move(rows);
+    }
     if (flags & MS_RUN_REPORT) {
       const RunArtifacts ex = run_scenario(sc, Policy::Exclusive, eo);
       const RunArtifacts exlp = run_scenario(sc, Policy::ExclusiveLp, eo);

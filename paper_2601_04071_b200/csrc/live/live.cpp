@@ -87,11 +87,10 @@ struct LpTask {
   Ns tile_ns = 50000;
 };
 
-int64_t mono_ns() {
-  timespec ts;
-  clock_gettime(CLOCK_MONOTONIC, &ts);
-  return static_cast<int64_t>(ts.tv_sec) * 1000000000ll + ts.tv_nsec;
-}
+// Host clock of the device layer (CLOCK_MONOTONIC; the ring / raise timestamps use the same
+// clock).  Taken through the C-ABI so a virtual-time model of the device layer can drive
+// this scheduler unchanged (tests/livemock, tests/test_live_decisions.py).
+int64_t mono_ns() { return ms_host_now_ns(); }
 
 class LiveRun {
  public:
@@ -276,6 +275,12 @@ class LiveRun {
     h.ring_t = t_ring - t0_;
     h.inflight = true;
     emit(h.ring_t, EventKind::Launch, h.index, h.spec->name, "seq=" + std::to_string(h.seq));
+    // Log order of the reference (engine.hpp:707-713): Launch, then PreemptBegin at the same
+    // instant — physically the flag was raised just before the ring.
+    if (preempt_emit_pending_) {
+      emit(h.ring_t, EventKind::PreemptBegin, -1, "");
+      preempt_emit_pending_ = false;
+    }
   }
 
   void hp_turned_active() {
@@ -287,7 +292,7 @@ class LiveRun {
     rec.begin = now_;
     rec.lp_in_flight = lp_running_;
     pending_preempt_ = rec;
-    emit(now_, EventKind::PreemptBegin, -1, "");
+    preempt_emit_pending_ = true;  // logged right after the segment's Launch (issue_segment)
     if (harvest_ && lp_running_ && !preempt_raised_) {
       int64_t t_raise = 0;
       check(ms_preempt_raise(dev_, nullptr, &t_raise), "ms_preempt_raise");
@@ -599,6 +604,7 @@ class LiveRun {
   std::vector<LpTask> lp_;
   int hp_active_ = 0;
   bool p_flag_ = false;
+  bool preempt_emit_pending_ = false;
   long generation_ = 0;
   int open_hint_ = -1;
   Ns last_hp_activity_ = 0, last_arrival_ = -1;

@@ -157,9 +157,9 @@ def generate_bursty_arrivals(rate: float, burstiness: float, horizon_ns: int, se
 
 
 def run_scenario(scenario, policy: str, ndjson: bool = False, report: bool = False,
-                 delays: bool = False, options: dict | None = None) -> dict:
+                 delays: bool = False, options: dict | None = None, rows: bool = False) -> dict:
     flags = (N.MS_RUN_NDJSON if ndjson else 0) | (N.MS_RUN_REPORT if report else 0) | \
-            (N.MS_RUN_DELAYS if delays else 0)
+            (N.MS_RUN_DELAYS if delays else 0) | (N.MS_RUN_ROWS if rows else 0)
     return N.replay_run(scenario, policy, flags, options)
 
 

@@ -243,7 +243,7 @@ def test_optimizer_streamer_bit_exact_preempted(dev, T, mode):
         dev.lp_run(k, begin, k.total_tiles)
         runs += 1
         if runs <= 2:
-            time.sleep(0.00005 * runs)
+            time.sleep(0.00002 * (runs - 1))  # first run: raised right after the launch
             dev.preempt_raise()
         st = dev.lp_wait(k, 60)
         begin = st["cursor"]
