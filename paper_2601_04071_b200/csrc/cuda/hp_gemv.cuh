@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
   const uint32_t ring_s = smem_u32(ring), xs_s = smem_u32(xs);
   __shared__ uint64_t full[kGemvStages], empty[kGemvStages], desc_bar;
   __shared__ int2 stage_meta[kGemvStages];  // (op, unit) loaded into each stage; op == n_ops: end
+  __shared__ uint32_t prod_pos;            // ring positions whose stage_meta is written (producer)
   // Op descriptors live in shared memory (one bulk copy from global at entry): dynamically
   // indexed kernel-parameter reads go through the constant cache, whose misses wait behind
   // the saturated memory system, and small parameters keep the launch itself short.
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
       mbar_init(&empty[i], 1);
     }
     mbar_init(&desc_bar, 1);
+    prod_pos = 0;
     fence_mbar_init();
     const uint32_t bytes = static_cast<uint32_t>(p.n_ops * sizeof(GemvOpDesc));
     mbar_arrive_expect_tx(&desc_bar, bytes);
@@ -424,6 +426,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
             const uint32_t st = pos % kGemvStages;
             mbar_wait(&empty[st], ((pos / kGemvStages) & 1) ^ 1);
             stage_meta[st] = make_int2(oi, u);
+            __threadfence_block();
+            st_volatile_smem(&prod_pos, pos + 1);  // consumers may read the meta before the data lands
             const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
             const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
             uint8_t* dst = ring + st * kGemvStageBytes;
@@ -447,6 +451,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         const uint32_t st = pos % kGemvStages;
         mbar_wait(&empty[st], ((pos / kGemvStages) & 1) ^ 1);
         stage_meta[st] = make_int2(p.n_ops, 0);
+        __threadfence_block();
+        st_volatile_smem(&prod_pos, pos + 1);
         mbar_arrive(&full[st]);
       }
     }
@@ -479,11 +485,15 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         // This warp's ring positions: cw, cw + S, ... (counted across ops).  The op ends for
         // this warp at the first position holding a later op's unit (or the terminal entry):
         // that stage is kept (not released) and consumed when the warp reaches that op.
+        // The producer publishes a position's (op, unit) before its data lands, so a warp
+        // learns that its op ended without waiting for the next op's weights to arrive.
         for (;;) {
           const uint32_t stage = j % kGemvStages;
-          mbar_wait(&full[stage], (j / kGemvStages) & 1);
-          const int2 meta = stage_meta[stage];
+          while (ld_volatile_smem(&prod_pos) <= j) __nanosleep(20);
+          const volatile int* mp = reinterpret_cast<volatile int*>(&stage_meta[stage]);
+          const int2 meta = make_int2(mp[0], mp[1]);
           if (meta.x != oi) break;
+          mbar_wait(&full[stage], (j / kGemvStages) & 1);
           const int u = meta.y;
           const float v = gemv_unit(o, u, ring_s + stage * kGemvStageBytes, xs_s, lane);
           __syncwarp();

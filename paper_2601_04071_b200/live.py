@@ -242,7 +242,10 @@ class _TrainInferConfig:
 
     HP_TASK = LP_TASK = NAME = ""
     RATE = 100.0
-    THRESHOLD_MS = 0.5  # large-bubble threshold (scheduler.threshold_ms): the gaps are a few ms
+    # Large-bubble threshold (the reference's scheduler.threshold_ms, default 2 ms): these HP
+    # tenants have no in-request hints, so LP runs only between requests; with a preemption
+    # that costs a few us there is no reason to let a gap of a few ms idle for 2 ms first.
+    THRESHOLD_MS = 0.02
 
     def _finish(self, dev: Device, hp, lp):
         self.dev, self.hp, self.lp = dev, hp, lp
