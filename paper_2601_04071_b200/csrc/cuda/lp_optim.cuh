@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(kAxpyGroups * kStreamThreads + 64, 1) optim_ke
     if ((threadIdx.x & 31) == 0 && q.run.preemptible) poll_mirror(q.run, &preempt, &producer_done);
   } else if (warp == kStreamWarps + 1) {
     if ((threadIdx.x & 31) == 0 && q.run.preemptible && blockIdx.x == 0) poll_host(q.run, &preempt, &producer_done);
+    if ((threadIdx.x & 31) == 0 && q.run.preemptible && blockIdx.x >= 1 && blockIdx.x <= kAuxPollers)
+      poll_host_aux(q.run, &preempt, &producer_done, 300u * blockIdx.x);
   } else {
     const int g = warp / (kStreamThreads / 32);
     const int tid = threadIdx.x % kStreamThreads;

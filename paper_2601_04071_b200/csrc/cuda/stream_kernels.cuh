@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(GROUPS * kStreamThreads + 64, GROUPS == 1 ? 4 
     if ((threadIdx.x & 31) == 0 && p.run.preemptible) poll_mirror(p.run, &preempt, &producer_done);
   } else if (warp == kStreamWarps + 1) {
     if ((threadIdx.x & 31) == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &preempt, &producer_done);
+    if ((threadIdx.x & 31) == 0 && p.run.preemptible && blockIdx.x >= 1 && blockIdx.x <= kAuxPollers)
+      poll_host_aux(p.run, &preempt, &producer_done, 300u * blockIdx.x);
   } else {
     const int g = warp / (kStreamThreads / 32);
     const int tid = threadIdx.x % kStreamThreads;

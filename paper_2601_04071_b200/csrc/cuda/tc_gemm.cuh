@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0 && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->producer_done);
   } else if (warp == 3) {
     if (lane == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &s->preempt, &s->producer_done);
+    if (lane == 0 && p.run.preemptible && blockIdx.x >= 1 && blockIdx.x <= kAuxPollers)
+      poll_host_aux(p.run, &s->preempt, &s->producer_done, 300u * blockIdx.x);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp - 4;  // TMEM lane quarter

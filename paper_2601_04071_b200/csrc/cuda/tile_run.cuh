@@ -129,6 +129,29 @@ __device__ __forceinline__ void poll_host(const TileRun& r, const uint32_t* pree
   }
 }
 
+// Auxiliary host pollers (CTAs 1 .. kAuxPollers of an LP grid, one otherwise idle lane
+// each): the same 16-byte ld.acquire.sys of {epoch, budget} as CTA 0's poller, started
+// `stagger` ns apart, forwarding only the epoch to the device mirror.  With P pollers a host
+// store is seen ~RTT/(2P) + RTT/2 after it lands instead of ~RTT (one PCIe round trip is
+// ~1.2 us here).  Each leaves with its own CTA (no cross-CTA wait).
+constexpr int kAuxPollers = 3;
+
+__device__ __forceinline__ void poll_host_aux(const TileRun& r, const uint32_t* preempt, const uint32_t* producer_done,
+                                              unsigned stagger_ns) {
+  __nanosleep(stagger_ns);
+  for (;;) {
+    if (ld_volatile_smem(preempt) || ld_volatile_smem(producer_done)) break;
+    uint64_t ep, bud;
+    ld_acquire_sys_v2(r.host_line, ep, bud);
+    const uint32_t e = static_cast<uint32_t>(ep);
+    if (e > r.run_epoch) {
+#pragma unroll
+      for (int c = 0; c < MS_MIRROR_COPIES; ++c) atomicMax(&r.mirror->epoch[c * MS_MIRROR_STRIDE], e);
+      break;
+    }
+  }
+}
+
 // Called by thread 0 of each CTA after all of the CTA's work (and TMEM traffic) is done.
 // One acq_rel atomic per CTA on MsLpCtl::top ((tiles << 32) | 1) publishes this CTA's
 // tile / redo accounting (ordered by the CTA barrier before cta_exit) and lets the last
