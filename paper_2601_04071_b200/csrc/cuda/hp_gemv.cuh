@@ -23,14 +23,16 @@
 //     measured ~2 us per op under full HBM load) is used only for inputs that are not
 //     produced in the chain.
 //   * units are dealt to CTAs round-robin on a counter that continues across ops, so each
-//     CTA's total byte count over the chain is balanced to within one unit (static mode), or
-//     (dynamic mode, default) each CTA's producer CLAIMS batches of units of the op from a
-//     per-op counter (the next batch's atomic in flight while the current one loads): a CTA
-//     that starts late (its SM still draining a preempted LP CTA when the doorbell fires)
-//     simply claims fewer units instead of holding back every later op by its start delay.
-//     The producer writes each stage's (op, unit) next to it; a consumer warp's op ends at
-//     the first of its positions that holds a later op's unit.  The L2 lookahead keeps the
-//     static unit plan (whichever CTA claims a prefetched unit finds it in L2).
+//     CTA's total byte count over the chain is balanced to within one unit (DYN = false), or
+//     (DYN = true) each CTA's producer CLAIMS batches of B units of the op from a per-op
+//     counter, so a CTA that starts late (its SM still draining a preempted LP CTA when the
+//     doorbell fires) takes fewer units instead of holding back every later op by its start
+//     delay.  The producer writes each stage's (op, unit) before arming its barrier and,
+//     once an op's claims run out, the ring position where the op ends in this CTA; a
+//     consumer warp leaves the op at that position (or, racing the producer, at a landed
+//     stage that holds a later op's unit).  The L2 lookahead keeps the static unit plan
+//     (whichever CTA claims a prefetched unit finds it in L2).  The two variants are
+//     separate instantiations: the static one is the round-1 code path unchanged.
 //
 // Per-unit algorithmic bytes = the unit's weight bytes (the vectors are L2-resident and
 // small).  Roofline: HBM (MEASURED_PEAKS.json hbm_gbs).
@@ -74,9 +76,8 @@ static_assert(sizeof(GemvOpDesc) % 16 == 0, "descriptors are bulk-copied (16-byt
 struct GemvParams {
   TileRun run;  // HP bookkeeping (first-CTA stamp, completion record, phase-counter reset)
   uint32_t* phase_cnt;  // [n_ops]: CTAs that finished op i
-  uint32_t* claim;      // [n_ops]: dynamic mode unit claim counters (reset by the last CTA)
-  int dynamic;          // 1: units claimed dynamically (default), 0: static round-robin
-  int claim_batch;      // dynamic: units per claim (one atomic per batch, the next in flight)
+  uint32_t* claim;      // [n_ops]: DYN unit-claim counters (reset by the last CTA)
+  int claim_batch;      // DYN: units per claim
   const GemvOpDesc* ops;  // [n_ops] in global memory (16-byte aligned), bulk-copied to smem
   int n_ops;
   uint32_t tag;  // this launch's wire tag (16 bits)
@@ -327,14 +328,16 @@ __device__ __forceinline__ void gemv_load_x(const GemvOpDesc& o, uint8_t* xs, in
           make_uint2((v[i].x & 0xFFFFu) | (v[i].y << 16), (v[i].z & 0xFFFFu) | (v[i].w << 16));
 }
 
+template <bool DYN>
 __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_constant__ GemvParams p) {
   extern __shared__ __align__(128) uint8_t gsm_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 127) & ~uintptr_t(127));
   uint8_t* xs = ring + kGemvStages * kGemvStageBytes;
   const uint32_t ring_s = smem_u32(ring), xs_s = smem_u32(xs);
   __shared__ uint64_t full[kGemvStages], empty[kGemvStages], desc_bar;
-  __shared__ int2 stage_meta[kGemvStages];  // (op, unit) loaded into each stage; op == n_ops: end
-  __shared__ uint32_t prod_pos;            // ring positions whose stage_meta is written (producer)
+  // DYN: (op, unit) in each stage, and where each op ends in this CTA's ring stream
+  __shared__ int2 stage_meta[DYN ? kGemvStages : 1];
+  __shared__ uint32_t op_end[DYN ? kGemvMaxOps : 1];
   // Op descriptors live in shared memory (one bulk copy from global at entry): dynamically
   // indexed kernel-parameter reads go through the constant cache, whose misses wait behind
   // the saturated memory system, and small parameters keep the launch itself short.
@@ -349,7 +352,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
       mbar_init(&empty[i], 1);
     }
     mbar_init(&desc_bar, 1);
-    prod_pos = 0;
     fence_mbar_init();
     const uint32_t bytes = static_cast<uint32_t>(p.n_ops * sizeof(GemvOpDesc));
     mbar_arrive_expect_tx(&desc_bar, bytes);
@@ -358,6 +360,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
                  "l"(p.ops), "r"(bytes), "r"(smem_u32(&desc_bar))
                  : "memory");
   }
+  if constexpr (DYN)
+    for (int i = threadIdx.x; i < kGemvMaxOps; i += blockDim.x) op_end[i] = 0xFFFFFFFFu;
   __syncthreads();
   mbar_wait(&desc_bar, 0);
   if (p.run.pdl_wait) pdl_wait();
@@ -397,63 +401,88 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         pf_seek(pf_oi, pf_u + G);
         return true;
       };
-      // Ring position `pos` (counted across ops) holds one unit; the unit's (op, id) is
-      // written next to the stage before the load is issued (the full-barrier completion
-      // publishes it).  Unit source: dynamic = batches of B units claimed from the op's
-      // counter, the next batch's atomic in flight while the current one is issued; static
-      // = every G-th unit from this CTA's round-robin start.
-      uint32_t pos = 0;
-      const int B = p.claim_batch;
-      for (int oi = 0; oi < p.n_ops; ++oi) {
+      for (int oi = 0; oi < p.n_ops && DYN; ++oi) {
         const GemvOpDesc& o = sops[oi];
         if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
         const size_t row_bytes = static_cast<size_t>(o.k) * 2;
-        int next = p.dynamic ? static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)))
-                             : gemv_first_unit(o, G);
+        const int B = p.claim_batch;
         for (;;) {
-          const int b0 = next;
+          const int b0 = static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)));
           if (b0 >= o.units) break;
-          const int b1 = p.dynamic ? min(b0 + B, o.units) : b0 + 1;
-          next = p.dynamic ? static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B))) : b0 + G;
-          for (int u = b0; u < b1; ++u, ++pos, ++issued) {
-            // Bound the loads in flight: a full 12-stage queue on every SM inflates HBM latency
-            // (and the op->op handoff traffic behind it); landed units may still fill the
-            // whole ring while the consumers wait for an op's input.
-            if (pos >= D) {
-              const uint32_t back = pos - D;
-              mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
-            }
-            const uint32_t st = pos % kGemvStages;
-            mbar_wait(&empty[st], ((pos / kGemvStages) & 1) ^ 1);
-            stage_meta[st] = make_int2(oi, u);
-            __threadfence_block();
-            st_volatile_smem(&prod_pos, pos + 1);  // consumers may read the meta before the data lands
+          for (int u = b0; u < min(b0 + B, o.units); ++u, ++issued) {
             const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
             const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
-            uint8_t* dst = ring + st * kGemvStageBytes;
+            if (issued >= D) {
+              const uint32_t back = issued - D;
+              mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
+            }
+            mbar_wait(&empty[stage], phase ^ 1);
+            stage_meta[stage] = make_int2(oi, u);  // published by the barrier's arrive (release)
+            uint8_t* dst = ring + stage * kGemvStageBytes;
             const uint8_t* src = reinterpret_cast<const uint8_t*>(o.w) + r0 * row_bytes;
             if (o.kind == kGemvSwiglu) {
-              mbar_arrive_expect_tx(&full[st], 2 * bytes);
-              bulk_load(dst, src, bytes, &full[st], pol);  // gate rows
-              bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[st], pol);
+              mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+              bulk_load(dst, src, bytes, &full[stage], pol);
+              bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[stage], pol);
             } else {
-              mbar_arrive_expect_tx(&full[st], bytes);
-              bulk_load(dst, src, bytes, &full[st], pol);
+              mbar_arrive_expect_tx(&full[stage], bytes);
+              bulk_load(dst, src, bytes, &full[stage], pol);
+            }
+            if (++stage == kGemvStages) {
+              stage = 0;
+              phase ^= 1;
             }
             while (pf_step()) {
-            }  // keep the L2 lookahead P units past the issue point
+            }
           }
         }
-        if (oi < 16) gemv_stamp(p.run, 48 + oi);  // last unit of op oi issued
+        st_volatile_smem(&op_end[oi], issued);  // op oi ends at ring position `issued` here
+        if (oi < 16) gemv_stamp(p.run, 48 + oi);
       }
-      // end of the chain: one terminal entry per consumer warp (no data)
-      for (int w = 0; w < kGemvConsumers; ++w, ++pos) {
-        const uint32_t st = pos % kGemvStages;
-        mbar_wait(&empty[st], ((pos / kGemvStages) & 1) ^ 1);
-        stage_meta[st] = make_int2(p.n_ops, 0);
-        __threadfence_block();
-        st_volatile_smem(&prod_pos, pos + 1);
-        mbar_arrive(&full[st]);
+      if constexpr (DYN) {  // end of the chain: one terminal entry per consumer warp (no data)
+        for (int w = 0; w < kGemvConsumers; ++w, ++issued) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          stage_meta[stage] = make_int2(p.n_ops, 0);
+          mbar_arrive(&full[stage]);
+          if (++stage == kGemvStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      for (int oi = 0; oi < p.n_ops && !DYN; ++oi) {
+        const GemvOpDesc& o = sops[oi];
+        if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
+        const size_t row_bytes = static_cast<size_t>(o.k) * 2;
+        for (int u = gemv_first_unit(o, G); u < o.units; u += G, ++issued) {
+          const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
+          const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);
+          // Bound the loads in flight: a full 12-stage queue on every SM inflates HBM latency
+          // (and the op->op handoff traffic behind it); landed units may still fill the
+          // whole ring while the consumers wait for an op's input.
+          if (issued >= D) {
+            const uint32_t back = issued - D;
+            mbar_wait(&full[back % kGemvStages], (back / kGemvStages) & 1);
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* dst = ring + stage * kGemvStageBytes;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(o.w) + r0 * row_bytes;
+          if (o.kind == kGemvSwiglu) {
+            mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+            bulk_load(dst, src, bytes, &full[stage], pol);  // gate rows
+            bulk_load(dst + o.rows * row_bytes, src + static_cast<size_t>(o.n) * row_bytes, bytes, &full[stage], pol);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            bulk_load(dst, src, bytes, &full[stage], pol);
+          }
+          if (++stage == kGemvStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+          while (pf_step()) {
+          }  // keep the L2 lookahead P units past the issue point
+        }
+        if (oi < 16) gemv_stamp(p.run, 48 + oi);  // last unit of op oi issued
       }
     }
   } else {
@@ -464,7 +493,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
     // phase ahead of a stage another warp has not released: mbarrier parity ABA).
     const int cw = warp - 1;
     const int t = threadIdx.x - 32;  // 0..255
-    uint32_t j = static_cast<uint32_t>(cw);  // this warp's next ring position
+    uint32_t j = DYN ? static_cast<uint32_t>(cw) : 0u;  // DYN: this warp's next ring position
     const uint32_t tag = p.tag;
     for (int oi = 0; oi < p.n_ops; ++oi) {
       const GemvOpDesc& o = sops[oi];
@@ -482,24 +511,29 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(g) : "r"(xs_s) : "memory");
           if (g != 0x7FEDCBA9u) p.run.dbg[2048 + 148 * 64 + blockIdx.x * 16 + oi] = globaltimer();
         }
-        // This warp's ring positions: cw, cw + S, ... (counted across ops).  The op ends for
-        // this warp at the first position holding a later op's unit (or the terminal entry):
-        // that stage is kept (not released) and consumed when the warp reaches that op.
-        // The producer publishes a position's (op, unit) before its data lands, so a warp
-        // learns that its op ended without waiting for the next op's weights to arrive.
-        for (;;) {
+        if constexpr (DYN) {
+          for (;;) {
+            if (j >= ld_volatile_smem(&op_end[oi])) break;  // the producer knows where op oi ends
+            const uint32_t stage = j % kGemvStages;
+            mbar_wait(&full[stage], (j / kGemvStages) & 1);
+            const int2 meta = stage_meta[stage];
+            if (meta.x != oi) break;  // (raced the producer: a later op's unit, kept for that op)
+            const int u = meta.y;
+            const float v = gemv_unit(o, u, ring_s + stage * kGemvStageBytes, xs_s, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (lane < gemv_unit_rows(o, u)) store_out(o, u * o.rows + lane, v, tag);
+            j += kGemvConsumers;
+          }
+        }
+        for (int u = gemv_first_unit(o, G); u < o.units && !DYN; u += G, ++j) {
+          if (static_cast<int>(j % kGemvConsumers) != cw) continue;
           const uint32_t stage = j % kGemvStages;
-          while (ld_volatile_smem(&prod_pos) <= j) __nanosleep(20);
-          const volatile int* mp = reinterpret_cast<volatile int*>(&stage_meta[stage]);
-          const int2 meta = make_int2(mp[0], mp[1]);
-          if (meta.x != oi) break;
           mbar_wait(&full[stage], (j / kGemvStages) & 1);
-          const int u = meta.y;
           const float v = gemv_unit(o, u, ring_s + stage * kGemvStageBytes, xs_s, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[stage]);  // release the stage before any global store
           if (lane < gemv_unit_rows(o, u)) store_out(o, u * o.rows + lane, v, tag);
-          j += kGemvConsumers;
         }
       } else {
         gemv_elementwise(o, t, G, tag);

@@ -109,7 +109,8 @@ int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint6
 }
 
 constexpr int kRedoCap = 8192;
-constexpr int kMaxChainOps = 512;  // per-op chains (config-2 ResNet-50: ~160 ops); fused / GEMV plans are shorter
+constexpr int kMaxChainOps = 512;
+constexpr bool kGemvDynamicDefault = false;  // decided by tools/gemv_dynamic_ab.py  // per-op chains (config-2 ResNet-50: ~160 ops); fused / GEMV plans are shorter
 
 // FFI callers may pass any id: every entry point that indexes a slot checks it first.
 #define MS_CHECK_LP(d, id) \
@@ -231,7 +232,8 @@ int set_smem_attrs() {
                                FusedCfg<4>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_fused_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                FusedCfg<1, 32>::kSmemBytes));
-  MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
@@ -846,9 +848,9 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
   p.run.n_reset = ch.n_phases;
   p.phase_cnt = ch.phase_d;
   p.claim = ch.phase_d + ch.gemv_descs.size();
-  p.dynamic = [] {
-    const char* e = getenv("MS_GEMV_DYNAMIC");  // A/B: 0 = static round-robin unit plan
-    return e ? atoi(e) : 1;
+  const bool dynamic = [] {
+    const char* e = getenv("MS_GEMV_DYNAMIC");  // 1: units claimed per op (hp_gemv_kernel<true>)
+    return e ? atoi(e) != 0 : kGemvDynamicDefault;
   }();
   p.claim_batch = [] {
     const char* e = getenv("MS_GEMV_CLAIM_BATCH");
@@ -868,7 +870,10 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
     return e ? std::max(0, atoi(e)) : 16;
   }();
   p.prefetch = prefetch;
-  MS_CUDA(launch_kc(hp_gemv_kernel, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
+  if (dynamic)
+    MS_CUDA(launch_kc(hp_gemv_kernel<true>, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
+  else
+    MS_CUDA(launch_kc(hp_gemv_kernel<false>, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
   return 0;
 }
 

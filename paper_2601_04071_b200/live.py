@@ -86,9 +86,12 @@ class Config1:
     def binding(self, e2e: bool = False) -> dict:
         return {"lp": {"lp_gemm_8192": self.lp.id}, "hp": {"hp_infer": [self.chain_e2e if e2e else self.chain]}}
 
-    def calibrate(self, reps: int = 5) -> dict:
+    def calibrate(self, reps: int = 5, profile: bool = True) -> dict:
         """Measured per-tile / per-chain times feeding both the live pacing and the replay
-        scenario (KernelSpec calibrated from the B200 kernels)."""
+        scenario (KernelSpec calibrated from the B200 kernels).  `profile`:
+        also the on-B200 profile of the LP GEMM over tile prefixes (profiler.py), which the
+        scenario carries as KernelSpec.measured_time — the reference's measured execution
+        oracle for split plans (engine.hpp:461-481, splitter.hpp:141-207)."""
         ms_gemm = self.dev.lp_time_full(self.lp, reps)
         waves = math.ceil(self.lp.total_tiles / self.dev.info["sm_count"])
         ms_chain = self.dev.hp_time_chain(self.chain, 20)
@@ -101,6 +104,12 @@ class Config1:
             "hp_gemm_tile_ns": int(ms_chain * 1e6 * 0.95 / 4),
             "hp_ew_tile_ns": max(1000, int(ms_chain * 1e6 * 0.05)),
         }
+        if profile:
+            from . import profiler
+            sm = self.dev.info["sm_count"]
+            spec = profiler.profile_lp_kernel(self.dev, self.lp, "lp_gemm_8192", sm - 1,
+                                              scenarios.DEFAULT_CALIB["lp_gemm_tile_bytes"], reps=2)
+            self.calib["lp_gemm_measured_time"] = spec["measured_time"]
         return self.calib
 
     def scenario(self, seed: int, horizon_s: float) -> dict:
@@ -215,6 +224,13 @@ class Config4:
             "hp_layer_ns": int(ms_chain * 1e6 * 0.79 / self.LAYERS),
             "hp_lm_head_ns": int(ms_chain * 1e6 * 0.21),
         }
+        # on-B200 profiles -> KernelSpec.measured_time of both LP kernels (profiler.py)
+        from . import profiler
+        self.calib["lp_gemm_measured_time"] = profiler.profile_lp_kernel(
+            self.dev, self.lp_gemm, "lp_gemm_8192", sm - 1, scenarios.DEFAULT_CALIB["lp_gemm_tile_bytes"],
+            reps=1)["measured_time"]
+        self.calib["lp_ew_measured_time"] = profiler.profile_lp_kernel(
+            self.dev, self.lp_axpy, "lp_axpy_1g", 3 * (sm - 1), 6 * 8192, reps=1)["measured_time"]
         return self.calib
 
     def hp_rate(self, utilisation: float = 0.5) -> float:

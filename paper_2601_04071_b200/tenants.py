@@ -310,13 +310,16 @@ def step_plan(prefix: str, gemms: list[tuple[str, int, int, int]], optim_mode: i
     return {nm: shp for shp, nm in shapes.items()}, sequence, optim_name
 
 
-def kernel_spec(name: str, tiles: int, tile_ns: int, tile_bytes: int, per_sm: int = 1) -> dict:
+def kernel_spec(name: str, tiles: int, tile_ns: int, tile_bytes: int, per_sm: int = 1, measured_time=None) -> dict:
     """Reference-schema KernelSpec (scenario_io.hpp) of a persistent preemptible LP kernel:
     grid = tile count, one CTA per SM (tpb 256, occupancy per_sm/8 -> Eq. 1 = 148 * per_sm),
     block_time = per-wave tile time, bandwidth = the tile's compulsory bytes / tile time."""
-    return {"name": name, "grid": [int(tiles), 1, 1], "threads_per_block": 256, "occupancy": per_sm / 8.0,
-            "block_time": {"dist": "point", "value": {"value": int(tile_ns), "unit": "ns"}},
-            "bw_demand_per_block": float(tile_bytes) / (tile_ns * 1e-9), "splittable": True}
+    k = {"name": name, "grid": [int(tiles), 1, 1], "threads_per_block": 256, "occupancy": per_sm / 8.0,
+         "block_time": {"dist": "point", "value": {"value": int(tile_ns), "unit": "ns"}},
+         "bw_demand_per_block": float(tile_bytes) / (tile_ns * 1e-9), "splittable": True}
+    if measured_time:  # on-B200 profile rows -> the reference's measured oracle (engine.hpp:461-481)
+        k["measured_time"] = measured_time
+    return k
 
 
 def gemm_tiles(m: int, n: int) -> int:
@@ -328,19 +331,21 @@ def gemm_tile_bytes(n: int, k: int) -> int:
     return (128 + bn) * k * 2 + 128 * bn * 2
 
 
-def step_specs(prefix: str, gemms, n_params: int, optim_mode: int, tile_ns: dict | None = None) -> tuple:
+def step_specs(prefix: str, gemms, n_params: int, optim_mode: int, tile_ns: dict | None = None,
+               measured: dict | None = None) -> tuple:
     """(specs, sequence) of a training step without a device (tile times default to a
     roofline estimate at 1300 TFLOP/s / 6.5 TB/s over 147 SMs)."""
     shapes, sequence, optim_name = step_plan(prefix, gemms, optim_mode)
-    tile_ns = tile_ns or {}
+    tile_ns, measured = tile_ns or {}, measured or {}
     specs = []
     for nm, (m, n, k) in shapes.items():
         est = int(2 * 128 * block_n_for(n) * k / (1300e12 / 147) * 1e9)
-        specs.append(kernel_spec(nm, gemm_tiles(m, n), tile_ns.get(nm, max(500, est)), gemm_tile_bytes(n, k)))
+        specs.append(kernel_spec(nm, gemm_tiles(m, n), tile_ns.get(nm, max(500, est)), gemm_tile_bytes(n, k),
+                                 measured_time=measured.get(nm)))
     ob = 26 if optim_mode == 0 else 18
     est = int(ob * 4096 * 3 / (6.5e12 / 147) * 1e9)
     specs.append(kernel_spec(optim_name, (pad_to(n_params, 4) + 4095) // 4096, tile_ns.get(optim_name, est),
-                             ob * 4096 * 3))
+                             ob * 4096 * 3, measured_time=measured.get(optim_name)))
     return specs, sequence
 
 
@@ -390,6 +395,7 @@ class TrainStepLP:
                                                                   self.opt_bufs[3], np_, mode=1, lr=0.1, beta1=0.9,
                                                                   wd=1e-4)
         self.tile_ns: dict[str, int] = {}
+        self.measured: dict[str, list] = {}
 
     def binding(self) -> dict:
         return {nm: k.id for nm, k in self.kernels.items()}
@@ -402,8 +408,14 @@ class TrainStepLP:
         for nm, k in self.kernels.items():
             ms = self.dev.lp_time_full(k, reps)
             self.ms[nm] = ms
-            waves = math.ceil(k.total_tiles / (sm if nm != self.optim_name else 3 * sm))
+            resident = sm if nm != self.optim_name else 3 * sm
+            waves = math.ceil(k.total_tiles / resident)
             self.tile_ns[nm] = max(500, int(ms * 1e6 / max(1, waves)))
+            # two-point on-B200 profile (one wave, whole kernel) -> KernelSpec.measured_time
+            rows = [(k.total_tiles, int(ms * 1e6))]
+            if k.total_tiles > resident:
+                rows.insert(0, (resident, int(self.dev.lp_time_range(k, 0, resident, 1) * 1e6)))
+            self.measured[nm] = [{"n_blocks": int(n), "time": {"value": max(1, t), "unit": "ns"}} for n, t in rows]
         self.step_ms = sum(self.ms[nm] * r for nm, r in self.sequence)
         return {"step_ms": self.step_ms, "kernels": len(self.kernels), "gemm_tflop_per_step": self.flops / 1e12,
                 "gemm_tflops": self.flops / (sum(self.ms[nm] * r for nm, r in self.sequence
@@ -412,7 +424,7 @@ class TrainStepLP:
     def kernel_specs(self) -> list[dict]:
         """Reference-schema KernelSpecs of the step's kernels with the measured tile times
         (grids = this device's tile counts)."""
-        specs, _ = step_specs(self.prefix, self.gemms, self.n_params, self.optim_mode, self.tile_ns)
+        specs, _ = step_specs(self.prefix, self.gemms, self.n_params, self.optim_mode, self.tile_ns, self.measured)
         for sp in specs:
             assert sp["grid"][0] == self.kernels[sp["name"]].total_tiles, sp["name"]
         return specs
