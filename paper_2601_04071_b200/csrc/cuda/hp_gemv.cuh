@@ -406,9 +406,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
         const size_t row_bytes = static_cast<size_t>(o.k) * 2;
         const int B = p.claim_batch;
+        int next = static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)));
         for (;;) {
-          const int b0 = static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)));
+          const int b0 = next;
           if (b0 >= o.units) break;
+          // the next batch's claim is in flight while this batch's stages are waited for
+          next = static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)));
           for (int u = b0; u < min(b0 + B, o.units); ++u, ++issued) {
             const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
             const uint32_t bytes = static_cast<uint32_t>(nr * row_bytes);

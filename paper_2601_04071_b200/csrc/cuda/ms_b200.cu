@@ -752,7 +752,13 @@ int plan_gemv(ms_dev* d, HpChain& ch) {
     if (is_copy(ch.ops[i].op)) return fail(MS_E_ARG, "batch-1 chains: copies only before/after the kernel ops");
   if (last - first + 1 > kGemvMaxOps) return fail(MS_E_ARG, "batch-1 chain too long");
   ch.gemv_descs.clear();
-  const int grid = d->prop.multiProcessorCount - 1;
+  // Grid: SMs - 1 (one SM stays free for the doorbell gate), or MS_GEMV_GRID (A/B: a smaller
+  // chain starts once that many SMs are free instead of waiting for the last LP CTA to drain)
+  const int grid = [&] {
+    const char* e = getenv("MS_GEMV_GRID");
+    const int g = e ? atoi(e) : 0;
+    return g > 0 && g < d->prop.multiProcessorCount ? g : d->prop.multiProcessorCount - 1;
+  }();
   int64_t unit_ctr = 0;
   for (int i = first; i <= last; ++i) {
     const ms_hp_op& op = ch.ops[i].op;
