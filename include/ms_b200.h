@@ -86,7 +86,10 @@ typedef struct ms_lp_desc {
   int32_t ctas_per_sm;/* AXPY layout: 1 (default, 0) = ONE CTA per SM with 3 x 256 streaming
                          threads, so a capped grid leaves whole SMs free for HP; 2..4 = that
                          many 256-thread CTAs per SM (the block scheduler spreads them) */
-  int32_t pad;
+  int32_t split_k;    /* GEMM: k-slices per output tile (0/1: none).  Work unit = (tile, slice):
+                         fp32 partials, the tile's last unit reduces them in slice order
+                         (deterministic).  Bounds a unit's duration (the preemption grain) and
+                         fills the GPU when a GEMM has few tiles and a long K (wgrad) */
   uint64_t a, b, c;
   int64_t m, n, k;
   uint64_t x, y;

@@ -133,6 +133,9 @@ struct LpSlot {
   uint64_t last_begin = 0, last_end = 0, last_redo_in = 0;
   int64_t t_launch_host = 0;
   bool launched = false;
+  int split = 1;                    // GEMM k-slices per tile (units = tiles x split)
+  float* ws = nullptr;              // split-K fp32 partials [tiles][split][128 x BN]
+  unsigned int* tile_cnt = nullptr; // split-K: slices finished per tile (self-resetting)
   uint8_t* slow = nullptr;          // streamer off-device tile groups (ms_lp_set_slow_tiles)
   unsigned int* slow_sem = nullptr;
   int slow_group = 0, slow_max = 0;
@@ -1117,7 +1120,16 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     const int tm = s.pair ? 256 : kBM;
     s.tiles_m = static_cast<int>(desc->m / tm);
     s.tiles_n = static_cast<int>(desc->n / bn);
-    s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n;
+    s.split = desc->split_k > 1 ? desc->split_k : 1;
+    if (s.split > 1) {
+      if (s.pair) return fail(MS_E_ARG, "split_k is not supported on CTA pairs");
+      if ((desc->k / kBK) % s.split) return fail(MS_E_ARG, "split_k must divide K / 64");
+      const size_t tiles = static_cast<size_t>(s.tiles_m) * s.tiles_n;
+      MS_CUDA(cudaMalloc(&s.ws, sizeof(float) * tiles * s.split * kBM * bn));
+      MS_CUDA(cudaMalloc(&s.tile_cnt, sizeof(unsigned int) * tiles));
+      MS_CUDA(cudaMemset(s.tile_cnt, 0, sizeof(unsigned int) * tiles));
+    }
+    s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n * s.split;
     if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
     if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, s.pair ? 128 : bn)) return rc;
     if (int rc = encode_c(&s.tma_c, reinterpret_cast<void*>(desc->c), desc->m, desc->n)) return rc;
@@ -1157,6 +1169,8 @@ int ms_lp_unregister(ms_dev* d, int id) {
   }
   if (s.slow) cudaFree(s.slow);
   if (s.slow_sem) cudaFree(s.slow_sem);
+  if (s.ws) cudaFree(s.ws);
+  if (s.tile_cnt) cudaFree(s.tile_cnt);
   const uint64_t keep_run_id = s.run_id;  // run ids stay monotonic per slot (exit records)
   s = LpSlot{};
   s.run_id = keep_run_id;
@@ -1230,6 +1244,9 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.tiles_n = s.tiles_n;
     p.group_m = s.desc.group_m ? s.desc.group_m : 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(s.desc.c);
+    p.split_k = s.split;
+    p.ws = s.ws;
+    p.tile_cnt = s.tile_cnt;  // the tile's last unit reduces the slices in-kernel
     const int mma_lag = [] {  // read per launch (A/B probes flip it in-process)
       const char* e = getenv("MS_LP_MMA_LAG");
       // default 2: unbounded is +2.5% TFLOP/s alone (profiles/r01_mma_lag_ab.json) but under the
@@ -1447,6 +1464,10 @@ int ms_lp_reset(ms_dev* d, int id) {
   s.redo_carry = 0;
   // The last exit record is consumed: a later ms_lp_poll must not restore its carry.
   s.launched = false;
+  // A fresh pass: slices of half-finished split-K tiles from an abandoned pass must not
+  // count towards the new pass's reductions.
+  if (s.tile_cnt)
+    MS_CUDA(cudaMemsetAsync(s.tile_cnt, 0, sizeof(unsigned int) * s.tiles_m * s.tiles_n, d->lp));
   return 0;
 }
 

@@ -29,7 +29,7 @@ class DevInfo(C.Structure):
 
 class LpDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("group_m", C.c_int32),
-                ("tile_elems", C.c_int32), ("ctas_per_sm", C.c_int32), ("pad", C.c_int32),
+                ("tile_elems", C.c_int32), ("ctas_per_sm", C.c_int32), ("split_k", C.c_int32),
                 ("a", C.c_uint64), ("b", C.c_uint64), ("c", C.c_uint64),
                 ("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64),
                 ("x", C.c_uint64), ("y", C.c_uint64), ("alpha", C.c_float), ("pad2", C.c_float),
@@ -200,8 +200,11 @@ class Device:
 
     # ---- LP
     def lp_register_gemm(self, a: int, b: int, c: int, m: int, n: int, k: int, block_n: int = 256,
-                         group_m: int = 16) -> LpKernel:
-        d = LpDesc(kind=MS_LP_GEMM, block_n=block_n, group_m=group_m, a=a, b=b, c=c, m=m, n=n, k=k)
+                         group_m: int = 16, split_k: int = 1) -> LpKernel:
+        """split_k > 1: work unit = (tile, k-slice), the tile's last unit reduces the fp32
+        partials in slice order (total_tiles counts units)."""
+        d = LpDesc(kind=MS_LP_GEMM, block_n=block_n, group_m=group_m, a=a, b=b, c=c, m=m, n=n, k=k,
+                   split_k=split_k)
         return self._lp_register(d)
 
     def lp_register_axpy(self, x: int, y: int, n_elems: int, alpha: float, tile_elems: int = 8192,

@@ -326,6 +326,19 @@ def gemm_tiles(m: int, n: int) -> int:
     return (m // 128) * (n // block_n_for(n))
 
 
+def split_for(m: int, n: int, k: int, sms: int = 147, max_unit_kb: int = 64, min_unit_kb: int = 8) -> int:
+    """k-slices per tile of an LP training GEMM: enough units to fill the GPU when the GEMM
+    has few tiles and a long K (the wgrad GEMMs reduce over the whole batch: K up to 802,816),
+    and no unit longer than `max_unit_kb` k-blocks (the preemption grain: 128 x 256 x 4096
+    bf16 is ~30 us on one SM).  A power of two dividing K / 64."""
+    kb, tiles = k // 64, gemm_tiles(m, n)
+    split = 1
+    while kb % (2 * split) == 0 and kb // (2 * split) >= min_unit_kb and (
+            tiles * split < sms or kb // split > max_unit_kb):
+        split *= 2
+    return split
+
+
 def gemm_tile_bytes(n: int, k: int) -> int:
     bn = block_n_for(n)
     return (128 + bn) * k * 2 + 128 * bn * 2
@@ -339,9 +352,10 @@ def step_specs(prefix: str, gemms, n_params: int, optim_mode: int, tile_ns: dict
     tile_ns, measured = tile_ns or {}, measured or {}
     specs = []
     for nm, (m, n, k) in shapes.items():
-        est = int(2 * 128 * block_n_for(n) * k / (1300e12 / 147) * 1e9)
-        specs.append(kernel_spec(nm, gemm_tiles(m, n), tile_ns.get(nm, max(500, est)), gemm_tile_bytes(n, k),
-                                 measured_time=measured.get(nm)))
+        sp = split_for(m, n, k)
+        est = int(2 * 128 * block_n_for(n) * (k // sp) / (1300e12 / 147) * 1e9)
+        specs.append(kernel_spec(nm, gemm_tiles(m, n) * sp, tile_ns.get(nm, max(500, est)),
+                                 gemm_tile_bytes(n, k // sp), measured_time=measured.get(nm)))
     ob = 26 if optim_mode == 0 else 18
     est = int(ob * 4096 * 3 / (6.5e12 / 147) * 1e9)
     specs.append(kernel_spec(optim_name, (pad_to(n_params, 4) + 4095) // 4096, tile_ns.get(optim_name, est),
@@ -372,7 +386,7 @@ class TrainStepLP:
         self.flops = 0
         for (m, n, k), nm in shapes.items():
             self.kernels[nm] = dev.lp_register_gemm(self.scratch[0], self.scratch[1], self.scratch[2], m, n, k,
-                                                     block_n=block_n_for(n))
+                                                     block_n=block_n_for(n), split_k=split_for(m, n, k))
             self.shape[nm] = (m, n, k)
         for _, m, n, k in gemms:
             self.flops += 2 * m * n * k

@@ -292,3 +292,47 @@ def test_live_short(cfg):
            ring_p99_us=sk["ring_to_first_hp_cta_all"].get("p99_ns", 0) / 1e3)
     w.close()
     dev.close()
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 192, 802816), (256, 2304, 12544), (768, 768, 4096)])
+def test_lp_gemm_split_k_preempt_resume(dev, T, m, n, k):
+    """LP GEMMs with k-slices (the training steps' wgrad shapes: few tiles, long K): units =
+    (tile, slice), fp32 partials reduced in slice order by the tile's last unit.  Preempted
+    repeatedly and resumed from the cursor + redo list, the result is bit-identical to the
+    uninterrupted run, and matches the oracle on sampled rows."""
+    from paper_2601_04071_b200.tenants import block_n_for, split_for
+    sp = split_for(m, n, k)
+    assert sp > 1
+    a, b, c = dev.alloc(m * k * 2), dev.alloc(n * k * 2), dev.alloc(m * n * 2)
+    s = float(np.float32(1 / math.sqrt(k)))
+    dev.fill_synth(a, m * k, SEED, 31, 1.0)
+    dev.fill_synth(b, n * k, SEED, 32, s)
+    kern = dev.lp_register_gemm(a, b, c, m, n, k, block_n=block_n_for(n), split_k=sp)
+    assert kern.total_tiles == (m // 128) * (n // block_n_for(n)) * sp
+    dev.lp_run(kern, 0, kern.total_tiles)
+    dev.lp_wait(kern, 60)
+    ref = d2h(dev, c, m * n)
+    dev.memset(c, 0, m * n * 2)
+    dev.lp_reset(kern)
+    begin, runs = 0, 0
+    while True:
+        dev.lp_run(kern, begin, kern.total_tiles)
+        runs += 1
+        time.sleep(0.00003)
+        dev.preempt_raise()
+        st = dev.lp_wait(kern, 60)
+        begin = st["cursor"]
+        if begin >= kern.total_tiles and st["redo_count"] == 0:
+            break
+        assert runs < 5000
+    assert runs > 1
+    assert np.array_equal(d2h(dev, c, m * n), ref)
+    rows = sorted({t * 128 + (t * 29) % 128 for t in range(m // 128)})[:16]
+    want = T.gemm_rows(T.synth_bf16(m * k, SEED, 31, 1.0), T.synth_bf16(n * k, SEED, 32, s), rows, n, k)
+    got = T.bf16_to_f32(ref.reshape(m, n)[rows].reshape(-1)).reshape(len(rows), n)
+    nw, ew = errs(got, want)
+    record(f"lp_split_gemm_{m}x{n}x{k}", split=sp, runs=runs, normwise=nw, elementwise=ew)
+    assert nw <= 1e-2 and ew <= 2e-2 * max(1.0, math.sqrt(k / 65536)), (nw, ew)
+    dev.lp_unregister(kern)
+    for p_ in (a, b, c):
+        dev.free(p_)
