@@ -318,7 +318,7 @@ def test_lp_gemm_split_k_preempt_resume(dev, T, m, n, k):
     while True:
         dev.lp_run(kern, begin, kern.total_tiles)
         runs += 1
-        time.sleep(0.00003)
+        time.sleep(0.00001 * (runs % 3))  # raised right after the launch, or 10 / 20 us into the run
         dev.preempt_raise()
         st = dev.lp_wait(kern, 60)
         begin = st["cursor"]
