@@ -286,11 +286,11 @@ CFG4_WORKLOAD = ("cfg4 (BASELINE configs[3]): HP Llama-3.2-1B-geometry bs=1 deco
                  "80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 axpy streamer; governed")
 
 
-CFG2_WORKLOAD = ("cfg2 (BASELINE configs[1]): HP ResNet-50 bs=1 224x224 inference (130-op chain: im2col + tcgen05 "
-                 "conv GEMMs + bias/ReLU/residual + pools + FC), Poisson; LP ResNet-50 bs=64 training step (161 "
-                 "GEMMs fwd/dgrad/wgrad, 48 shapes, + SGD-momentum 25.6 M params); governed")
-CFG3_WORKLOAD = ("cfg3 (BASELINE configs[2]): HP BERT-base bs=1 seq-128 encoder (96-op chain), Poisson; LP BERT-base "
-                 "bs=32 training step (144 GEMMs, 9 shapes, + AdamW 110 M params); governed")
+CFG2_WORKLOAD = ("cfg2 (BASELINE configs[1]): HP ResNet-50 bs=1 224x224 inference (76-op chain: im2col + tcgen05 "
+                 "conv GEMMs with bias/residual/ReLU epilogues + pools + FC), Poisson; LP ResNet-50 bs=64 training "
+                 "step (161 GEMMs fwd/dgrad/wgrad, 48 shapes, split-K, + SGD-momentum 25.6 M params); governed")
+CFG3_WORKLOAD = ("cfg3 (BASELINE configs[2]): HP BERT-base bs=1 seq-128 encoder (84-op chain), Poisson; LP BERT-base "
+                 "bs=32 training step (144 GEMMs, 9 shapes, split-K, + AdamW 110 M params); governed")
 
 
 # ----------------------------------------------------------------------------- host facts

@@ -196,6 +196,10 @@ typedef struct ms_hp_op {
   int64_t lda;       /* GEMM: row stride of a in elements (0: k) — e.g. a column slice of a wider
                         activation */
   ms_hp_geo geo;     /* IM2COL / MAXPOOL / AVGPOOL geometry, BIAS_ACT flags (zero otherwise) */
+  uint64_t resid;    /* MS_HP_GEMM epilogue (per-op chains, m >= 128): C = act(A B^T + bias[col] + resid),
+                        bias != 0 adds a per-column bf16 bias, resid != 0 an [m x n] bf16 residual,
+                        geo.flags bit 0 = ReLU, bit 1 = tanh-GELU; applied to the fp32 accumulators
+                        (one rounding) — the folded-BN / residual / activation of a conv, FFN1 + GELU */
 } ms_hp_op;
 
 typedef struct ms_hp_times {

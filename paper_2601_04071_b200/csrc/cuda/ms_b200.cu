@@ -480,8 +480,16 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
     p.tiles_n = o.tiles_n;
     p.group_m = 16;
     p.c = reinterpret_cast<__nv_bfloat16*>(o.op.c);
+    const __nv_bfloat16* e_bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
+    const __nv_bfloat16* e_resid = reinterpret_cast<const __nv_bfloat16*>(o.op.resid);
+    const int e_act = (o.op.geo.flags & 1) ? 1 : (o.op.geo.flags & 2) ? 2 : 0;
     const int grid = static_cast<int>(std::min<uint64_t>(p.run.end, d->prop.multiProcessorCount));
-    if (o.split == 1) return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, o.tma_c, p, grid, d->hp, prev_is_kernel);
+    if (o.split == 1) {
+      p.bias = e_bias;
+      p.resid = e_resid;
+      p.act = e_act;
+      return launch_gemm(d, o.op.block_n, o.tma_a, o.tma_b, o.tma_c, p, grid, d->hp, prev_is_kernel);
+    }
     // split-K: the GEMM streams partials; the reduce kernel carries the chain's last-op role
     const bool last = p.run.hp_last;
     p.run.hp_last = 0;
@@ -504,6 +512,9 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
     rp.bn = o.op.block_n;
     rp.split = o.split;
     rp.total = static_cast<long long>(o.tiles_m) * o.tiles_n * (o.op.block_n / 4) * kBM;
+    rp.bias = e_bias;
+    rp.resid = e_resid;
+    rp.act = e_act;
     const int rgrid = static_cast<int>(std::min<long long>((rp.total + 255) / 256, 2ll * d->prop.multiProcessorCount));
     MS_CUDA(launch_k(splitk_reduce_kernel, rgrid, 256, 0, d->hp, true, rp));
     return 0;
@@ -538,6 +549,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
     const ms_hp_op& op = ch.ops[i].op;
     if (is_copy(op)) return 0;  // copies between kernels: keep per-op launches
     if (is_glue(op.kind)) return 0;
+    if (op.kind == MS_HP_GEMM && (op.bias || op.resid || op.geo.flags)) return 0;  // epilogue: per-op path
     if (last - first + 1 > kFusedMaxOps) return 0;
     if (op.kind == MS_HP_GEMM && (op.m % kBM || op.n % 32 || op.k % kBK)) return 0;
     if (op.kind == MS_HP_GEMM && op.n % kFusedBN && !(op.m == kBM && d->hp_fused == 1)) return 0;
@@ -1503,6 +1515,8 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
     if ((ops[i].kind == MS_HP_BIAS_GELU || ops[i].kind == MS_HP_SILU_MUL) && ops[i].m != 1)
       return fail(MS_E_ARG, "batch-1 chain: elementwise ops must have m == 1");
     if (is_glue(ops[i].kind)) return fail(MS_E_ARG, "batch-1 chain: conv / attention glue ops need m >= 16 rows");
+    if (ops[i].kind == MS_HP_GEMM && ops[i].m == 1 && (ops[i].bias || ops[i].resid || ops[i].geo.flags))
+      return fail(MS_E_ARG, "batch-1 chain: GEMM epilogues are not supported (use BIAS_GELU / SILU_MUL ops)");
   }
   if (any_gemv && n_ops > kGemvMaxOps) return fail(MS_E_ARG, "batch-1 chain too long");
   HpChain ch;
@@ -1520,6 +1534,8 @@ int ms_hp_register_chain(ms_dev* d, const ms_hp_op* ops, int n_ops, int* chain_i
       o.gemv = true;
       o.split = 1;
     } else if (o.op.kind == MS_HP_GEMM) {
+      if ((o.op.bias % 16) || (o.op.resid % 16) || ((o.op.geo.flags & 3) == 3) || (o.op.resid && o.op.n % 8))
+        return fail(MS_E_ARG, "HP GEMM epilogue: 16-byte aligned bias / resid, one activation");
       const int bn = o.op.block_n ? o.op.block_n : 128;
       o.op.block_n = bn;
       if (o.op.m % kBM || o.op.n % bn || o.op.k % kBK) return fail(MS_E_ARG, "HP GEMM shape");

@@ -46,7 +46,44 @@ struct GemmParams {
   // Preemptible runs keep at most mma_lag k-blocks of MMAs queued on the tensor core
   // (1..4; 0 = unbounded): an abort then drains <= mma_lag k-blocks.
   int mma_lag;
+  // HP epilogue (split_k == 1 here; the split-K reduce kernel applies it otherwise):
+  // C = act(acc + bias[col] (+ resid[row, col])), act 0 none / 1 ReLU / 2 tanh-GELU.
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* resid;
+  int act;
 };
+
+// fp32 epilogue of 8 consecutive columns: + bias, + residual, activation (tanh-GELU as in
+// bias_gelu_kernel / oracle tr_bias_gelu).
+__device__ __forceinline__ void epilogue8(float (&v)[8], const __nv_bfloat16* bias8, const __nv_bfloat16* resid8,
+                                          int act) {
+  if (bias8) {
+    const uint4 b = *reinterpret_cast<const uint4*>(bias8);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[2 * e] += __low2float(b2[e]);
+      v[2 * e + 1] += __high2float(b2[e]);
+    }
+  }
+  if (resid8) {
+    const uint4 r = *reinterpret_cast<const uint4*>(resid8);
+    const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[2 * e] += __low2float(r2[e]);
+      v[2 * e + 1] += __high2float(r2[e]);
+    }
+  }
+  if (act == 1) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = fmaxf(v[e], 0.0f);
+  } else if (act == 2) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = 0.5f * v[e] * (1.0f + tanhf(k0 * (v[e] + k1 * v[e] * v[e] * v[e])));
+  }
+}
 
 template <int BN>
 struct GemmCfg {
@@ -301,13 +338,21 @@ __global__ void __launch_bounds__(256, 1)
             uint8_t* cbuf = smem_c + (q * 2 + cbuf_idx) * (32 * 64);
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
+            const bool epi = p.bias || p.resid || p.act;
+            const size_t col0 = static_cast<size_t>(nb) * BN + c0;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
+              float f[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(r[8 * v + e]);
+              if (epi)
+                epilogue8(f, p.bias ? p.bias + col0 + 8 * v : nullptr,
+                          p.resid ? p.resid + static_cast<size_t>(row) * p.n + col0 + 8 * v : nullptr, p.act);
               uint4 w;
-              w.x = pack_bf16x2(__uint_as_float(r[8 * v + 0]), __uint_as_float(r[8 * v + 1]));
-              w.y = pack_bf16x2(__uint_as_float(r[8 * v + 2]), __uint_as_float(r[8 * v + 3]));
-              w.z = pack_bf16x2(__uint_as_float(r[8 * v + 4]), __uint_as_float(r[8 * v + 5]));
-              w.w = pack_bf16x2(__uint_as_float(r[8 * v + 6]), __uint_as_float(r[8 * v + 7]));
+              w.x = pack_bf16x2(f[0], f[1]);
+              w.y = pack_bf16x2(f[2], f[3]);
+              w.z = pack_bf16x2(f[4], f[5]);
+              w.w = pack_bf16x2(f[6], f[7]);
               *reinterpret_cast<uint4*>(cbuf + lane * 64 + ((v ^ ((lane >> 1) & 3)) * 16)) = w;
             }
             fence_proxy_async_smem();
@@ -384,6 +429,9 @@ struct SplitReduceParams {
   __nv_bfloat16* c;
   int n, tiles_m, tiles_n, group_m, bn, split;
   long long total;  // tiles * (bn / 4) * 128
+  const __nv_bfloat16* bias;  // GEMM epilogue (GemmParams::bias / resid / act)
+  const __nv_bfloat16* resid;
+  int act;
 };
 
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ SplitReduceParams p) {
@@ -411,6 +459,22 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     }
     int mb, nb;
     tile_coords(tile, gp, mb, nb);
+    if (p.bias || p.resid || p.act) {
+      const size_t col = static_cast<size_t>(nb) * p.bn + cq * 4;
+      const size_t rr = static_cast<size_t>(mb * kBM + row);
+      float f[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (p.bias) f[e] += __bfloat162float(p.bias[col + e]);
+        if (p.resid) f[e] += __bfloat162float(p.resid[rr * p.n + col + e]);
+        if (p.act == 1) f[e] = fmaxf(f[e], 0.0f);
+        if (p.act == 2) {
+          const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+          f[e] = 0.5f * f[e] * (1.0f + tanhf(k0 * (f[e] + k1 * f[e] * f[e] * f[e])));
+        }
+      }
+      x = make_float4(f[0], f[1], f[2], f[3]);
+    }
     uint2 o;
     o.x = pack_bf16x2(x.x, x.y);
     o.y = pack_bf16x2(x.z, x.w);

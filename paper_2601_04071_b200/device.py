@@ -56,7 +56,7 @@ class HpOp(C.Structure):
     _fields_ = [("kind", C.c_int32), ("block_n", C.c_int32), ("a", C.c_uint64), ("b", C.c_uint64),
                 ("c", C.c_uint64), ("bias", C.c_uint64), ("m", C.c_int64), ("n", C.c_int64),
                 ("k", C.c_int64), ("split_k", C.c_int32), ("b_layout", C.c_int32), ("lda", C.c_int64),
-                ("geo", HpGeo)]
+                ("geo", HpGeo), ("resid", C.c_uint64)]
 
     @classmethod
     def from_dict(cls, o: dict) -> "HpOp":

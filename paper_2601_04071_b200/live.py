@@ -304,9 +304,10 @@ class _TrainInferConfig:
 
 
 class Config2(_TrainInferConfig):
-    """Config 2 (BASELINE configs[1]): HP ResNet-50 bs=1 inference (~160-op chain: im2col +
-    tcgen05 conv GEMMs + folded-BN/ReLU/residual + pools + FC) at 200 req/s, LP ResNet-50
-    training step at bs=64 (48 distinct conv/FC GEMM shapes fwd/dgrad/wgrad + SGD)."""
+    """Config 2 (BASELINE configs[1]): HP ResNet-50 bs=1 inference (76-op chain: im2col +
+    tcgen05 conv GEMMs with folded-BN / residual / ReLU epilogues + pools + FC) at 200 req/s,
+    LP ResNet-50 training step at bs=64 (48 distinct conv/FC GEMM shapes fwd/dgrad/wgrad +
+    SGD)."""
 
     HP_TASK, LP_TASK, NAME, RATE = "hp_resnet50", "lp_resnet50_train", "cfg2_resnet50", 200.0
 
@@ -319,7 +320,7 @@ class Config2(_TrainInferConfig):
 
 
 class Config3(_TrainInferConfig):
-    """Config 3 (BASELINE configs[2]): HP BERT-base bs=1 seq-128 encoder (96-op chain) at
+    """Config 3 (BASELINE configs[2]): HP BERT-base bs=1 seq-128 encoder (84-op chain) at
     100 req/s, LP BERT-base training step at bs=32 (9 distinct GEMM shapes x 144 GEMMs +
     AdamW over 110 M parameters)."""
 

@@ -1,12 +1,14 @@
 """Tenant workloads of BASELINE.json configs[1] and configs[2]:
 
   config 2: HP ResNet-50 bs=1 224x224 inference (53 convolutions as tcgen05 GEMMs over
-            im2col patch matrices, folded-BN bias + ReLU (+ residual) epilogue ops, 3x3/2
-            max pool, global average pool, FC 2048 -> 1000) + LP ResNet-50 training step at
+            im2col patch matrices with the folded-BN bias + residual + ReLU fused in the GEMM
+            epilogue, 3x3/2 max pool, global average pool, FC 2048 -> 1000) + LP ResNet-50
+            training step at
             bs=64 (the fwd / dgrad / wgrad GEMM of every convolution and the FC at their
             true shapes, then an SGD-momentum step over the 25.6 M parameters);
   config 3: HP BERT-base bs=1 seq 128 encoder (12 x {QKV GEMM, attention, O GEMM,
-            residual + LayerNorm, FFN1 GEMM + bias/GELU, FFN2 GEMM, residual + LayerNorm})
+            residual + LayerNorm, FFN1 GEMM with bias/GELU epilogue, FFN2 GEMM, residual +
+            LayerNorm})
             + LP BERT-base training step at bs=32 seq 128 (the 12 GEMMs of each of the 12
             layers, fwd + dgrad + wgrad, then AdamW over 110 M parameters).
 
@@ -25,8 +27,7 @@ from __future__ import annotations
 
 import math
 
-from .device import (MS_HP_ADD_LN, MS_HP_ATTN, MS_HP_AVGPOOL, MS_HP_BIAS_ACT, MS_HP_BIAS_GELU, MS_HP_GEMM,
-                     MS_HP_IM2COL, MS_HP_MAXPOOL, Device)
+from .device import MS_HP_ADD_LN, MS_HP_ATTN, MS_HP_AVGPOOL, MS_HP_GEMM, MS_HP_IM2COL, MS_HP_MAXPOOL, Device
 
 
 def pad_to(x: int, m: int) -> int:
@@ -94,15 +95,14 @@ class ResNet50HP:
             self.bufs[name] = (p, rows * cols * 2)
             return p
 
-        def gemm(a, w, c, m, n, k):
-            self.ops.append(dict(kind=MS_HP_GEMM, block_n=block_n_for(n), a=a, b=w, c=c, bias=0, m=m, n=n, k=k))
+        def gemm(a, w, c, m, n, k, bias=0, resid=0, relu=False):
+            """tcgen05 GEMM op with the conv epilogue fused (folded-BN shift, residual, ReLU on
+            the fp32 accumulators: ms_hp_op.bias / resid / geo.flags)."""
+            self.ops.append(dict(kind=MS_HP_GEMM, block_n=block_n_for(n), a=a, b=w, c=c, bias=bias, m=m, n=n, k=k,
+                                 resid=resid, geo=dict(flags=1 if relu else 0)))
 
-        def bias_act(a, bias, resid, c, m, n, relu):
-            self.ops.append(dict(kind=MS_HP_BIAS_ACT, block_n=0, a=a, b=resid, c=c, bias=bias, m=m, n=n, k=0,
-                                 geo=dict(flags=1 if relu else 0)))
-
-        def conv(c, x, name):
-            """conv c over NHWC x ([pad(hin^2) x cin]) -> output buffer pointer."""
+        def conv(c, x, name, resid=0):
+            """conv c (+ bias, + resid, ReLU per c["relu"]) over NHWC x ([pad(hin^2) x cin])."""
             ho = conv_out(c)
             m = pad_to(ho * ho, 128)
             kvalid = c["k"] * c["k"] * c["cin"]
@@ -116,9 +116,9 @@ class ResNet50HP:
                                               pad=c["p"])))
             w = weight(f"{name}.w", c["cout"], kp, math.sqrt(6.0 / kvalid))
             bias = weight(f"{name}.b", 1, c["cout"], 0.1)
-            y = buf(f"{name}.gemm", m, c["cout"])
-            gemm(a, w, y, m, c["cout"], kp)
-            return y, bias, m
+            y = buf(f"{name}.out", m, c["cout"])
+            gemm(a, w, y, m, c["cout"], kp, bias=bias, resid=resid, relu=c["relu"])
+            return y, m
 
         # stem
         self.input = buf("input", 224 * 224, 3)
@@ -126,9 +126,7 @@ class ResNet50HP:
         self.input_tensor = tid[0]
         dev.fill_synth(self.input, 224 * 224 * 3, seed, self.input_tensor, 1.0)
         convs = resnet50_convs()
-        y, b, m = conv(convs[0], self.input, "conv1")
-        x = buf("conv1.out", m, 64)
-        bias_act(y, b, 0, x, m, 64, True)
+        x, m = conv(convs[0], self.input, "conv1")
         mp = buf("pool1", pad_to(56 * 56, 128), 64)
         self.ops.append(dict(kind=MS_HP_MAXPOOL, block_n=0, a=x, b=0, c=mp, bias=0, m=pad_to(56 * 56, 128), n=64, k=0,
                              geo=dict(h=112, w=112, cin=64, kh=3, kw=3, stride=2, pad=1)))
@@ -137,22 +135,12 @@ class ResNet50HP:
         while i < len(convs):
             red, c3, ex = convs[i], convs[i + 1], convs[i + 2]
             down = convs[i + 3] if i + 3 < len(convs) and convs[i + 3]["role"] == "down" else None
-            tag = red["name"].rsplit("_", 1)[0]
-            y, b, m1 = conv(red, x, red["name"])
-            t1 = buf(f"{red['name']}.out", m1, red["cout"])
-            bias_act(y, b, 0, t1, m1, red["cout"], True)
-            y, b, m2 = conv(c3, t1, c3["name"])
-            t2 = buf(f"{c3['name']}.out", m2, c3["cout"])
-            bias_act(y, b, 0, t2, m2, c3["cout"], True)
-            y3, b3, m3 = conv(ex, t2, ex["name"])
+            t1, _ = conv(red, x, red["name"])
+            t2, _ = conv(c3, t1, c3["name"])
             resid = x
-            if down:
-                yd, bd, md = conv(down, x, down["name"])
-                resid = buf(f"{down['name']}.out", md, down["cout"])
-                bias_act(yd, bd, 0, resid, md, down["cout"], False)
-            out = buf(f"{tag}.out", m3, ex["cout"])
-            bias_act(y3, b3, resid, out, m3, ex["cout"], True)
-            x = out
+            if down:  # projection shortcut first: the expand conv's epilogue adds it
+                resid, _ = conv(down, x, down["name"])
+            x, _ = conv(ex, t2, ex["name"], resid=resid)
             i += 4 if down else 3
         # head: global average pool (row 0) -> FC (1000 classes padded to 1024) -> + bias
         pooled = buf("avgpool", 128, 2048)
@@ -160,10 +148,8 @@ class ResNet50HP:
                              geo=dict(h=7, w=7)))
         wfc = weight("fc.w", self.FC_PAD, 2048, math.sqrt(6.0 / 2048))
         bfc = weight("fc.b", 1, self.FC_PAD, 0.1)
-        fc = buf("fc.gemm", 128, self.FC_PAD)
-        gemm(pooled, wfc, fc, 128, self.FC_PAD, 2048)
         self.logits = buf("logits", 128, self.FC_PAD)
-        bias_act(fc, bfc, 0, self.logits, 128, self.FC_PAD, False)
+        gemm(pooled, wfc, self.logits, 128, self.FC_PAD, 2048, bias=bfc)
 
     @property
     def gemm_flops(self) -> int:
@@ -252,11 +238,9 @@ class BertHP:
             x1 = buf(f"{t}.x1", S, D)
             self.ops.append(dict(kind=MS_HP_ADD_LN, block_n=0, a=o, b=x, c=x1, bias=weight(f"{t}.ln1", 2, D, 1.0),
                                  m=S, n=D, k=0))
-            f = buf(f"{t}.ffn1", S, F)
-            gemm(x1, weight(f"{t}.w1", F, D, math.sqrt(6.0 / D)), f, F, D)
-            g = buf(f"{t}.gelu", S, F)
-            self.ops.append(dict(kind=MS_HP_BIAS_GELU, block_n=0, a=f, b=0, c=g, bias=weight(f"{t}.b1", 1, F, 0.1),
-                                 m=S, n=F, k=0))
+            g = buf(f"{t}.ffn1_gelu", S, F)  # FFN1 + bias + GELU fused in the GEMM epilogue
+            self.ops.append(dict(kind=MS_HP_GEMM, block_n=128, a=x1, b=weight(f"{t}.w1", F, D, math.sqrt(6.0 / D)),
+                                 c=g, bias=weight(f"{t}.b1", 1, F, 0.1), m=S, n=F, k=D, geo=dict(flags=2)))
             f2 = buf(f"{t}.ffn2", S, D)
             gemm(g, weight(f"{t}.w2", D, F, math.sqrt(6.0 / F)), f2, D, F)
             x2 = buf(f"{t}.out", S, D)

@@ -73,7 +73,19 @@ class ChainOracle:
             if lda != K:
                 a = np.ascontiguousarray(np.lib.stride_tricks.as_strided(a, (m, K), (lda * 2, 2))).reshape(-1)
             w = rd(o["b"], n * K)
-            return rnd(T.gemm_rows(a, w, list(range(m)), n, K).reshape(-1))
+            y = T.gemm_rows(a, w, list(range(m)), n, K)
+            flags = (o.get("geo") or {}).get("flags", 0)
+            if o.get("bias") or o.get("resid") or flags:  # fused epilogue on the fp32 accumulators
+                y = y.astype(np.float32)
+                if o.get("bias"):
+                    y = y + T.bf16_to_f32(rd(o["bias"], n))[None, :]
+                if o.get("resid"):
+                    y = y + T.bf16_to_f32(rd(o["resid"], m * n)).reshape(m, n)
+                if flags & 1:
+                    y = np.maximum(y, 0.0)
+                if flags & 2:
+                    y = 0.5 * y * (1.0 + np.tanh(0.7978845608028654 * (y + 0.044715 * y * y * y)))
+            return rnd(y.reshape(-1))
         if k == GEMM_SWIGLU:  # silu(x Wg^T) * (x Wu^T) on the fp32 accumulators, W = [Wg; Wu]
             K, lda = o["k"], o.get("lda") or o["k"]
             a = rd(o["a"], (m - 1) * lda + K)

@@ -182,7 +182,9 @@ def test_resnet50_hp_chain_full_size(dev, T):
     from paper_2601_04071_b200.tenants import ResNet50HP
     net = ResNet50HP(dev, SEED)
     kinds = [o["kind"] for o in net.ops]
-    assert kinds.count(1) == 54 and kinds.count(7) == 20 and kinds.count(9) == 1 and kinds.count(10) == 1
+    # 53 convs + FC as GEMMs with fused bias / residual / ReLU epilogues, 20 im2col, 2 pools
+    assert len(kinds) == 76 and kinds.count(1) == 54 and kinds.count(7) == 20 and kinds.count(9) == 1
+    assert sum(1 for o in net.ops if o.get("resid")) == 16  # one residual add per bottleneck
     ch = check_chain(dev, T, net, net.logits, 1000, "resnet50_bs1_chain", 1e-2)
     dev.hp_unregister_chain(ch)
     net.free()
@@ -191,7 +193,7 @@ def test_resnet50_hp_chain_full_size(dev, T):
 def test_bert_base_hp_chain_full_size(dev, T):
     from paper_2601_04071_b200.tenants import BertHP
     net = BertHP(dev, SEED)
-    assert len(net.ops) == 96
+    assert len(net.ops) == 84  # 12 x {QKV, attn, O, add-LN, FFN1 (+bias+GELU epilogue), FFN2, add-LN}
     ch = check_chain(dev, T, net, net.output, 128 * 768, "bert_base_bs1_seq128_chain", 2e-2)
     dev.hp_unregister_chain(ch)
     net.free()
