@@ -151,7 +151,8 @@ class Config4:
     N_LP = 8192
     N_EW = 1 << 30
 
-    def __init__(self, dev: Device, seed: int = SEED, m: int | None = None, tier=None, slow_max: int = 8):
+    def __init__(self, dev: Device, seed: int = SEED, m: int | None = None, tier=None, slow_max: int = 8,
+                 lp_split: int = 1):
         """tier: a MemoryTier (tier.py) to place the tenants' memory through — HP buffers
         and weights pinned (task 0), LP GEMM (task 1) and streamer (task 2) spillable, in
         that allocation order (the memory-intensive case)."""
@@ -180,7 +181,9 @@ class Config4:
         self.a, self.b, self.c = gemm_alloc(n * n * 2), gemm_alloc(n * n * 2), gemm_alloc(n * n * 2)
         dev.fill_synth(self.a, n * n, seed, 1, 1.0)
         dev.fill_synth(self.b, n * n, seed, 2, 1.0 / math.sqrt(n))
-        self.lp_gemm = dev.lp_register_gemm(self.a, self.b, self.c, n, n, n, block_n=256)
+        # lp_split > 1: 128 x 256 tiles cut into k-slices (shorter preemption grain, finer
+        # harvest packing; fp32 partials reduced in-kernel)
+        self.lp_gemm = dev.lp_register_gemm(self.a, self.b, self.c, n, n, n, block_n=256, split_k=lp_split)
         self.x, self.y = ew_alloc(self.N_EW * 2), ew_alloc(self.N_EW * 2)
         dev.fill_synth(self.x, self.N_EW, seed, 21, 1.0)
         dev.fill_synth(self.y, self.N_EW, seed, 22, 1.0)

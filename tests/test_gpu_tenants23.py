@@ -320,7 +320,9 @@ def test_lp_gemm_split_k_preempt_resume(dev, T, m, n, k):
     while True:
         dev.lp_run(kern, begin, kern.total_tiles)
         runs += 1
-        time.sleep(0.00001 * (runs % 3))  # raised right after the launch, or 10 / 20 us into the run
+        t_end = time.perf_counter() + 1e-5 * ((runs - 1) % 3)  # raised at once, or 10 / 20 us in
+        while time.perf_counter() < t_end:
+            pass
         dev.preempt_raise()
         st = dev.lp_wait(kern, 60)
         begin = st["cursor"]
