@@ -83,7 +83,17 @@ struct GemvParams {
   uint32_t tag;  // this launch's wire tag (16 bits)
   int inflight;  // max units issued but not yet landed (the rest of the ring buffers landed data)
   int prefetch;  // L2 lookahead in units past the issue point
+  // Head prefetch: the first kGemvHeadCtas CTAs to start prefetch the first head_kb KB of the
+  // chain's weights (op order, every CTA's units) into L2.  When the doorbell fires while a
+  // preempted LP grid still drains, the CTAs that start on free SMs keep HBM busy for the
+  // CTAs that start late; those then find their first units in L2 and catch up, instead of
+  // holding back every op of the static unit plan by their start delay.
+  int head_kb;
+  uint32_t* start_cnt;  // CTAs started (reset by the last CTA)
 };
+
+constexpr int kGemvHeadCtas = 8;
+constexpr uint32_t kGemvHeadChunk = 64 * 1024;
 
 __device__ __forceinline__ uint4 ld_relaxed_v4(const uint32_t* p) {
   uint4 v;
@@ -389,6 +399,24 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         pf_u = u;
       };
       pf_seek(0, gemv_first_unit(sops[0], G));
+      if (p.head_kb > 0) {
+        const uint32_t r = atomicAdd(p.start_cnt, 1u);
+        if (r < static_cast<uint32_t>(kGemvHeadCtas)) {
+          // chunk c of the head (64 KB, op order, contiguous weight ranges) -> CTA c % 8
+          const size_t head = static_cast<size_t>(p.head_kb) * 1024;
+          size_t pos = 0;
+          uint32_t c = 0;
+          for (int oi = 0; oi < p.n_ops && pos < head; ++oi) {
+            const GemvOpDesc& q = sops[oi];
+            if (q.kind != kGemvMatvec && q.kind != kGemvSwiglu) continue;
+            const size_t bytes = static_cast<size_t>(q.kind == kGemvSwiglu ? 2 * q.n : q.n) * q.k * 2;
+            const uint8_t* base = reinterpret_cast<const uint8_t*>(q.w);
+            for (size_t off = 0; off < bytes && pos < head; off += kGemvHeadChunk, pos += kGemvHeadChunk, ++c)
+              if (c % kGemvHeadCtas == r)
+                bulk_prefetch_l2(base + off, static_cast<uint32_t>(min(static_cast<size_t>(kGemvHeadChunk), bytes - off)));
+          }
+        }
+      }
       auto pf_step = [&]() -> bool {
         if (pf_oi >= p.n_ops || pf_count >= issued + P) return false;
         const GemvOpDesc& q = sops[pf_oi];

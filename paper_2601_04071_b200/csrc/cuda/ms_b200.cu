@@ -110,6 +110,7 @@ int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint6
 
 constexpr int kRedoCap = 8192;
 constexpr int kMaxChainOps = 512;
+constexpr int kGemvHeadKbDefault = 0;  // head prefetch (hp_gemv.cuh), A/B: tools/gemv_head_ab.py
 constexpr bool kGemvDynamicDefault = false;  // decided by tools/gemv_dynamic_ab.py  // per-op chains (config-2 ResNet-50: ~160 ops); fused / GEMV plans are shorter
 
 // FFI callers may pass any id: every entry point that indexes a slot checks it first.
@@ -841,15 +842,16 @@ int plan_gemv(ms_dev* d, HpChain& ch) {
   const int np = n;
   // [0, n): grid phase counters; [n, 2n): dynamic unit-claim counters (both reset by the
   // last CTA of each launch)
-  MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * 2 * np));
-  MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * 2 * np));
+  // [2n]: CTAs started (head prefetch)
+  MS_CUDA(cudaMalloc(&ch.phase_d, sizeof(uint32_t) * (2 * np + 1)));
+  MS_CUDA(cudaMemset(ch.phase_d, 0, sizeof(uint32_t) * (2 * np + 1)));
   ch.fused_ctl = d->next_hp_ctl++;
   if (ch.fused_ctl >= MS_N_CTL) return fail(MS_E_ARG, "out of HP control blocks");
   ch.fused_first = first;
   ch.fused_last = last;
   ch.fused_grid = grid;
   ch.fused_cs = 1;
-  ch.n_phases = 2 * np;
+  ch.n_phases = 2 * np + 1;
   ch.gemv = true;
   ch.fusable = true;
   return 0;
@@ -891,6 +893,12 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
     return e ? std::max(0, atoi(e)) : 16;
   }();
   p.prefetch = prefetch;
+  static const int head_kb = [] {
+    const char* e = getenv("MS_GEMV_HEAD_KB");  // 0: no head prefetch
+    return e ? std::max(0, atoi(e)) : kGemvHeadKbDefault;
+  }();
+  p.head_kb = head_kb;
+  p.start_cnt = ch.phase_d + 2 * ch.gemv_descs.size();
   if (dynamic)
     MS_CUDA(launch_kc(hp_gemv_kernel<true>, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
   else
@@ -1138,8 +1146,9 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
       if ((desc->k / kBK) % s.split) return fail(MS_E_ARG, "split_k must divide K / 64");
       const size_t tiles = static_cast<size_t>(s.tiles_m) * s.tiles_n;
       MS_CUDA(cudaMalloc(&s.ws, sizeof(float) * tiles * s.split * kBM * bn));
-      MS_CUDA(cudaMalloc(&s.tile_cnt, sizeof(unsigned int) * tiles));
-      MS_CUDA(cudaMemset(s.tile_cnt, 0, sizeof(unsigned int) * tiles));
+      // reduction-tree group counters: <= split per tile (tc_gemm.cuh split_tree_reduce)
+      MS_CUDA(cudaMalloc(&s.tile_cnt, sizeof(unsigned int) * tiles * s.split));
+      MS_CUDA(cudaMemset(s.tile_cnt, 0, sizeof(unsigned int) * tiles * s.split));
     }
     s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n * s.split;
     if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
@@ -1479,7 +1488,7 @@ int ms_lp_reset(ms_dev* d, int id) {
   // A fresh pass: slices of half-finished split-K tiles from an abandoned pass must not
   // count towards the new pass's reductions.
   if (s.tile_cnt)
-    MS_CUDA(cudaMemsetAsync(s.tile_cnt, 0, sizeof(unsigned int) * s.tiles_m * s.tiles_n, d->lp));
+    MS_CUDA(cudaMemsetAsync(s.tile_cnt, 0, sizeof(unsigned int) * s.tiles_m * s.tiles_n * s.split, d->lp));
   return 0;
 }
 

@@ -113,6 +113,8 @@ struct GemmSmemCtl {
   uint32_t producer_done;
   uint32_t tiles_done;
   uint32_t fix_last;
+  uint32_t red_stop;
+  uint32_t epi_done;  // epilogue warps finished (the CTA's mirror poller may stop)
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -123,6 +125,138 @@ __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, in
   const int in_group = static_cast<int>(t - group * group_span);
   mb = first_m + in_group % gm;
   nb = in_group / gm;
+}
+
+// ---------------------------------------------------------------- split-K reduction tree
+// An LP unit is (tile, k-slice).  Its fp32 partial goes to ws slot `slice`.  Slices are
+// reduced by a fixed tree of fan-in kRedFan: level 0 holds the S partials, the group
+// (level l, g) sums partials [g*F, g*F + F) of level l (in index order) into partial g of
+// level l + 1, which lives in ws slot g * F^(l+1) (the group's first slot, in place).  The
+// last unit to arrive at a group's counter reduces it; the top group (<= F partials) writes
+// bf16 C.  The summation order is fixed by the tree, never by timing, so a preempted and
+// resumed GEMM is bit-identical to an uninterrupted one.  A reducer reads at most F partials
+// (<= 512 KB) instead of all S (25 MB for the 128 x 192 x 802,816 wgrad at S = 256, which
+// made one CTA spend ~0.5 ms in a non-preemptible reduction), and it stops at 32-column
+// chunk boundaries when preempted, parking the rest as a continuation entry on the redo
+// list (kRedEntry | tile << 32 | level << 24 | group << 8 | chunk).
+constexpr int kRedFan = 4;
+constexpr unsigned long long kRedEntry = 1ull << 62;
+
+__device__ __forceinline__ int red_level_count(int S, int level) {
+  int n = S;
+  for (int i = 0; i < level; ++i) n = (n + kRedFan - 1) / kRedFan;
+  return n;
+}
+// counter index of group (level, g) inside the tile's block of S counters
+__device__ __forceinline__ int red_counter(int S, int level, int g) {
+  int base = 0, n = S;
+  for (int i = 0; i < level; ++i) {
+    base += (n + kRedFan - 1) / kRedFan;
+    n = (n + kRedFan - 1) / kRedFan;
+  }
+  return base + g;
+}
+
+__device__ __forceinline__ float4 f4add(float4 a, const float4 b) {
+  a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  return a;
+}
+
+// Run by the 128 epilogue threads (named barrier 1).  `arrive`: this unit just wrote its
+// level-0 partial into slot `g * F + j` and arrives at group (0, g); otherwise resume the
+// already-won group (level, g) at `chunk`.  Returns when the tree above this unit needs no
+// more work from it (another unit will arrive later), when C is written, or after parking a
+// continuation because of a preemption.
+template <int BN>
+__device__ void split_tree_reduce(const GemmParams& p, GemmSmemCtl* s, long long tile, int level, int g, int chunk,
+                                  bool arrive, int mb, int nb, int row) {
+  const int S = p.split_k;
+  float4* const ws = reinterpret_cast<float4*>(p.ws) + static_cast<size_t>(tile) * S * (kBM * BN / 4);
+  unsigned int* const cnt = p.tile_cnt + static_cast<size_t>(tile) * S;
+  const int tid = threadIdx.x - 128;
+  for (;;) {
+    const int n = red_level_count(S, level);
+    const int gsize = min(kRedFan, n - g * kRedFan);
+    const bool top = n <= kRedFan;
+    if (arrive) {
+      __threadfence();  // release this thread's partial stores (gpu scope) ...
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // ... before the group counter moves
+      if (tid == 0) {
+        unsigned int* c = cnt + red_counter(S, level, g);
+        const bool last = atomicAdd(c, 1u) + 1 == static_cast<unsigned>(gsize);
+        if (last) *c = 0;  // self-resetting: nobody else arrives at this group in this pass
+        s->fix_last = last ? 1u : 0u;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (!s->fix_last) return;
+      __threadfence();
+    }
+    size_t stride = 1;  // ws slots between consecutive partials of this level: F^level
+    for (int i = 0; i < level; ++i) stride *= kRedFan;
+    const size_t slot0 = static_cast<size_t>(g) * kRedFan * stride;
+    for (int c = chunk; c < BN / 32; ++c) {
+      if (c > chunk) {
+        // preemption point between 32-column chunks (one decision for all 128 threads; every
+        // claim of a group makes at least one chunk of progress)
+        if (tid == 0) s->red_stop = (p.run.preemptible && ld_volatile_smem(&s->preempt)) ? 1u : 0u;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const bool stop = s->red_stop != 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (stop) {
+          if (tid == 0)
+            push_redo(p.run, kRedEntry | (static_cast<unsigned long long>(tile) << 32) |
+                                 (static_cast<unsigned long long>(level) << 24) |
+                                 (static_cast<unsigned long long>(g) << 8) | static_cast<unsigned long long>(c));
+          return;
+        }
+      }
+      // partial j of the group, column quad cq: ws[(slot0 + j*stride) * (128*BN/4) + cq*128 + row]
+      // every partial of the group in flight at once for half a chunk (16 x 16 B per thread,
+      // 32 KB per CTA), then summed in index order
+      float4 acc[8];
+      const float4* b0 = ws + slot0 * (kBM * BN / 4) + static_cast<size_t>(c * 8) * kBM + row;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 x[kRedFan][4];
+#pragma unroll
+        for (int j = 0; j < kRedFan; ++j)
+          if (j < gsize) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) x[j][v] = __ldcg(b0 + j * stride * (kBM * BN / 4) + (h * 4 + v) * kBM);
+          }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[h * 4 + v] = x[0][v];
+#pragma unroll
+        for (int j = 1; j < kRedFan; ++j)
+          if (j < gsize) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[h * 4 + v] = f4add(acc[h * 4 + v], x[j][v]);
+          }
+      }
+      if (top) {
+        __nv_bfloat16* crow = p.c + static_cast<size_t>(mb * kBM + row) * p.n + static_cast<size_t>(nb) * BN + c * 32;
+#pragma unroll
+        for (int v = 0; v < 8; v += 2) {
+          uint4 o;
+          o.x = pack_bf16x2(acc[v].x, acc[v].y);
+          o.y = pack_bf16x2(acc[v].z, acc[v].w);
+          o.z = pack_bf16x2(acc[v + 1].x, acc[v + 1].y);
+          o.w = pack_bf16x2(acc[v + 1].z, acc[v + 1].w);
+          *reinterpret_cast<uint4*>(crow + v * 4) = o;
+        }
+      } else {
+        float4* d0 = ws + slot0 * (kBM * BN / 4) + static_cast<size_t>(c * 8) * kBM + row;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) __stcg(d0 + v * kBM, acc[v]);
+      }
+    }
+    if (top) return;
+    // this group's sum is partial g of the next level, in group g / F there
+    level += 1;
+    g /= kRedFan;
+    chunk = 0;
+    arrive = true;
+  }
 }
 
 template <int BN>
@@ -156,6 +290,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(&s->mma_drain, 1);
     s->preempt = 0;
     s->producer_done = 0;
+    s->epi_done = 0;
     s->tiles_done = 0;
     fence_mbar_init();
     cta_started(p.run);
@@ -193,6 +328,7 @@ __global__ void __launch_bounds__(256, 1)
         s->tile_abort[slot] = 0;
         mbar_arrive(&s->tile_full[slot]);
         if (tile < 0) break;
+        if (tile & kRedEntry) continue;  // reduction continuation: no MMA work
         int mb, nb;
         tile_coords(tile / split, p, mb, nb);
         const int kb0 = static_cast<int>(tile % split) * num_kb;
@@ -238,6 +374,10 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
         if (s->tile_id[slot] < 0) break;
         if (j >= 2) mbar_wait(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);
+        if (s->tile_id[slot] & kRedEntry) {  // reduction continuation: hand the slot on
+          mbar_arrive(&s->tmem_full[slot]);
+          continue;
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(slot * BN);
         bool aborted = false;
@@ -292,7 +432,9 @@ __global__ void __launch_bounds__(256, 1)
       dbg_stamp(p.run, 2);
     }
   } else if (warp == 2) {
-    if (lane == 0 && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->producer_done);
+    // The mirror poller stays up until the epilogue is done, not just the producer: an epilogue
+    // still reducing split-K partials must see a preemption (it stops at a chunk boundary).
+    if (lane == 0 && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->epi_done);
   } else if (warp == 3) {
     if (lane == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &s->preempt, &s->producer_done);
     if (lane == 0 && p.run.preemptible && blockIdx.x >= 1 && blockIdx.x <= kAuxPollers)
@@ -308,12 +450,13 @@ __global__ void __launch_bounds__(256, 1)
       if (tile < 0) break;
       mbar_wait(&s->tmem_full[slot], (j >> 1) & 1);
       tc_fence_after();
-      const bool keep = !s->tile_abort[slot];
-      const long long unit_tile = tile / split;
-      const int unit_slice = static_cast<int>(tile % split);
+      const bool cont = (tile & kRedEntry) != 0;  // reduction continuation (split-K tree)
+      const bool keep = !cont && !s->tile_abort[slot];
+      const long long unit_tile = cont ? static_cast<long long>((tile >> 32) & 0x3FFFFFFF) : tile / split;
+      const int unit_slice = cont ? 0 : static_cast<int>(tile % split);
       int mb = 0, nb = 0;
+      if (keep || cont) tile_coords(unit_tile, p, mb, nb);
       if (keep) {
-        tile_coords(unit_tile, p, mb, nb);
         const int row_in_tile = q * 32 + lane;
         const int row = mb * kBM + row_in_tile;
         // split-K partial layout (per unit, 128 x BN fp32): [BN / 4][128 rows] of float4, so for a
@@ -371,44 +514,24 @@ __global__ void __launch_bounds__(256, 1)
       if (q == 0 && lane == 0) {
         mbar_arrive(&s->tmem_empty[slot]);
         mbar_arrive(&s->tile_empty[slot]);
-        if (keep && split > 1 && p.tile_cnt) {
-          __threadfence();
-          s->fix_last = atomicAdd(&p.tile_cnt[unit_tile], 1u) + 1 == static_cast<unsigned>(split) ? 1u : 0u;
-        }
       }
-      if (keep && split > 1 && p.tile_cnt) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (s->fix_last) {
-          // Last slice of this tile: reduce all slices in slice order, write bf16 C.
-          __threadfence();
-          const int row_in_tile = q * 32 + lane;
-          const float4* base = reinterpret_cast<const float4*>(p.ws) +
-                               static_cast<size_t>(unit_tile) * split * (kBM * BN / 4);
-          __nv_bfloat16* crow = p.c + static_cast<size_t>(mb * kBM + row_in_tile) * p.n + static_cast<size_t>(nb) * BN;
-#pragma unroll 1
-          for (int cq = 0; cq < BN / 4; cq += 2) {
-            float4 x = base[static_cast<size_t>(cq) * kBM + row_in_tile];
-            float4 y = base[static_cast<size_t>(cq + 1) * kBM + row_in_tile];
-            for (int sl = 1; sl < split; ++sl) {  // slice order: deterministic sum
-              const float4* sb = base + static_cast<size_t>(sl) * (kBM * BN / 4);
-              const float4 u = sb[static_cast<size_t>(cq) * kBM + row_in_tile];
-              const float4 w = sb[static_cast<size_t>(cq + 1) * kBM + row_in_tile];
-              x.x += u.x; x.y += u.y; x.z += u.z; x.w += u.w;
-              y.x += w.x; y.y += w.y; y.z += w.z; y.w += w.w;
-            }
-            uint4 o;
-            o.x = pack_bf16x2(x.x, x.y);
-            o.y = pack_bf16x2(x.z, x.w);
-            o.z = pack_bf16x2(y.x, y.y);
-            o.w = pack_bf16x2(y.z, y.w);
-            *reinterpret_cast<uint4*>(crow + cq * 4) = o;
-          }
-          if (q == 0 && lane == 0) p.tile_cnt[unit_tile] = 0;
-        }
+      if (split > 1 && p.tile_cnt && (keep || cont)) {
+        // split-K: arrive at this slice's level-0 group (or resume a parked group) and
+        // reduce up the tree as far as this unit is the last arrival
+        const int row_in_tile = q * 32 + lane;
+        if (cont)
+          split_tree_reduce<BN>(p, s, unit_tile, static_cast<int>((tile >> 24) & 0xFF),
+                                static_cast<int>((tile >> 8) & 0xFFFF), static_cast<int>(tile & 0xFF), false, mb, nb,
+                                row_in_tile);
+        else
+          split_tree_reduce<BN>(p, s, unit_tile, 0, unit_slice / kRedFan, 0, true, mb, nb, row_in_tile);
       }
     }
     if (lane == 0) bulk_wait_read<0>();  // staging must stay valid until the TMA read it
-    if (q == 0 && lane == 0) dbg_stamp(p.run, 3);
+    if (q == 0 && lane == 0) {
+      st_volatile_smem(&s->epi_done, 1u);
+      dbg_stamp(p.run, 3);
+    }
   }
 
   tc_fence_before();

@@ -757,8 +757,16 @@ json LiveRun::run() {
     }
     emit(done, EventKind::KernelDone, smp.stream, hp_[smp.stream].spec->name, "seq=" + std::to_string(smp.seq));
   }
+  json preempted_runs = json::array();  // [kernel, exit - raise, start - raise, seen - raise, detail]
   for (const LpSample& smp : lp_samples_) {
     if (smp.raise >= 0) {
+      json e = json::array();
+      e.push_back(json(smp.kernel));
+      e.push_back(json(static_cast<long long>(dev_to_host(smp.exit) - smp.raise)));
+      e.push_back(json(static_cast<long long>(smp.start ? dev_to_host(smp.start) - smp.raise : 0)));
+      e.push_back(json(static_cast<long long>(smp.seen ? dev_to_host(smp.seen) - smp.raise : 0)));
+      e.push_back(json(smp.detail));
+      preempted_runs.push_back(std::move(e));
       // A run whose first CTA started after the raise was still queued behind the HP chain
       // (its CTAs get SMs only when HP leaves them): it never occupied an SM HP needed, so
       // its exit time is reported apart from the drain of running LP work.
@@ -830,6 +838,7 @@ json LiveRun::run() {
   json c = json::array();
   for (const Ns x : ring_to_first_) c.push_back(json(static_cast<long long>(x)));
   raw["ring_to_first_hp_cta_all"] = std::move(c);
+  raw["preempted_lp_runs"] = std::move(preempted_runs);
   out["samples"] = std::move(raw);
   if (!debug_.empty()) {
     // phase p of CTA c relative to the raise, converted with the drift-corrected clock

@@ -320,7 +320,9 @@ def test_lp_gemm_split_k_preempt_resume(dev, T, m, n, k):
     while True:
         dev.lp_run(kern, begin, kern.total_tiles)
         runs += 1
-        t_end = time.perf_counter() + 1e-5 * ((runs - 1) % 3)  # raised at once, or 10 / 20 us in
+        # raised at once, or 10 / 20 / 80 us in: every fourth run outlasts a unit (a 49-k-block
+        # slice of the 128x192 tile is ~14 us on one SM plus the launch), so progress is certain
+        t_end = time.perf_counter() + (0.0, 1e-5, 2e-5, 8e-5)[(runs - 1) % 4]
         while time.perf_counter() < t_end:
             pass
         dev.preempt_raise()

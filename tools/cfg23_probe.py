@@ -37,7 +37,9 @@ for cls in ("Config3", "Config2"):
                       "launches": lp["launches"], "preemptions": lp["preemptions"],
                       "extensions": lp["budget_extensions"], "parents": lp["parents_completed"],
                       "ring_p99_us": r["ring_to_first_hp_cta_all"].get("p99_ns", 0) / 1e3,
-                      "lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms")}
+                      "lp_sms": (r.get("power_governor") or {}).get("mean_lp_sms"),
+                      "lp_exit_p99_us": (lambda x: sorted(x)[max(0, -(-99 * len(x) // 100) - 1)] / 1e3 if x else None)(
+                          r["samples"].get("preempt_flag_to_last_lp_exit", []))}
     out[cls] = res
     w.close()
 print(json.dumps(out, indent=1))
