@@ -511,9 +511,11 @@ def main():
     peak = peaks.get("bf16_tflops", 1590.0)
     achieved = 2.0 * 8192 ** 3 / (calib["lp_gemm_ms"] * 1e-3) / 1e12
     ncu = ROOT / "profiles" / "ncu_summary.json"
+    pair = calib.get("lp_gemm_tile_ctas", 1) == 2
+    kname = "tc_gemm2_kernel<512>" if pair else "tc_gemm_kernel<256>"
     traffic = None
     if ncu.exists():
-        traffic = json.loads(ncu.read_text()).get("tc_gemm_kernel<256>", {}).get("dram_bytes_per_launch")
+        traffic = json.loads(ncu.read_text()).get(kname, {}).get("dram_bytes_per_launch")
     cfg4_agg = aggregate_leg([r["cfg4"] for r in allr], CFG4_WORKLOAD) if allr[0]["cfg4"] else None
     legs_agg = {key: aggregate_leg([r["legs23"][key] for r in allr], wl) for key, wl in
                 (("cfg2", CFG2_WORKLOAD), ("cfg3", CFG3_WORKLOAD)) if key in allr[0]["legs23"]}
@@ -556,7 +558,8 @@ def main():
                                    "clocks": {k: allr[0]["pb_clocks"].get(k) for k in ("sm_mhz", "reasons")}},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "tc_gemm_kernel<256> (LP 8192^3 bf16, 2048 128x256 tiles)",
+                     "kernel": (f"{kname} (LP 8192^3 bf16, {calib.get('lp_gemm_tiles')} "
+                                + ("256x512 tiles on CTA pairs)" if pair else "128x256 tiles)")),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
         "e2e": {"value": _us(percentile(E2E, 0.99)), "unit": "us",
                 "h2d_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),

@@ -128,6 +128,9 @@ int ms_lp_run_ex(ms_dev* dev, int id, uint64_t begin, uint64_t end, uint64_t bud
  * first, then fresh tiles), for harvest-budget pacing. */
 uint64_t ms_lp_progress(ms_dev* dev, int id);
 uint64_t ms_lp_total_tiles(ms_dev* dev, int id);
+/* SMs (CTAs) one tile of the kernel occupies: 2 for GEMMs on CTA pairs (256 x 512 tiles),
+ * else 1.  A wave of an LP run over n SMs covers n / ms_lp_tile_ctas tiles. */
+int ms_lp_tile_ctas(ms_dev* dev, int id);
 /* Number of SMs a preemptible LP GEMM grid leaves free (default 0). */
 int ms_set_lp_sm_reserve(ms_dev* dev, int n);
 /* Diagnostics: enable=1 arms per-CTA phase timestamps for subsequent LP runs; enable=0

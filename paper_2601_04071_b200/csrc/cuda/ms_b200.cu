@@ -123,7 +123,8 @@ constexpr int kGateSmem = 40 * 1024;
 
 struct LpSlot {
   bool used = false;
-  bool pair = false;  // GEMM on CTA pairs (tc_gemm2.cuh): 256 x 256 tiles
+  bool pair = false;  // GEMM on CTA pairs (tc_gemm2.cuh): 256 x pair_tn tiles
+  int pair_tn = 256;
   ms_lp_desc desc{};
   uint64_t total_tiles = 0;
   int tiles_m = 0, tiles_n = 0;
@@ -212,7 +213,10 @@ struct ms_dev {
   uint32_t hp_seq = 0;  // monotonic doorbell sequence of this device
   unsigned long long* dbg = nullptr;  // per-CTA phase stamps of the next LP run (diagnostics)
   unsigned long long* dbg_buf = nullptr;
-  int lp_sm_reserve = 1;  // SMs an LP GEMM grid leaves free (the HP gate's home)
+  // SMs an LP grid leaves free.  0: the gate kernel (one warp, 1 KB smem) co-resides with
+  // an LP CTA, and the pair GEMM's 74 pairs fill the machine (a reserved SM left 73 pairs,
+  // i.e. 8 waves of 256 x 512 tiles for 8192^3 instead of 7).
+  int lp_sm_reserve = 0;
   int lp_align_clusters[5] = {0, 0, 0, 0, 0};  // max active C-CTA clusters of the LP GEMM (MS_LP_CLUSTER_ALIGN)
   int hp_fused = 1;       // 0: per-op kernels; 1: fused launch (cluster split-K when it fits); 2: fused, no clusters
 };
@@ -239,7 +243,10 @@ int set_smem_attrs() {
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(hp_gemv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmemBytes));
-  MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm2Cfg::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Gemm2Cfg<256>::kSmemBytes));
+  MS_CUDA(cudaFuncSetAttribute(tc_gemm2_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Gemm2Cfg<512>::kSmemBytes));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
@@ -1131,15 +1138,23 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     if (desc->m % kBM || desc->n % bn || desc->k % kBK || desc->k < kBK)
       return fail(MS_E_ARG, "GEMM shape must be a multiple of (128, block_n, 64)");
     if (desc->m > (1ll << 31) || desc->n > (1ll << 31) || desc->k > (1ll << 31)) return fail(MS_E_ARG, "shape too large");
-    // MS_LP_GEMM_PAIR=1: 256-aligned shapes with 256-wide tiles run on CTA pairs
-    // (cta_group::2, tc_gemm2.cuh).  Measured at parity with the single-CTA kernel on 8192^3
-    // (1302 vs 1308 TF/s, tensor pipe ~72% active in both under the power cap), so the
-    // single-CTA kernel (lower preemption drain, fewer moving parts) stays the default.
-    s.pair = bn == 256 && desc->m % 256 == 0 && desc->n % 256 == 0 && getenv("MS_LP_GEMM_PAIR") &&
-             atoi(getenv("MS_LP_GEMM_PAIR")) != 0;
+    // Large GEMMs run on CTA pairs (cta_group::2, tc_gemm2.cuh) with 256 x 512 tiles: 8192^3
+    // at 1574-1585 TFLOP/s burst vs 1331-1346 for the single-CTA 128 x 256 kernel and
+    // 1610-1612 for cuBLAS on the same box (tools/gemm_ab2.py, profiles/r02_gemm_ab.json).
+    // Chosen when the shape has >= 4 waves of pair tiles (fewer tiles lose more to the last
+    // wave than the pair saves) and no k-split.  MS_LP_GEMM_PAIR=0 forces the single-CTA
+    // kernel, =1 pairs with 256 x 256 tiles, =2 pairs with 256 x 512 tiles.
+    const char* pe = getenv("MS_LP_GEMM_PAIR");
+    int pair_mode = pe ? atoi(pe) : -1;
+    if (pair_mode < 0) {
+      const int64_t pair_tiles = desc->n % 512 == 0 ? (desc->m / 256) * (desc->n / 512) : 0;
+      pair_mode = (desc->split_k <= 1 && pair_tiles >= 4 * (d->prop.multiProcessorCount / 2)) ? 2 : 0;
+    }
+    s.pair_tn = pair_mode == 2 && desc->n % 512 == 0 ? 512 : 256;
+    s.pair = bn == 256 && desc->m % 256 == 0 && desc->n % s.pair_tn == 0 && pair_mode != 0 && desc->split_k <= 1;
     const int tm = s.pair ? 256 : kBM;
     s.tiles_m = static_cast<int>(desc->m / tm);
-    s.tiles_n = static_cast<int>(desc->n / bn);
+    s.tiles_n = static_cast<int>(desc->n / (s.pair ? s.pair_tn : bn));
     s.split = desc->split_k > 1 ? desc->split_k : 1;
     if (s.split > 1) {
       if (s.pair) return fail(MS_E_ARG, "split_k is not supported on CTA pairs");
@@ -1282,8 +1297,12 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
       const int pairs = static_cast<int>(std::max<uint64_t>(
           1, std::min<uint64_t>(work, static_cast<uint64_t>(std::max(2, d->prop.multiProcessorCount - d->lp_sm_reserve) / 2))));
       p.group_m = s.desc.group_m ? s.desc.group_m : 8;
-      MS_CUDA(launch_kc(tc_gemm2_kernel, 2 * pairs, 256, Gemm2Cfg::kSmemBytes, d->lp, false, 2, s.tma_a, s.tma_b,
-                        s.tma_c, p));
+      if (s.pair_tn == 512)
+        MS_CUDA(launch_kc(tc_gemm2_kernel<512>, 2 * pairs, 256, Gemm2Cfg<512>::kSmemBytes, d->lp, false, 2, s.tma_a,
+                          s.tma_b, s.tma_c, p));
+      else
+        MS_CUDA(launch_kc(tc_gemm2_kernel<256>, 2 * pairs, 256, Gemm2Cfg<256>::kSmemBytes, d->lp, false, 2, s.tma_a,
+                          s.tma_b, s.tma_c, p));
       return 0;
     }
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount - d->lp_sm_reserve)));
@@ -1419,6 +1438,11 @@ int ms_debug_stamps(ms_dev* d, int enable, unsigned long long* out, size_t n) {
 
 uint64_t ms_lp_total_tiles(ms_dev* d, int id) {
   return (d && id >= 0 && id < MS_MAX_LP && d->lp_slots[id].used) ? d->lp_slots[id].total_tiles : 0;
+}
+
+int ms_lp_tile_ctas(ms_dev* d, int id) {
+  if (!d || id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP kernel id");
+  return d->lp_slots[id].pair ? 2 : 1;
 }
 
 uint64_t ms_lp_progress(ms_dev* d, int id) {

@@ -89,11 +89,16 @@ __device__ __forceinline__ void st_relaxed_sys_v2(uint64_t* p, uint64_t a, uint6
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+// Shared-window volatile access (LDS/STS).  A volatile access through a generic pointer
+// compiles to LD.E.STRONG.SYS / ST.E.STRONG.SYS, which the per-k-block preempt checks of
+// the MMA issue loop then pay on every k-block.
 __device__ __forceinline__ uint32_t ld_volatile_smem(const uint32_t* p) {
-  return *reinterpret_cast<const volatile uint32_t*>(p);
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
 }
 __device__ __forceinline__ void st_volatile_smem(uint32_t* p, uint32_t v) {
-  *reinterpret_cast<volatile uint32_t*>(p) = v;
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 // ---- mbarrier -------------------------------------------------------------------

@@ -319,9 +319,9 @@ struct PullParams {
   MsHpCtl* hp_ctl;
   unsigned int* done;    // CTAs finished (self-resetting)
 };
-constexpr int kPullThreads = 256, kPullCtas = 7, kPullUnroll = 8;
+constexpr int kPullThreads = 256, kPullCtas = 7, kPullUnroll = 4;
 
-__global__ void __launch_bounds__(kPullThreads) hp_pull_kernel(const __grid_constant__ PullParams p) {
+__global__ void __launch_bounds__(kPullThreads, kPullCtas) hp_pull_kernel(const __grid_constant__ PullParams p) {
   pdl_launch_dependents();  // the chain kernel may become resident now; it waits for our completion
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * kPullThreads;
   for (unsigned long long i0 = blockIdx.x * static_cast<unsigned long long>(kPullThreads) + threadIdx.x; i0 < p.n16;

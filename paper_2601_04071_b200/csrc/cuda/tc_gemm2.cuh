@@ -3,54 +3,81 @@
 //
 //   C[M, N] (bf16) = A[M, K] * B[N, K]^T, bf16 in, fp32 accumulate in TMEM; 256 x 256 tiles.
 //
-// Why pairs: a single-CTA 128 x 256 x 64 k-block moves 48 KB into shared memory and reads
-// 48 KB back into the tensor core every 512 MMA cycles — ~192 B/clk of smem traffic against
-// ~128 B/clk available, which held the single-CTA kernel at ~72% tensor-pipe activity
-// (profiles/r01_ncu_gemm_details.csv).  With cta_group::2 the two SMs of a TPC run one
-// M=256 x N=256 UMMA: each CTA stages only its 128 rows of A and its 128 columns of B
-// (32 KB per k-block), so the smem traffic halves and a 6-stage ring fits in 192 KB.
+// Why pairs: a single-CTA 128 x 256 x 64 k-block moves 48 KB into one SM's shared memory
+// per 512 MMA cycles; the pair's M=256 x N=256 UMMA needs only each CTA's 128 rows of A and
+// 128 columns of B (32 KB per SM per k-block), which is what cuBLAS's own B200 kernel for
+// this shape does (nvjet ..._256x256_64x4_2x1_2cta: 96% tensor-pipe activity vs 72-78% for
+// the single-CTA kernel, profiles/r02_ncu_gemm_vs_cublas.txt).
 //
-// Roles (256 threads per CTA, cluster of 2; rank 0 = leader):
-//   leader warp 0  : tile scheduler + TMA producer; decides every stage (load / abort /
-//                    end) and forwards the decision to the peer through DSMEM (command word +
-//                    remote mbarrier arrive), so both CTAs always agree on a preemption point
-//   peer   warp 0  : command follower: issues its half of each stage's TMA loads, completing
-//                    their bytes on the LEADER's full barrier (cp.async.bulk.tensor .cta_group::2)
-//   leader warp 1  : single-thread UMMA issuer (tcgen05.mma.cta_group::2, M=256, N=256, K=16);
-//                    accumulator-ready commits multicast to both CTAs
-//   warp 2         : TMEM allocator (cta_group::2, 512 columns = 2 x 256 fp32 accumulators);
-//                    leader lane 0 then polls the preempt epoch
-//   warp 3 (CTA 0) : host poller
-//   warps 4-7      : epilogue of this CTA's 128 rows (tcgen05.ld -> bf16 -> TMA store)
-// Preemption semantics are those of tc_gemm.cuh (tile claim counter, abort at a k-block,
-// abandoned tiles on the redo list, C written only for complete tiles); tile ids count
-// 256 x 256 pair tiles.
+// Steady state has no per-stage cross-CTA messages (the round-1 pair kernel sent every
+// stage's command from the leader to the peer and ran at parity with the single kernel):
+//   leader warp 0 : claims a tile, announces {tile, first ring position} to the peer (one
+//                   DSMEM store + remote arrive per TILE), then streams its halves of A/B
+//                   into its ring; it arms each stage's full barrier for BOTH CTAs' bytes
+//   peer   warp 0 : on each announcement streams its halves into its own ring, completing
+//                   the bytes on the leader's full barrier (cp.async.bulk.tensor .cta_group::2);
+//                   it waits only on its own empty barriers
+//   leader warp 1 : single-thread UMMA issuer (tcgen05.mma.cta_group::2, M=256, N=256, K=16);
+//                   every commit is multicast to both CTAs' empty barriers, accumulator-ready
+//                   commits to both CTAs' tmem_full barriers
+//   warp 2        : TMEM allocator (cta_group::2, 512 columns = 2 x 256 fp32 accumulators);
+//                   leader lane 0 then polls the preempt epoch
+//   warp 3 (CTA 0): host poller
+//   warps 4-7     : epilogue of this CTA's 128 rows (tcgen05.ld -> bf16 -> TMA store)
+//
+// Preemption (same semantics as tc_gemm.cuh: claim counter, abort at a k-block, abandoned
+// tiles on the redo list, C written only for complete tiles).  The two producers run ahead
+// independently, so they must agree where the aborted tile's stream ends before either
+// moves on: the leader stops at k-block L, asks the peer to stop, the peer answers with the
+// k-block P it stopped at (or num_kb if it had issued everything).  Ring positions [P, L)
+// were armed for both halves but get only the leader's: the leader completes the missing
+// bytes itself (mbarrier.complete_tx); positions [L, P) get only the peer's bytes: the
+// leader arms them for those bytes and flags them "discard"; then one terminal position ends
+// the tile.  The MMA warp consumes every position (no MMAs once aborted) and releases it in
+// both CTAs, so both rings stay phase-aligned; the next announcement carries the ring
+// position both producers resume from.
 #pragma once
 
 #include "tc_gemm.cuh"
 
 namespace msdev {
 
+// TN = pair tile width: 256 (one M=256 x N=256 UMMA per k-step, two accumulators in TMEM)
+// or 512 (two UMMAs per k-step over the tile's column halves; the accumulator fills all 512
+// TMEM columns, so the epilogue of tile j and the MMAs of tile j+1 do not overlap, but each
+// SM stages 48 KB per 1024 MMA cycles instead of 32 KB per 512 — the shape of cuBLAS's own
+// kernel for 8192^3 on this part).
+template <int TN>
 struct Gemm2Cfg {
-  static constexpr int kHalfBytes = 128 * kBK * 2;  // 16 KB: 128 rows (A) or columns (B) x 64 k
-  static constexpr int kStageBytes = 2 * kHalfBytes;
-  static constexpr int kStages = 6;
+  static constexpr int kHalfBytes = 128 * kBK * 2;      // 16 KB: 128 rows (A) or columns (B) x 64 k
+  static constexpr int kBHalves = TN / 256;             // UMMAs (N = 256) per k-step
+  static constexpr int kStageBytes = (1 + kBHalves) * kHalfBytes;  // one CTA's bytes of a k-block
+  static constexpr int kStages = TN == 256 ? 6 : 4;
+  static constexpr int kSlots = 512 / TN;               // accumulators in TMEM
   static constexpr int kTmemCols = 512;
   static constexpr int kCStageBytes = 4 * 2 * 32 * 64;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kCStageBytes + 1024;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(256, 256);
 };
+constexpr int kGemm2MaxStages = 6;
 
+// Stage flags (leader): 0 data, 1 data + last k-block, 2 terminal (no data), 3 peer-only
+// bytes of an aborted tile (discard).
 struct Gemm2Ctl {
-  uint64_t full[Gemm2Cfg::kStages];   // leader: one arrive_expect_tx + both CTAs' TMA bytes
-  uint64_t empty[Gemm2Cfg::kStages];  // leader: MMA commit (both CTAs' stage reads done)
-  uint64_t go[Gemm2Cfg::kStages];     // peer: leader's command for this stage
-  uint64_t tmem_full[2], tmem_empty[2], tile_full[2], tile_empty[2];
+  uint64_t full[kGemm2MaxStages];   // leader: producer's arrive.expect_tx + both CTAs' TMA bytes
+  uint64_t empty[kGemm2MaxStages];  // both: MMA commit multicast (or the abort path's arrives)
+  uint64_t tile_full[2];              // both: tile announcement
+  uint64_t tile_empty[2];             // leader: both epilogues
+  uint64_t tmem_full[2];              // both: accumulator ready / aborted
+  uint64_t tmem_empty[2];             // leader: both epilogues
+  uint64_t stop_bar;                  // leader: the peer's stop report
   uint64_t mma_drain;
   long long tile_id[2];
-  alignas(16) int4 cmd[Gemm2Cfg::kStages];  // peer: {tile lo, tile hi, kb, 0}; tile -1 skip, -2 end
+  uint32_t tile_start[2];  // ring position of the tile's first k-block
   uint32_t tile_abort[2];
-  uint32_t stage_flag[Gemm2Cfg::kStages];  // leader: 0 data, 1 data + last k-block, 2 aborted
+  uint32_t stage_flag[kGemm2MaxStages];
+  uint32_t stop_req;   // peer: ordinal (j + 1) of the tile the leader asks it to stop
+  uint32_t peer_stop;  // leader: k-block at which the peer stopped
   uint32_t tmem_base;
   uint32_t preempt;
   uint32_t producer_done;
@@ -114,15 +141,54 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_complete_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait for the barrier phase unless *flag == want first (then false).
+__device__ __forceinline__ bool mbar_wait_unless(uint64_t* bar, uint32_t parity, const uint32_t* flag,
+                                                 uint32_t want) {
+  for (;;) {
+    if (mbar_try_wait(bar, parity)) return true;
+    if (flag && ld_volatile_smem(flag) == want) return false;
+  }
+}
+
+template <int TN>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ GemmParams p) {
-  using Cfg = Gemm2Cfg;
+  using Cfg = Gemm2Cfg<TN>;
   constexpr int S = Cfg::kStages;
+  constexpr int NS = Cfg::kSlots;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;                              // [S][128 x 64] bf16, SW128
-  uint8_t* smem_b = smem + S * Cfg::kHalfBytes;        // [S][128 x 64] bf16, SW128
+  uint8_t* smem_b = smem + S * Cfg::kHalfBytes;        // [S][kBHalves][128 x 64] bf16, SW128
   uint8_t* smem_c = smem + S * Cfg::kStageBytes;
   Gemm2Ctl* s = reinterpret_cast<Gemm2Ctl*>(smem_c + Cfg::kCStageBytes);
 
@@ -140,15 +206,17 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < S; ++i) {
       mbar_init(&s->full[i], 1);
       mbar_init(&s->empty[i], 1);
-      mbar_init(&s->go[i], 1);
+      s->stage_flag[i] = 0;
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s->tmem_full[i], 1);
-      mbar_init(&s->tmem_empty[i], 2);  // both CTAs' epilogues
       mbar_init(&s->tile_full[i], 1);
       mbar_init(&s->tile_empty[i], 2);  // both CTAs' epilogues
+      mbar_init(&s->tmem_full[i], 1);
+      mbar_init(&s->tmem_empty[i], 2);  // both CTAs' epilogues
     }
+    mbar_init(&s->stop_bar, 1);
     mbar_init(&s->mma_drain, 1);
+    s->stop_req = 0;
     s->preempt = 0;
     s->producer_done = 0;
     s->tiles_done = 0;
@@ -166,92 +234,122 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = s->tmem_base;
   const int num_kb = p.k / kBK;
-  if (!leader && threadIdx.x == 0)
-    for (int i = 0; i < S; ++i) mbar_arrive_expect_tx(&s->go[i], 16);  // first command of each slot
 
   if (warp == 0) {
-    if (lane == 0) {
-      if (leader) {
-        // ===================== leader: scheduler + producer + peer commands =====================
-        uint32_t stage = 0, phase = 0;
-        const uint32_t peer_cmd = mapa_shared(smem_u32(&s->cmd[0]), 1);
-        const uint32_t peer_go = mapa_shared(smem_u32(&s->go[0]), 1);
-        const uint32_t peer_tile_id = mapa_shared(smem_u32(&s->tile_id[0]), 1);
-        const uint32_t peer_tile_abort = mapa_shared(smem_u32(&s->tile_abort[0]), 1);
-        const uint32_t peer_tile_full = mapa_shared(smem_u32(&s->tile_full[0]), 1);
-        // Command to the peer: load (tile, kb) / skip (-1) / end (-2).  One 16-byte st.async
-        // carries the data and completes the peer's go barrier (no release fence: a
-        // release.cluster arrive costs a MEMBAR.GPU per stage, which capped this loop at one
-        // stage per ~0.9 us).
-        auto command = [&](long long tile, int kb) {
-          const unsigned long long t = static_cast<unsigned long long>(tile);
-          st_async_v4(peer_cmd + stage * 16, static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
-                      static_cast<uint32_t>(kb), 0u, peer_go + stage * 8);
-        };
-        for (int j = 0;; ++j) {
-          const int slot = j & 1;
-          if (j >= 2) mbar_wait_cluster(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
-          long long tile = -1;
-          if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
-          s->tile_id[slot] = tile;
-          s->tile_abort[slot] = 0;
-          st_cluster_u64(peer_tile_id + slot * 8, static_cast<unsigned long long>(tile));
-          st_cluster_u32(peer_tile_abort + slot * 4, 0u);
-          mbar_arrive(&s->tile_full[slot]);
-          mbar_arrive_cluster(peer_tile_full + slot * 8);
-          if (tile < 0) {
-            command(-2, 0);  // the peer's producer leaves (its stage counter is not reused)
+    if (lane == 0 && leader) {
+      // ===================== leader: tile scheduler + producer =====================
+      const uint32_t peer_tile_id = mapa_shared(smem_u32(&s->tile_id[0]), 1);
+      const uint32_t peer_tile_start = mapa_shared(smem_u32(&s->tile_start[0]), 1);
+      const uint32_t peer_tile_abort = mapa_shared(smem_u32(&s->tile_abort[0]), 1);
+      const uint32_t peer_tile_full = mapa_shared(smem_u32(&s->tile_full[0]), 1);
+      const uint32_t peer_stop_req = mapa_shared(smem_u32(&s->stop_req), 1);
+      uint32_t pos = 0, stop_phase = 0;
+      for (int j = 0;; ++j) {
+        const int slot = j & 1;
+        if (j >= 2) mbar_wait_cluster(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
+        long long tile = -1;
+        if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
+        s->tile_id[slot] = tile;
+        s->tile_start[slot] = pos;
+        s->tile_abort[slot] = 0;
+        st_cluster_u64(peer_tile_id + slot * 8, static_cast<unsigned long long>(tile));
+        st_cluster_u32(peer_tile_start + slot * 4, pos);
+        st_cluster_u32(peer_tile_abort + slot * 4, 0u);
+        mbar_arrive(&s->tile_full[slot]);
+        mbar_arrive_cluster(peer_tile_full + slot * 8);  // release.cluster: the stores above first
+        if (tile < 0) break;
+        int mb, nb;
+        tile_coords(tile, p, mb, nb);
+        const uint32_t pos0 = pos;
+        int lead_stop = num_kb;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const bool may_stop = p.run.preemptible && kb > 0;
+          if (may_stop && ld_volatile_smem(&s->preempt)) {
+            lead_stop = kb;
             break;
           }
-          int mb, nb;
-          tile_coords(tile, p, mb, nb);
-          for (int kb = 0; kb < num_kb; ++kb) {
-            const bool abort = p.run.preemptible && kb > 0 && ld_volatile_smem(&s->preempt);
-            mbar_wait(&s->empty[stage], phase ^ 1);
-            if (abort) {
-              s->stage_flag[stage] = 2;  // the MMA warp owns the redo push for this tile
-              command(-1, kb);
-              mbar_arrive(&s->full[stage]);
-            } else {
-              s->stage_flag[stage] = (kb == num_kb - 1) ? 1u : 0u;
-              mbar_arrive_expect_tx(&s->full[stage], 2 * Cfg::kStageBytes);  // before any peer byte lands
-              command(tile, kb);
-              const uint32_t fb = smem_u32(&s->full[stage]);
-              tma_load_2d_pair(smem_u32(smem_a + stage * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256);
-              tma_load_2d_pair(smem_u32(smem_b + stage * Cfg::kHalfBytes), &tma_b, fb, kb * kBK, nb * 256);
-            }
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1;
-            }
-            if (abort) break;
+          const uint32_t st = pos % S;
+          if (!mbar_wait_unless(&s->empty[st], ((pos / S) & 1) ^ 1, may_stop ? &s->preempt : nullptr, 1u)) {
+            lead_stop = kb;
+            break;
           }
+          s->stage_flag[st] = (kb == num_kb - 1) ? 1u : 0u;
+          mbar_arrive_expect_tx(&s->full[st], 2 * Cfg::kStageBytes);  // both CTAs' halves
+          const uint32_t fb = smem_u32(&s->full[st]);
+          tma_load_2d_pair(smem_u32(smem_a + st * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256);
+#pragma unroll
+          for (int h = 0; h < Cfg::kBHalves; ++h)
+            tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
+                             nb * TN + h * 256);
+          ++pos;
         }
-      } else {
-        // ===================== peer: follow the leader's stage commands =====================
-        uint32_t stage = 0, phase = 0;
-        for (;;) {
-          mbar_wait(&s->go[stage], phase);
-          uint32_t c0, c1, c2, c3;
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(c0), "=r"(c1), "=r"(c2), "=r"(c3)
-                       : "r"(smem_u32(&s->cmd[stage]))
-                       : "memory");
-          const long long tile = static_cast<long long>((static_cast<unsigned long long>(c1) << 32) | c0);
-          const int kb = static_cast<int>(c2);
-          (void)c3;
-          if (tile == -2) break;
-          mbar_arrive_expect_tx(&s->go[stage], 16);  // arm the slot's next command
-          if (tile >= 0) {
-            int mb, nb;
-            tile_coords(tile, p, mb, nb);
-            const uint32_t fb = mapa_shared(smem_u32(&s->full[stage]), 0);
-            tma_load_2d_pair(smem_u32(smem_a + stage * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256 + 128);
-            tma_load_2d_pair(smem_u32(smem_b + stage * Cfg::kHalfBytes), &tma_b, fb, kb * kBK, nb * 256 + 128);
+        if (lead_stop < num_kb) {
+          // agree on the end of this tile's stream with the peer (see the header)
+          st_cluster_u32(peer_stop_req, static_cast<uint32_t>(j + 1));
+          mbar_wait_cluster(&s->stop_bar, stop_phase);
+          stop_phase ^= 1;
+          const int ps = static_cast<int>(ld_volatile_smem(&s->peer_stop));
+          for (int kb = ps; kb < lead_stop; ++kb)  // armed for both halves, the peer's never comes
+            mbar_complete_tx(&s->full[(pos0 + kb) % S], Cfg::kStageBytes);
+          for (int kb = lead_stop; kb < ps; ++kb) {  // only the peer's half comes
+            const uint32_t st = pos % S;
+            mbar_wait(&s->empty[st], ((pos / S) & 1) ^ 1);
+            s->stage_flag[st] = 3u;
+            mbar_arrive_expect_tx(&s->full[st], Cfg::kStageBytes);
+            ++pos;
           }
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
+          const uint32_t st = pos % S;  // terminal position: ends the tile for the MMA warp
+          mbar_wait(&s->empty[st], ((pos / S) & 1) ^ 1);
+          s->stage_flag[st] = 2u;
+          mbar_arrive(&s->full[st]);
+          ++pos;
+        }
+      }
+      st_volatile_smem(&s->producer_done, 1u);
+      dbg_stamp(p.run, 1);
+    } else if (lane == 0) {
+      // ===================== peer: producer of its halves =====================
+      const uint32_t lead_peer_stop = mapa_shared(smem_u32(&s->peer_stop), 0);
+      const uint32_t lead_stop_bar = mapa_shared(smem_u32(&s->stop_bar), 0);
+      auto report = [&](int kb) {
+        st_cluster_u32(lead_peer_stop, static_cast<uint32_t>(kb));
+        mbar_arrive_cluster(lead_stop_bar);  // release.cluster: the store above first
+      };
+      mbar_wait_cluster(&s->tile_full[0], 0);
+      for (int j = 0;; ++j) {
+        const int slot = j & 1;
+        const long long tile = *reinterpret_cast<volatile long long*>(&s->tile_id[slot]);
+        if (tile < 0) break;
+        uint32_t pos = *reinterpret_cast<volatile uint32_t*>(&s->tile_start[slot]);
+        int mb, nb;
+        tile_coords(tile, p, mb, nb);
+        const uint32_t ord = static_cast<uint32_t>(j + 1);
+        bool reported = false;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const uint32_t st = pos % S;
+          if (!mbar_wait_unless(&s->empty[st], ((pos / S) & 1) ^ 1, &s->stop_req, ord) ||
+              ld_volatile_smem(&s->stop_req) == ord) {
+            report(kb);
+            reported = true;
+            break;
+          }
+          const uint32_t fb = mapa_shared(smem_u32(&s->full[st]), 0);
+          tma_load_2d_pair(smem_u32(smem_a + st * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256 + 128);
+#pragma unroll
+          for (int h = 0; h < Cfg::kBHalves; ++h)
+            tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
+                             nb * TN + h * 256 + 128);
+          ++pos;
+        }
+        // Next announcement; a stop request for this tile that comes after every k-block was
+        // issued is answered with num_kb.
+        const int ns = (j + 1) & 1;
+        const uint32_t np = static_cast<uint32_t>(((j + 1) >> 1) & 1);
+        for (;;) {
+          if (mbar_try_wait_cluster(&s->tile_full[ns], np)) break;
+          if (!reported && ld_volatile_smem(&s->stop_req) == ord) {
+            report(num_kb);
+            reported = true;
           }
         }
       }
@@ -260,50 +358,50 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     // ===================== leader: UMMA issuer (cta_group::2) =====================
     if (lane == 0 && leader) {
-      uint32_t stage = 0, phase = 0, drain_phase = 0;
+      uint32_t pos = 0, drain_phase = 0;
       const int lag = p.run.preemptible ? p.mma_lag : 0;  // see tc_gemm.cuh
-      int consumed = 0;
+      uint32_t consumed = 0;
       const uint32_t peer_tile_abort = mapa_shared(smem_u32(&s->tile_abort[0]), 1);
       const uint32_t peer_tmem_full = mapa_shared(smem_u32(&s->tmem_full[0]), 1);
+      const uint32_t peer_empty = mapa_shared(smem_u32(&s->empty[0]), 1);
       for (int j = 0;; ++j) {
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
         if (s->tile_id[slot] < 0) break;
-        if (j >= 2) mbar_wait_cluster(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);
+        const int ts = j % NS;  // accumulator slot
+        if (j >= NS) mbar_wait_cluster(&s->tmem_empty[ts], ((j / NS) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(slot * 256);
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(ts * TN);
         bool aborted = false;
         for (int kb = 0;; ++kb) {
-          mbar_wait(&s->full[stage], phase);
+          const uint32_t st = pos % S;
+          mbar_wait(&s->full[st], (pos / S) & 1);
           tc_fence_after();
-          const uint32_t flag = s->stage_flag[stage];
+          const uint32_t flag = s->stage_flag[st];
           if (!aborted && p.run.preemptible && ld_volatile_smem(&s->preempt)) aborted = true;
-          if (flag == 2) aborted = true;
+          if (flag >= 2) aborted = true;
           if (aborted) {
-            mbar_arrive(&s->empty[stage]);
+            // no MMA reads this position: release it in both CTAs
+            mbar_arrive(&s->empty[st]);
+            mbar_arrive_remote_relaxed(peer_empty + st * 8);
           } else {
-            if (lag > 0 && consumed >= lag) {
-              int ps = static_cast<int>(stage) - lag;
-              uint32_t pp = phase;
-              if (ps < 0) {
-                ps += S;
-                pp ^= 1;
-              }
-              mbar_wait(&s->empty[ps], pp);
+            if (lag > 0 && consumed >= static_cast<uint32_t>(lag)) {
+              const uint32_t bp = pos - lag;
+              mbar_wait(&s->empty[bp % S], (bp / S) & 1);
             }
-            const uint64_t a0 = umma_desc_k_sw128(smem_u32(smem_a + stage * Cfg::kHalfBytes));
-            const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + stage * Cfg::kHalfBytes));
+            const uint64_t a0 = umma_desc_k_sw128(smem_u32(smem_a + st * Cfg::kHalfBytes));
 #pragma unroll
             for (int k = 0; k < kBK / kUmmaK; ++k)
-              umma_bf16_pair(d_tmem, a0 + 2ull * k, b0 + 2ull * k, Cfg::kIdesc, (kb | k) != 0 ? 1u : 0u);
-            umma_commit_pair(&s->empty[stage]);
+#pragma unroll
+              for (int h = 0; h < Cfg::kBHalves; ++h) {
+                const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes));
+                umma_bf16_pair(d_tmem + h * 256, a0 + 2ull * k, b0 + 2ull * k, Cfg::kIdesc, (kb | k) != 0 ? 1u : 0u);
+              }
+            umma_commit_pair_mc(&s->empty[st], 0x3);
           }
           ++consumed;
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
-          if (flag != 0) break;
+          ++pos;
+          if (flag == 1 || flag == 2) break;
         }
         if (aborted) {
           umma_commit_pair(&s->mma_drain);
@@ -312,12 +410,13 @@ __global__ void __launch_bounds__(256, 1)
           push_redo(p.run, static_cast<unsigned long long>(s->tile_id[slot]));
           s->tile_abort[slot] = 1;
           st_cluster_u32(peer_tile_abort + slot * 4, 1u);
-          mbar_arrive(&s->tmem_full[slot]);
-          mbar_arrive_cluster(peer_tmem_full + slot * 8);
+          mbar_arrive(&s->tmem_full[ts]);
+          mbar_arrive_cluster(peer_tmem_full + ts * 8);  // release.cluster: the abort flag first
         } else {
-          umma_commit_pair_mc(&s->tmem_full[slot], 0x3);
+          umma_commit_pair_mc(&s->tmem_full[ts], 0x3);
         }
       }
+      dbg_stamp(p.run, 2);
     }
   } else if (warp == 2) {
     if (lane == 0 && leader && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->producer_done);
@@ -335,7 +434,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait_cluster(&s->tile_full[slot], (j >> 1) & 1);
       const long long tile = *reinterpret_cast<volatile long long*>(&s->tile_id[slot]);
       if (tile < 0) break;
-      mbar_wait_cluster(&s->tmem_full[slot], (j >> 1) & 1);
+      const int ts = j % NS;
+      mbar_wait_cluster(&s->tmem_full[ts], (j / NS) & 1);
       tc_fence_after();
       const bool keep = !*reinterpret_cast<volatile uint32_t*>(&s->tile_abort[slot]);
       if (keep) {
@@ -343,9 +443,9 @@ __global__ void __launch_bounds__(256, 1)
         tile_coords(tile, p, mb, nb);
         const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
 #pragma unroll 1
-        for (int c0 = 0; c0 < 256; c0 += 32) {
+        for (int c0 = 0; c0 < TN; c0 += 32) {
           uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * 256 + c0), r);
+          tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(ts * TN + c0), r);
           tmem_ld_wait();
           uint8_t* cbuf = smem_c + (q * 2 + cbuf_idx) * (32 * 64);
           if (lane == 0) bulk_wait_read<1>();
@@ -362,7 +462,7 @@ __global__ void __launch_bounds__(256, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tma_c, cbuf, nb * 256 + c0, row0);
+            tma_store_2d(&tma_c, cbuf, nb * TN + c0, row0);
             bulk_commit();
           }
           cbuf_idx ^= 1;
@@ -372,17 +472,19 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_before();
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (q == 0 && lane == 0) {
-        mbar_arrive_cluster(lead_tmem_empty + slot * 8);
+        mbar_arrive_cluster(lead_tmem_empty + ts * 8);
         mbar_arrive_cluster(lead_tile_empty + slot * 8);
       }
     }
     if (lane == 0) bulk_wait_read<0>();
+    if (q == 0 && lane == 0) dbg_stamp(p.run, 3);
   }
 
   tc_fence_before();
   cluster_sync_all();  // no CTA frees TMEM or leaves while its peer may still signal it
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
+  if (threadIdx.x == 0) dbg_stamp(p.run, 4);
   if (threadIdx.x == 0) cta_exit(p.run, s->tiles_done);
 }
 

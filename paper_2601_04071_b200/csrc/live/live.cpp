@@ -85,6 +85,7 @@ struct LpTask {
   uint64_t total = 0, cursor = 0;
   uint64_t redo = 0;
   Ns tile_ns = 50000;
+  int tile_ctas = 1;  // SMs one tile occupies (ms_lp_tile_ctas)
 };
 
 // Host clock of the device layer (CLOCK_MONOTONIC; the ring / raise timestamps use the same
@@ -114,7 +115,7 @@ class LiveRun {
     // `small_bubble_sms` > 0 caps LP at that many SMs while harvesting a bubble INSIDE an HP
     // request (hint bubbles), so the co-running GEMM draws less power between HP iterations
     // and the HP chain keeps its clocks (B200 runs into its 1 kW cap under a full-GPU GEMM).
-    base_reserve_ = opts.value("lp_sm_reserve", 1);
+    base_reserve_ = opts.value("lp_sm_reserve", 0);
     small_sms_ = opts.value("small_bubble_sms", 0);
     max_sms_ = opts.value("lp_max_sms", 0);  // > 0: LP never uses more SMs (power budget)
     // Hint bubbles are harvested up to their predicted end / safety and not extended past
@@ -427,6 +428,7 @@ class LiveRun {
     l.tile_ns = tile_ns_.contains(l.kernel) ? tile_ns_.at(l.kernel).get<Ns>() : 50000;
     check(ms_lp_reset(dev_, l.dev_id), "ms_lp_reset");
     l.total = ms_lp_total_tiles(dev_, l.dev_id);
+    l.tile_ctas = std::max(1, ms_lp_tile_ctas(dev_, l.dev_id));
     l.cursor = 0;
     l.redo = 0;
     l.has_parent = true;
@@ -437,7 +439,9 @@ class LiveRun {
   // divided by the safety factor (consolidation_prefix sizing, scheduler.hpp:66-85).
   uint64_t batch_tiles(const LpTask& l, Ns gap) const {
     const double waves = static_cast<double>(gap) / sc_.sched.safety_factor / static_cast<double>(l.tile_ns);
-    const uint64_t t = static_cast<uint64_t>(std::max(1.0, std::floor(waves)) * lp_sms());
+    // one wave covers lp_sms() / (SMs per tile) tiles (2 SMs per tile on CTA pairs)
+    const int per = std::max(1, l.tile_ctas);
+    const uint64_t t = static_cast<uint64_t>(std::max(1.0, std::floor(waves)) * std::max(1, lp_sms() / per));
     return t;
   }
   // SMs the next LP launch may use
@@ -571,7 +575,7 @@ class LiveRun {
   bool harvest_ = false, reef_ = false, reef_req_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
   bool direct_hp_ = false, calibrate_ = true;
   int debug_runs_ = 0;
-  int base_reserve_ = 1, small_sms_ = 0, max_sms_ = 0;
+  int base_reserve_ = 0, small_sms_ = 0, max_sms_ = 0;
   bool bound_hints_ = false;
   double hint_quantile_ = -1.0;  // < 0: size hint harvests from the hint's mean
   std::unique_ptr<PowerGovernor> governor_;

@@ -103,7 +103,7 @@ def lib() -> C.CDLL:
             "ms_preempt_raise": (I, [P, C.POINTER(U32), C.POINTER(I64)]), "ms_preempt_epoch": (U32, [P]),
             "ms_hp_register_chain": (I, [P, C.POINTER(HpOp), I, C.POINTER(I)]),
             "ms_hp_arm": (I, [P, I, U32]), "ms_hp_ring": (I, [P, U32, C.POINTER(I64)]),
-            "ms_hp_next_seq": (U32, [P]), "ms_lp_total_tiles": (U64, [P, I]), "ms_lp_progress": (U64, [P, I]),
+            "ms_hp_next_seq": (U32, [P]), "ms_lp_total_tiles": (U64, [P, I]), "ms_lp_tile_ctas": (I, [P, I]), "ms_lp_progress": (U64, [P, I]),
             "ms_lp_run_ex": (I, [P, I, U64, U64, U64, I]), "ms_lp_unregister": (I, [P, I]),
             "ms_debug_stamps": (I, [P, I, C.POINTER(C.c_ulonglong), C.c_size_t]),
             "ms_set_lp_sm_reserve": (I, [P, I]),
@@ -139,6 +139,7 @@ def host_now_ns() -> int:
 class LpKernel:
     id: int
     total_tiles: int
+    tile_ctas: int = 1  # SMs one tile occupies (2: GEMM on CTA pairs)
 
 
 class Device:
@@ -227,7 +228,7 @@ class Device:
     def _lp_register(self, d: LpDesc) -> LpKernel:
         kid, tiles = C.c_int(), C.c_uint64()
         _ck(lib().ms_lp_register(self._h, C.byref(d), C.byref(kid), C.byref(tiles)))
-        return LpKernel(kid.value, tiles.value)
+        return LpKernel(kid.value, tiles.value, _ck(lib().ms_lp_tile_ctas(self._h, kid.value)))
 
     def lp_set_slow_tiles(self, k: LpKernel, slow_groups, tiles_per_group: int, max_inflight: int = 8):
         """Memory tier: bound the streamer's in-flight tiles over off-device chunks

@@ -93,13 +93,14 @@ class Config1:
         scenario carries as KernelSpec.measured_time — the reference's measured execution
         oracle for split plans (engine.hpp:461-481, splitter.hpp:141-207)."""
         ms_gemm = self.dev.lp_time_full(self.lp, reps)
-        waves = math.ceil(self.lp.total_tiles / self.dev.info["sm_count"])
+        waves = math.ceil(self.lp.total_tiles / (self.dev.info["sm_count"] // self.lp.tile_ctas))
         ms_chain = self.dev.hp_time_chain(self.chain, 20)
         tile_ns = int(ms_gemm * 1e6 / waves)
         self.calib = {
             "lp_gemm_ms": ms_gemm,
             "lp_gemm_tile_ns": tile_ns,
             "lp_gemm_tiles": int(self.lp.total_tiles),
+            "lp_gemm_tile_ctas": int(self.lp.tile_ctas),
             "hp_chain_ms": ms_chain,
             "hp_gemm_tile_ns": int(ms_chain * 1e6 * 0.95 / 4),
             "hp_ew_tile_ns": max(1000, int(ms_chain * 1e6 * 0.05)),
@@ -107,7 +108,7 @@ class Config1:
         if profile:
             from . import profiler
             sm = self.dev.info["sm_count"]
-            spec = profiler.profile_lp_kernel(self.dev, self.lp, "lp_gemm_8192", sm - 1,
+            spec = profiler.profile_lp_kernel(self.dev, self.lp, "lp_gemm_8192", sm // self.lp.tile_ctas,
                                               scenarios.DEFAULT_CALIB["lp_gemm_tile_bytes"], reps=2)
             self.calib["lp_gemm_measured_time"] = spec["measured_time"]
         return self.calib
@@ -218,8 +219,9 @@ class Config4:
         self.calib = {
             "lp_gemm_ms": ms_gemm, "lp_axpy_ms": ms_axpy, "hp_step_ms": ms_chain,
             "hp_weight_gbs": self.weight_bytes / (ms_chain * 1e-3) / 1e9,
-            "lp_gemm_tile_ns": int(ms_gemm * 1e6 / math.ceil(self.lp_gemm.total_tiles / sm)),
+            "lp_gemm_tile_ns": int(ms_gemm * 1e6 / math.ceil(self.lp_gemm.total_tiles / (sm // self.lp_gemm.tile_ctas))),
             "lp_gemm_tiles": int(self.lp_gemm.total_tiles),
+            "lp_gemm_tile_ctas": int(self.lp_gemm.tile_ctas),
             # one "tile" of the pacing model = one tile per SM per wave
             "lp_ew_tile_ns": int(ms_axpy * 1e6 / math.ceil(self.lp_axpy.total_tiles / sm)),
             "lp_ew_tiles": int(self.lp_axpy.total_tiles),
@@ -230,7 +232,7 @@ class Config4:
         # on-B200 profiles -> KernelSpec.measured_time of both LP kernels (profiler.py)
         from . import profiler
         self.calib["lp_gemm_measured_time"] = profiler.profile_lp_kernel(
-            self.dev, self.lp_gemm, "lp_gemm_8192", sm - 1, scenarios.DEFAULT_CALIB["lp_gemm_tile_bytes"],
+            self.dev, self.lp_gemm, "lp_gemm_8192", sm // self.lp_gemm.tile_ctas, scenarios.DEFAULT_CALIB["lp_gemm_tile_bytes"],
             reps=1)["measured_time"]
         self.calib["lp_ew_measured_time"] = profiler.profile_lp_kernel(
             self.dev, self.lp_axpy, "lp_axpy_1g", 3 * (sm - 1), 6 * 8192, reps=1)["measured_time"]

@@ -58,6 +58,16 @@ def _kernel(name, tiles, tile_ns, tile_bytes, splittable=True, per_sm=1, measure
     return k
 
 
+def _lp_gemm_kernel(c: dict) -> dict:
+    """The LP 8192^3 GEMM.  On CTA pairs (calib lp_gemm_tile_ctas = 2, 256 x 512 tiles) a
+    tile holds two SMs for its tile time T: modelled as one block per SM whose block time is
+    2 T (Eq. 1 capacity 148 x 1/(2T) = 74 tiles per T, the pair grid's real rate)."""
+    ctas = int(c.get("lp_gemm_tile_ctas", 1))
+    tile_bytes = c["lp_gemm_tile_bytes"] if ctas == 1 else (256 + 512) * 8192 * 2 + 256 * 512 * 2
+    return _kernel("lp_gemm_8192", c.get("lp_gemm_tiles", 2048), c["lp_gemm_tile_ns"] * ctas, tile_bytes,
+                   measured_time=c.get("lp_gemm_measured_time"))
+
+
 def config1(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, rate: float = 50.0) -> dict:
     """Config 1: HP small-GEMM-chain inference (Poisson) + LP batch GEMM loop."""
     c = dict(DEFAULT_CALIB, **(calib or {}))
@@ -69,8 +79,7 @@ def config1(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
         "kernels": [
             _kernel("hp_gemm_128x4096x4096", 128, c["hp_gemm_tile_ns"], c["hp_gemm_tile_bytes"], False),
             _kernel("hp_bias_gelu", 128, c["hp_ew_tile_ns"], c["hp_ew_tile_bytes"], False),
-            _kernel("lp_gemm_8192", c.get("lp_gemm_tiles", 2048), c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"],
-                    measured_time=c.get("lp_gemm_measured_time")),
+            _lp_gemm_kernel(c),
         ],
         "tasks": [
             {"name": "hp_infer", "priority": "high", "kind": "serving", "trace": "hp_trace",
@@ -96,8 +105,7 @@ def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
         "kernels": [
             _kernel("hp_decode_layer", 148, c.get("hp_layer_ns", 20_000), 148 * 1024 * 1024 // 148, False),
             _kernel("hp_lm_head", 148, c.get("hp_lm_head_ns", 40_000), 2048 * 128256 * 2 // 148, False),
-            _kernel("lp_gemm_8192", c.get("lp_gemm_tiles", 2048), c["lp_gemm_tile_ns"], c["lp_gemm_tile_bytes"],
-                    measured_time=c.get("lp_gemm_measured_time")),
+            _lp_gemm_kernel(c),
             _kernel("lp_axpy_1g", c.get("lp_ew_tiles", 16384), c["lp_ew_tile_ns"], c["lp_ew_tile_bytes"], per_sm=4,
                     measured_time=c.get("lp_ew_measured_time")),
         ],

@@ -175,6 +175,7 @@ int ms_set_lp_sm_reserve(ms_dev* d, int n) {
 }
 int ms_debug_stamps(ms_dev*, int, unsigned long long*, size_t) { return 0; }
 uint64_t ms_lp_total_tiles(ms_dev* d, int id) { return d->lp[id].used ? d->lp[id].total : 0; }
+int ms_lp_tile_ctas(ms_dev*, int) { return 1; }
 int ms_lp_reset(ms_dev* d, int id) {
   d->lp[id].redo_carry = 0;
   d->lp[id].exited = false;

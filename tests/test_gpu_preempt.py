@@ -87,7 +87,7 @@ def test_budget_bounds_the_run(dev, gemm):
     assert np.array_equal(d2h(dev, c, n * n), ref)
 
 
-@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("pair", [0, 1, 2])  # single CTA / pairs with 256 x 256 / 256 x 512 tiles
 def test_gemm_cta_pair_kernel_preempt_resume(dev, pair):
     """The cta_group::2 LP GEMM (MS_LP_GEMM_PAIR=1, tc_gemm2.cuh) and the single-CTA one
     produce the same bits, uninterrupted and preempted + resumed."""
@@ -105,7 +105,7 @@ def test_gemm_cta_pair_kernel_preempt_resume(dev, pair):
             os.environ.pop("MS_LP_GEMM_PAIR")
         else:
             os.environ["MS_LP_GEMM_PAIR"] = old
-    assert k.total_tiles == (n // 256) ** 2 if pair else (n // 128) * (n // 256)
+    assert k.total_tiles == {0: (n // 128) * (n // 256), 1: (n // 256) ** 2, 2: (n // 256) * (n // 512)}[pair]
     dev.lp_run(k, 0, k.total_tiles)
     dev.lp_wait(k, 30)
     ref = d2h(dev, c, n * n)
@@ -115,7 +115,9 @@ def test_gemm_cta_pair_kernel_preempt_resume(dev, pair):
     while True:
         dev.lp_run(k, begin, k.total_tiles)
         runs += 1
-        spin(15e-6)
+        # raised at different points of the run: the pair's two producers then stop at
+        # different k-blocks in either order (tc_gemm2.cuh stop agreement)
+        spin((2e-6, 15e-6, 40e-6, 7e-6)[runs % 4])
         dev.preempt_raise()
         st = dev.lp_wait(k, 30)
         begin = st["cursor"]

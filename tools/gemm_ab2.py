@@ -73,6 +73,8 @@ dev.fill_synth(b, N * K, 7, 2, 1.0 / 90.5)
 k1 = dev.lp_register_gemm(a, b, c, M, N, K, block_n=256)
 os.environ["MS_LP_GEMM_PAIR"] = "1"
 k2 = dev.lp_register_gemm(a, b, c, M, N, K, block_n=256)
+os.environ["MS_LP_GEMM_PAIR"] = "2"
+k3 = dev.lp_register_gemm(a, b, c, M, N, K, block_n=256)
 del os.environ["MS_LP_GEMM_PAIR"]
 out = {}
 for rnd in range(2):
@@ -85,6 +87,14 @@ for rnd in range(2):
     del os.environ["MS_LP_MMA_LAG"]
     r["pair"] = ours_preemptible(dev, k2); time.sleep(1)
     r["pair_np"] = ours_np(dev, k2); time.sleep(1)
+    r["pair512"] = ours_preemptible(dev, k3); time.sleep(1)
+    os.environ["MS_LP_MMA_LAG"] = "0"
+    r["pair512_np"] = ours_np(dev, k3); time.sleep(1)
+    dev.set_lp_sm_reserve(0)
+    r["pair512_np_74"] = ours_np(dev, k3); time.sleep(1)
+    r["np_lag0_148"] = ours_np(dev, k1); time.sleep(1)
+    dev.set_lp_sm_reserve(1)
+    del os.environ["MS_LP_MMA_LAG"]
     out[f"round{rnd}"] = r
     print(json.dumps({f"round{rnd}": r}), flush=True)
 dev.close()
