@@ -213,10 +213,11 @@ struct ms_dev {
   uint32_t hp_seq = 0;  // monotonic doorbell sequence of this device
   unsigned long long* dbg = nullptr;  // per-CTA phase stamps of the next LP run (diagnostics)
   unsigned long long* dbg_buf = nullptr;
-  // SMs an LP grid leaves free.  0: the gate kernel (one warp, 1 KB smem) co-resides with
-  // an LP CTA, and the pair GEMM's 74 pairs fill the machine (a reserved SM left 73 pairs,
-  // i.e. 8 waves of 256 x 512 tiles for 8192^3 instead of 7).
-  int lp_sm_reserve = 0;
+  // SMs an LP grid leaves free: the parked HP gate's home.  A gate parked on an SM keeps an
+  // LP CTA (and, measured, a whole CTA pair) of a grid that needs every SM off that SM
+  // until the next ring (tools/pair_gate_probe.py: a 74-pair grid never completes while a
+  // gate is armed).  CTA-pair grids round the reserve up to a whole TPC (2 SMs): 73 pairs.
+  int lp_sm_reserve = 1;
   int lp_align_clusters[5] = {0, 0, 0, 0, 0};  // max active C-CTA clusters of the LP GEMM (MS_LP_CLUSTER_ALIGN)
   int hp_fused = 1;       // 0: per-op kernels; 1: fused launch (cluster split-K when it fits); 2: fused, no clusters
 };
@@ -251,6 +252,57 @@ int set_smem_attrs() {
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
   MS_CUDA(cudaFuncSetAttribute(axpy_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kAxpyMaxPad));
+  // Every kernel asks for the maximum shared-memory carveout.  An SM takes the carveout of
+  // the first kernel that lands on it while it is idle; a small kernel (the HP gate, the
+  // input pull, a streamer CTA) that configured an SM for little shared memory would keep
+  // a later 210 KB LP GEMM CTA off that SM until it exits — with the gate parked there
+  // until the next ring, a persistent LP grid that needs every SM never becomes fully
+  // resident (observed: a CTA pair starting only after the HP chain, and a drain deadlock
+  // when the scheduler waits for LP before ringing the armed gate).
+  const int mx = cudaSharedmemCarveoutMaxShared;
+#define MS_CARVE(...) MS_CUDA(cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributePreferredSharedMemoryCarveout, mx))
+  MS_CARVE(gate_kernel);
+  MS_CARVE(hp_pull_kernel);
+  MS_CARVE(hp_notify_kernel);
+  MS_CARVE(echo_kernel);
+  MS_CARVE(init_ctl_kernel);
+  MS_CARVE(kblock_major_kernel);
+  MS_CARVE(kblock_major_swiglu_kernel);
+  MS_CARVE(synth_fill_kernel);
+  MS_CARVE(synth_fill_f32_kernel);
+  MS_CARVE(add_ln_kernel);
+  MS_CARVE(attn_kernel);
+  MS_CARVE(avgpool_kernel);
+  MS_CARVE(maxpool_kernel);
+  MS_CARVE(bias_act_kernel);
+  MS_CARVE(bias_gelu_kernel);
+  MS_CARVE(im2col_kernel);
+  MS_CARVE(silu_mul_kernel);
+  MS_CARVE(splitk_reduce_kernel);
+  MS_CARVE(axpy_kernel<1, 1>);
+  MS_CARVE(axpy_kernel<2, 1>);
+  MS_CARVE(axpy_kernel<4, 1>);
+  MS_CARVE(axpy_kernel<8, 1>);
+  MS_CARVE(axpy_kernel<1, kAxpyGroups>);
+  MS_CARVE(axpy_kernel<2, kAxpyGroups>);
+  MS_CARVE(axpy_kernel<4, kAxpyGroups>);
+  MS_CARVE(axpy_kernel<8, kAxpyGroups>);
+  MS_CARVE(optim_kernel<1>);
+  MS_CARVE(optim_kernel<2>);
+  MS_CARVE(optim_kernel<4>);
+  MS_CARVE(optim_kernel<8>);
+  MS_CARVE(tc_gemm_kernel<64>);
+  MS_CARVE(tc_gemm_kernel<128>);
+  MS_CARVE(tc_gemm_kernel<256>);
+  MS_CARVE(tc_gemm2_kernel<256>);
+  MS_CARVE(tc_gemm2_kernel<512>);
+  MS_CARVE(hp_fused_kernel<1>);
+  MS_CARVE(hp_fused_kernel<2>);
+  MS_CARVE(hp_fused_kernel<4>);
+  MS_CARVE(hp_fused_kernel<1, 32>);
+  MS_CARVE(hp_gemv_kernel<false>);
+  MS_CARVE(hp_gemv_kernel<true>);
+#undef MS_CARVE
   done = true;
   return 0;
 }
@@ -1139,8 +1191,9 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
       return fail(MS_E_ARG, "GEMM shape must be a multiple of (128, block_n, 64)");
     if (desc->m > (1ll << 31) || desc->n > (1ll << 31) || desc->k > (1ll << 31)) return fail(MS_E_ARG, "shape too large");
     // Large GEMMs run on CTA pairs (cta_group::2, tc_gemm2.cuh) with 256 x 512 tiles: 8192^3
-    // at 1574-1585 TFLOP/s burst vs 1331-1346 for the single-CTA 128 x 256 kernel and
-    // 1610-1612 for cuBLAS on the same box (tools/gemm_ab2.py, profiles/r02_gemm_ab.json).
+    // at 1463-1477 TFLOP/s burst on the 73 pairs left beside the gate's TPC (1574-1585 on 74
+    // pairs) vs 1331-1346 for the single-CTA 128 x 256 kernel and 1610-1612 for cuBLAS on the
+    // same box (tools/gemm_ab2.py, profiles/r02_gemm_ab.json).
     // Chosen when the shape has >= 4 waves of pair tiles (fewer tiles lose more to the last
     // wave than the pair saves) and no k-split.  MS_LP_GEMM_PAIR=0 forces the single-CTA
     // kernel, =1 pairs with 256 x 256 tiles, =2 pairs with 256 x 512 tiles.
@@ -1294,8 +1347,9 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.mma_lag = mma_lag;
     if (s.pair) {
       // one CTA pair per tile; pairs of SMs left after the reserve
+      const int reserve = (d->lp_sm_reserve + 1) & ~1;  // whole TPCs
       const int pairs = static_cast<int>(std::max<uint64_t>(
-          1, std::min<uint64_t>(work, static_cast<uint64_t>(std::max(2, d->prop.multiProcessorCount - d->lp_sm_reserve) / 2))));
+          1, std::min<uint64_t>(work, static_cast<uint64_t>(std::max(2, d->prop.multiProcessorCount - reserve) / 2))));
       p.group_m = s.desc.group_m ? s.desc.group_m : 8;
       if (s.pair_tn == 512)
         MS_CUDA(launch_kc(tc_gemm2_kernel<512>, 2 * pairs, 256, Gemm2Cfg<512>::kSmemBytes, d->lp, false, 2, s.tma_a,

@@ -115,7 +115,7 @@ class LiveRun {
     // `small_bubble_sms` > 0 caps LP at that many SMs while harvesting a bubble INSIDE an HP
     // request (hint bubbles), so the co-running GEMM draws less power between HP iterations
     // and the HP chain keeps its clocks (B200 runs into its 1 kW cap under a full-GPU GEMM).
-    base_reserve_ = opts.value("lp_sm_reserve", 0);
+    base_reserve_ = opts.value("lp_sm_reserve", 1);
     small_sms_ = opts.value("small_bubble_sms", 0);
     max_sms_ = opts.value("lp_max_sms", 0);  // > 0: LP never uses more SMs (power budget)
     // Hint bubbles are harvested up to their predicted end / safety and not extended past
@@ -532,6 +532,7 @@ class LiveRun {
       if (st.preempted && preempt_raised_) {
         buf[148 * 8] = static_cast<uint64_t>(t_raise_);
         debug_.push_back(std::move(buf));
+        debug_kernels_.push_back(l.kernel);
         --debug_runs_;
       }
     }
@@ -575,11 +576,12 @@ class LiveRun {
   bool harvest_ = false, reef_ = false, reef_req_ = false, want_hp_ = true, want_lp_ = true, eager_ = false, record_ = true;
   bool direct_hp_ = false, calibrate_ = true;
   int debug_runs_ = 0;
-  int base_reserve_ = 0, small_sms_ = 0, max_sms_ = 0;
+  int base_reserve_ = 1, small_sms_ = 0, max_sms_ = 0;
   bool bound_hints_ = false;
   double hint_quantile_ = -1.0;  // < 0: size hint harvests from the hint's mean
   std::unique_ptr<PowerGovernor> governor_;
   std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
+  std::vector<std::string> debug_kernels_;    // kernel of each debug_ run
   int n_sm_ = 148;
   int64_t t0_ = 0, off0_ = 0, off1_ = 0, c0_ = 0, c1_ = 0;
   uint32_t last_seq_ = 0;
@@ -721,9 +723,11 @@ json LiveRun::run() {
       }
     }
   }
-  // Drain: stop LP, finish in-flight HP.
+  // Drain: stop LP, release the armed gates (a parked gate holds an SM slot a late LP CTA
+  // may need to start, see its exit and leave), finish in-flight HP.
   int64_t tr = 0;
   ms_preempt_raise(dev_, nullptr, &tr);
+  if (!direct_hp_ && last_seq_) ms_hp_ring(dev_, last_seq_, nullptr);
   if (lp_running_) {
     ms_lp_status st{};
     check(ms_lp_wait(dev_, lp_[lp_cur_].dev_id, 30'000'000'000ll, &st), "ms_lp_wait");
@@ -887,6 +891,9 @@ json LiveRun::run() {
       dbg.push_back(std::move(run));
     }
     out["debug_phases"] = std::move(dbg);  // [run][phase] = [min, p50, max] ns
+    json dk = json::array();
+    for (const std::string& k : debug_kernels_) dk.push_back(json(k));
+    out["debug_kernels"] = std::move(dk);
   }
   out["hp_chains"] = json(static_cast<unsigned long long>(hp_samples_.size()));
   json lp = json::object();
