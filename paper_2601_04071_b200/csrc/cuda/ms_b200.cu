@@ -1345,6 +1345,15 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
       return v < 0 ? 0 : v > 4 ? 4 : v;
     }();
     p.mma_lag = mma_lag;
+    // k-split units stream their operands from HBM (no reuse across CTAs): bound the loads in
+    // flight to ~96 KB per SM, which still covers the SM's share of HBM bandwidth at the
+    // loaded latency (tools/drain23_stamps.py: producer stop 8-9 us after the flag with the
+    // whole ring in flight).  MS_LP_TMA_INFLIGHT overrides (0 = unbounded).
+    {
+      const char* e = getenv("MS_LP_TMA_INFLIGHT");
+      const int stage_bytes = (kBM + s.desc.block_n) * kBK * 2;
+      p.tma_inflight = e ? std::max(0, atoi(e)) : (s.split > 1 ? std::max(2, (96 * 1024) / stage_bytes) : 0);
+    }
     if (s.pair) {
       // one CTA pair per tile; pairs of SMs left after the reserve
       const int reserve = (d->lp_sm_reserve + 1) & ~1;  // whole TPCs

@@ -125,6 +125,46 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Wait for the barrier phase unless *flag == want first (then false).
+__device__ __forceinline__ bool mbar_wait_unless(uint64_t* bar, uint32_t parity, const uint32_t* flag,
+                                                 uint32_t want) {
+  for (;;) {
+    if (mbar_try_wait(bar, parity)) return true;
+    if (flag && ld_volatile_smem(flag) == want) return false;
+  }
+}
+
+// Cluster-scope variant (barriers that receive remote arrivals).
+__device__ __forceinline__ bool mbar_wait_cluster_unless(uint64_t* bar, uint32_t parity, const uint32_t* flag,
+                                                         uint32_t want) {
+  for (;;) {
+    if (mbar_try_wait_cluster(bar, parity)) return true;
+    if (flag && ld_volatile_smem(flag) == want) return false;
+  }
+}
+
 // ---- TMA --------------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");

@@ -46,6 +46,11 @@ struct GemmParams {
   // Preemptible runs keep at most mma_lag k-blocks of MMAs queued on the tensor core
   // (1..4; 0 = unbounded): an abort then drains <= mma_lag k-blocks.
   int mma_lag;
+  // Preemptible runs keep at most tma_inflight stages issued but not yet landed (0 =
+  // unbounded): an abort waits for the in-flight loads to land before the CTA can leave, and
+  // for an HBM-bound shape (skinny training GEMMs with K up to 802,816) a full ring of loads
+  // queued at the SM's share of HBM bandwidth is ~5 us of drain.
+  int tma_inflight;
   // HP epilogue (split_k == 1 here; the split-K reduce kernel applies it otherwise):
   // C = act(acc + bias[col] (+ resid[row, col])), act 0 none / 1 ReLU / 2 tanh-GELU.
   const __nv_bfloat16* bias;
@@ -188,6 +193,7 @@ __device__ void split_tree_reduce(const GemmParams& p, GemmSmemCtl* s, long long
         s->fix_last = last ? 1u : 0u;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tid == 0) dbg_stamp_ext(p.run, 12);  // arrival done
       if (!s->fix_last) return;
       __threadfence();
     }
@@ -195,14 +201,15 @@ __device__ void split_tree_reduce(const GemmParams& p, GemmSmemCtl* s, long long
     for (int i = 0; i < level; ++i) stride *= kRedFan;
     const size_t slot0 = static_cast<size_t>(g) * kRedFan * stride;
     for (int c = chunk; c < BN / 32; ++c) {
-      if (c > chunk) {
-        // preemption point between 32-column chunks (one decision for all 128 threads; every
-        // claim of a group makes at least one chunk of progress)
+      if (c > chunk || arrive) {
+        // preemption point before every 32-column chunk (one decision for all 128 threads); a
+        // resumed continuation always makes at least one chunk of progress
         if (tid == 0) s->red_stop = (p.run.preemptible && ld_volatile_smem(&s->preempt)) ? 1u : 0u;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const bool stop = s->red_stop != 0;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (stop) {
+          if (tid == 0) dbg_stamp_ext(p.run, 14);  // parked at a chunk boundary
           if (tid == 0)
             push_redo(p.run, kRedEntry | (static_cast<unsigned long long>(tile) << 32) |
                                  (static_cast<unsigned long long>(level) << 24) |
@@ -250,6 +257,7 @@ __device__ void split_tree_reduce(const GemmParams& p, GemmSmemCtl* s, long long
         for (int v = 0; v < 8; ++v) __stcg(d0 + v * kBM, acc[v]);
       }
     }
+    if (tid == 0) dbg_stamp_ext(p.run, 13);  // a group reduced
     if (top) return;
     // this group's sum is partial g of the next level, in group g / F there
     level += 1;
@@ -319,6 +327,8 @@ __global__ void __launch_bounds__(256, 1)
     // ===================== tile scheduler + TMA producer =====================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      uint32_t issued = 0;  // ring positions issued (for the in-flight bound)
+      const uint32_t D = p.run.preemptible ? static_cast<uint32_t>(p.tma_inflight) : 0u;
       for (int j = 0;; ++j) {
         const int slot = j & 1;
         if (j >= 2) mbar_wait(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
@@ -333,6 +343,10 @@ __global__ void __launch_bounds__(256, 1)
         tile_coords(tile / split, p, mb, nb);
         const int kb0 = static_cast<int>(tile % split) * num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
+          if (D > 0 && issued >= D) {  // position issued - D has landed (its full phase completed)
+            const uint32_t back = issued - D;
+            mbar_wait(&s->full[back % S], (back / S) & 1);
+          }
           const bool abort = p.run.preemptible && kb > 0 && ld_volatile_smem(&s->preempt);
           mbar_wait(&s->empty[stage], phase ^ 1);
           if (abort) {
@@ -347,6 +361,7 @@ __global__ void __launch_bounds__(256, 1)
             else
               tma_load_2d(smem_b + stage * Cfg::kBBytes, &tma_b, &s->full[stage], (kb0 + kb) * kBK, nb * BN);
           }
+          ++issued;
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -373,14 +388,24 @@ __global__ void __launch_bounds__(256, 1)
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
         if (s->tile_id[slot] < 0) break;
-        if (j >= 2) mbar_wait(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);
         if (s->tile_id[slot] & kRedEntry) {  // reduction continuation: hand the slot on
+          if (j >= 2) mbar_wait(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);
           mbar_arrive(&s->tmem_full[slot]);
           continue;
         }
+        // A preemption seen while the epilogue still holds this accumulator slot (a previous
+        // unit's epilogue, e.g. a k-split reduction): consume this unit's ring positions right
+        // away without MMAs, so the producer's stop is not held behind the epilogue, and take
+        // the slot (in order) afterwards.
+        bool aborted = false, have_slot = j < 2;
+        if (!have_slot) {
+          if (mbar_wait_unless(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1, p.run.preemptible ? &s->preempt : nullptr, 1u))
+            have_slot = true;
+          else
+            aborted = true;
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(slot * BN);
-        bool aborted = false;
         for (int kb = 0;; ++kb) {
           mbar_wait(&s->full[stage], phase);
           tc_fence_after();
@@ -417,6 +442,7 @@ __global__ void __launch_bounds__(256, 1)
           if (flag != 0) break;
         }
         if (aborted) {
+          if (!have_slot) mbar_wait(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);  // keep the slot order
           // Drain this tile's issued MMAs (TMEM must be quiescent before dealloc), park the
           // tile on the redo list, and tell the epilogue to skip it with a plain arrive.
           umma_commit(&s->mma_drain);
@@ -449,6 +475,7 @@ __global__ void __launch_bounds__(256, 1)
       const long long tile = s->tile_id[slot];
       if (tile < 0) break;
       mbar_wait(&s->tmem_full[slot], (j >> 1) & 1);
+      if (q == 0 && lane == 0) dbg_stamp_ext(p.run, 10);  // diagnostics: epilogue unit start
       tc_fence_after();
       const bool cont = (tile & kRedEntry) != 0;  // reduction continuation (split-K tree)
       const bool keep = !cont && !s->tile_abort[slot];
@@ -515,6 +542,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(&s->tmem_empty[slot]);
         mbar_arrive(&s->tile_empty[slot]);
       }
+      if (q == 0 && lane == 0) dbg_stamp_ext(p.run, 11);  // unit's TMEM drained / partial stored
       if (split > 1 && p.tile_cnt && (keep || cont)) {
         // split-K: arrive at this slice's level-0 group (or resume a parked group) and
         // reduce up the tree as far as this unit is the last arrival

@@ -76,8 +76,8 @@ struct Gemm2Ctl {
   uint32_t tile_start[2];  // ring position of the tile's first k-block
   uint32_t tile_abort[2];
   uint32_t stage_flag[kGemm2MaxStages];
+  alignas(16) uint32_t peer_stop[4];  // leader: k-block at which the peer stopped (st.async)
   uint32_t stop_req;   // peer: ordinal (j + 1) of the tile the leader asks it to stop
-  uint32_t peer_stop;  // leader: k-block at which the peer stopped
   uint32_t tmem_base;
   uint32_t preempt;
   uint32_t producer_done;
@@ -147,37 +147,6 @@ __device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr
 __device__ __forceinline__ void mbar_complete_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// Wait for the barrier phase unless *flag == want first (then false).
-__device__ __forceinline__ bool mbar_wait_unless(uint64_t* bar, uint32_t parity, const uint32_t* flag,
-                                                 uint32_t want) {
-  for (;;) {
-    if (mbar_try_wait(bar, parity)) return true;
-    if (flag && ld_volatile_smem(flag) == want) return false;
-  }
-}
-
 template <int TN>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -284,11 +253,13 @@ __global__ void __launch_bounds__(256, 1)
           ++pos;
         }
         if (lead_stop < num_kb) {
-          // agree on the end of this tile's stream with the peer (see the header)
+          // agree on the end of this tile's stream with the peer (see the header); the answer
+          // is one st.async completing the armed stop barrier (no release fence on the path)
+          mbar_arrive_expect_tx(&s->stop_bar, 16);
           st_cluster_u32(peer_stop_req, static_cast<uint32_t>(j + 1));
-          mbar_wait_cluster(&s->stop_bar, stop_phase);
+          mbar_wait(&s->stop_bar, stop_phase);
           stop_phase ^= 1;
-          const int ps = static_cast<int>(ld_volatile_smem(&s->peer_stop));
+          const int ps = static_cast<int>(ld_volatile_smem(&s->peer_stop[0]));
           for (int kb = ps; kb < lead_stop; ++kb)  // armed for both halves, the peer's never comes
             mbar_complete_tx(&s->full[(pos0 + kb) % S], Cfg::kStageBytes);
           for (int kb = lead_stop; kb < ps; ++kb) {  // only the peer's half comes
@@ -309,11 +280,10 @@ __global__ void __launch_bounds__(256, 1)
       dbg_stamp(p.run, 1);
     } else if (lane == 0) {
       // ===================== peer: producer of its halves =====================
-      const uint32_t lead_peer_stop = mapa_shared(smem_u32(&s->peer_stop), 0);
+      const uint32_t lead_peer_stop = mapa_shared(smem_u32(&s->peer_stop[0]), 0);
       const uint32_t lead_stop_bar = mapa_shared(smem_u32(&s->stop_bar), 0);
-      auto report = [&](int kb) {
-        st_cluster_u32(lead_peer_stop, static_cast<uint32_t>(kb));
-        mbar_arrive_cluster(lead_stop_bar);  // release.cluster: the store above first
+      auto report = [&](int kb) {  // data and completion in one async store
+        st_async_v4(lead_peer_stop, static_cast<uint32_t>(kb), 0u, 0u, 0u, lead_stop_bar);
       };
       mbar_wait_cluster(&s->tile_full[0], 0);
       for (int j = 0;; ++j) {
@@ -369,10 +339,19 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
         if (s->tile_id[slot] < 0) break;
         const int ts = j % NS;  // accumulator slot
-        if (j >= NS) mbar_wait_cluster(&s->tmem_empty[ts], ((j / NS) & 1) ^ 1);
+        // (see tc_gemm.cuh: a preemption seen while the epilogue holds the accumulator lets the
+        // MMA warp consume this tile's positions first, so the stop agreement is not held
+        // behind the previous tile's epilogue)
+        bool aborted = false, have_slot = j < NS;
+        if (!have_slot) {
+          if (mbar_wait_cluster_unless(&s->tmem_empty[ts], ((j / NS) & 1) ^ 1,
+                                       p.run.preemptible ? &s->preempt : nullptr, 1u))
+            have_slot = true;
+          else
+            aborted = true;
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(ts * TN);
-        bool aborted = false;
         for (int kb = 0;; ++kb) {
           const uint32_t st = pos % S;
           mbar_wait(&s->full[st], (pos / S) & 1);
@@ -404,6 +383,7 @@ __global__ void __launch_bounds__(256, 1)
           if (flag == 1 || flag == 2) break;
         }
         if (aborted) {
+          if (!have_slot) mbar_wait_cluster(&s->tmem_empty[ts], ((j / NS) & 1) ^ 1);  // keep the slot order
           umma_commit_pair(&s->mma_drain);
           mbar_wait(&s->mma_drain, drain_phase);
           drain_phase ^= 1;
