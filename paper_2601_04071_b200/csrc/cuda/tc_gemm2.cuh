@@ -403,6 +403,9 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 3) {
     // (CTA 0's peer cannot exit before CTA 0 reaches the teardown cluster barrier)
     if (lane == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &s->preempt, &s->producer_done, 2);
+    // auxiliary host pollers on the next leaders (see tile_run.cuh poll_host_aux)
+    if (lane == 0 && p.run.preemptible && leader && blockIdx.x >= 2 && blockIdx.x <= 2 * kAuxPollers)
+      poll_host_aux(p.run, &s->preempt, &s->producer_done, 150u * blockIdx.x);
   } else if (warp >= 4) {
     // ===================== epilogue (this CTA's 128 rows of the pair tile) =====================
     const int q = warp - 4;
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
   if (threadIdx.x == 0) dbg_stamp(p.run, 4);
-  if (threadIdx.x == 0) cta_exit(p.run, s->tiles_done);
+  if (threadIdx.x == 0 && leader) cta_exit(p.run, s->tiles_done, 2);  // accounts for the pair
 }
 
 }  // namespace msdev

@@ -157,14 +157,16 @@ __device__ __forceinline__ void poll_host_aux(const TileRun& r, const uint32_t* 
 // tile / redo accounting (ordered by the CTA barrier before cta_exit) and lets the last
 // CTA acquire everyone else's.  (A two-level tree measured slower: the last CTA then pays
 // two L2 round trips while the preempted CTAs' in-flight loads drain.)
-__device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_done_cta) {
+// `ctas`: CTAs this call accounts for (2: the leader of a CTA pair exits for both, after the
+// pair's teardown cluster barrier — half the atomics on `top` while a preempted grid drains).
+__device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_done_cta, unsigned int ctas = 1) {
   MsLpCtl* ctl = r.ctl;
   dbg_stamp(r, 5);
-  atomicAdd(&ctl->exited, 1u);  // relaxed: only CTA 0's host poller reads it
+  atomicAdd(&ctl->exited, ctas);  // relaxed: only CTA 0's host poller reads it
   const unsigned long long w =
-      atom_add_acqrel_gpu_u64(&ctl->top, (static_cast<unsigned long long>(tiles_done_cta) << 32) | 1ull);
+      atom_add_acqrel_gpu_u64(&ctl->top, (static_cast<unsigned long long>(tiles_done_cta) << 32) | ctas);
   dbg_stamp_ext(r, 1);
-  if (static_cast<unsigned int>(w) + 1 != gridDim.x) return;
+  if (static_cast<unsigned int>(w) + ctas != gridDim.x) return;
   const unsigned long long tiles_total = (w >> 32) + tiles_done_cta;
   // Issue every control-block read at once (each is an L2 round trip, slow while the
   // preempted CTAs' in-flight loads still drain).
