@@ -302,7 +302,9 @@ def aggregate_leg(parts: list, workload: str) -> dict:
 
 
 CFG4_WORKLOAD = ("cfg4 (BASELINE configs[3]): HP Llama-3.2-1B-geometry bs=1 decode (GEMV chain, 2.47 GB/token) at "
-                 "80% HP load, token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 axpy streamer; governed")
+                 "80% HP load (rate_req_s, deviating from SURVEY's 20 req/s, which is 1.4x what HP alone can serve: "
+                 "80 tokens x ~0.85 ms per request), token hint U[100,500]us; LP bf16 8192^3 GEMM + 2^30 axpy "
+                 "streamer; governed; policies interleaved over 2 trace windows")
 
 
 CFG2_WORKLOAD = ("cfg2 (BASELINE configs[1]): HP ResNet-50 bs=1 224x224 inference (76-op chain: im2col + tcgen05 "

@@ -90,7 +90,6 @@ struct GemvParams {
   // holding back every op of the static unit plan by their start delay.
   int head_kb;
   uint32_t* start_cnt;  // CTAs started (reset by the last CTA)
-  int dyn_ops;          // static kernel: the first dyn_ops ops are claimed dynamically
 };
 
 constexpr int kGemvHeadCtas = 8;
@@ -347,8 +346,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
   const uint32_t ring_s = smem_u32(ring), xs_s = smem_u32(xs);
   __shared__ uint64_t full[kGemvStages], empty[kGemvStages], desc_bar;
   // DYN: (op, unit) in each stage, and where each op ends in this CTA's ring stream
-  __shared__ int2 stage_meta[kGemvStages];
-  __shared__ uint32_t op_end[kGemvMaxOps];
+  __shared__ int2 stage_meta[DYN ? kGemvStages : 1];
+  __shared__ uint32_t op_end[DYN ? kGemvMaxOps : 1];
   // Op descriptors live in shared memory (one bulk copy from global at entry): dynamically
   // indexed kernel-parameter reads go through the constant cache, whose misses wait behind
   // the saturated memory system, and small parameters keep the launch itself short.
@@ -371,7 +370,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
                  "l"(p.ops), "r"(bytes), "r"(smem_u32(&desc_bar))
                  : "memory");
   }
-  if (DYN || p.dyn_ops > 0)
+  if constexpr (DYN)
     for (int i = threadIdx.x; i < kGemvMaxOps; i += blockDim.x) op_end[i] = 0xFFFFFFFFu;
   __syncthreads();
   mbar_wait(&desc_bar, 0);
@@ -430,10 +429,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         pf_seek(pf_oi, pf_u + G);
         return true;
       };
-      // one op's units claimed dynamically in batches (DYN, or the first p.dyn_ops ops of a
-      // static chain): a CTA that starts late takes fewer of them
-      auto produce_dyn = [&](int oi) {
+      for (int oi = 0; oi < p.n_ops && DYN; ++oi) {
         const GemvOpDesc& o = sops[oi];
+        if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
         const size_t row_bytes = static_cast<size_t>(o.k) * 2;
         const int B = p.claim_batch;
         int next = static_cast<int>(atomicAdd(p.claim + oi, static_cast<unsigned>(B)));
@@ -471,11 +469,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
         }
         st_volatile_smem(&op_end[oi], issued);  // op oi ends at ring position `issued` here
         if (oi < 16) gemv_stamp(p.run, 48 + oi);
-      };
-      for (int oi = 0; oi < p.n_ops && DYN; ++oi) {
-        const GemvOpDesc& o = sops[oi];
-        if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
-        produce_dyn(oi);
       }
       if constexpr (DYN) {  // end of the chain: one terminal entry per consumer warp (no data)
         for (int w = 0; w < kGemvConsumers; ++w, ++issued) {
@@ -491,10 +484,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
       for (int oi = 0; oi < p.n_ops && !DYN; ++oi) {
         const GemvOpDesc& o = sops[oi];
         if (o.kind != kGemvMatvec && o.kind != kGemvSwiglu) continue;
-        if (oi < p.dyn_ops) {  // dynamic prefix (absorbs CTAs that start late, e.g. behind a draining LP grid)
-          produce_dyn(oi);
-          continue;
-        }
         const size_t row_bytes = static_cast<size_t>(o.k) * 2;
         for (int u = gemv_first_unit(o, G); u < o.units; u += G, ++issued) {
           const int r0 = u * o.rows, nr = gemv_unit_rows(o, u);
@@ -535,9 +524,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
     // phase ahead of a stage another warp has not released: mbarrier parity ABA).
     const int cw = warp - 1;
     const int t = threadIdx.x - 32;  // 0..255
-    // DYN ops: j = this warp's next ring position; static ops: j = the CTA's stream position
-    uint32_t j = (DYN || p.dyn_ops > 0) ? static_cast<uint32_t>(cw) : 0u;
-    int last_dyn = -1;  // last dynamically claimed op (its op_end is where the static ops start)
+    uint32_t j = DYN ? static_cast<uint32_t>(cw) : 0u;  // DYN: this warp's next ring position
     const uint32_t tag = p.tag;
     for (int oi = 0; oi < p.n_ops; ++oi) {
       const GemvOpDesc& o = sops[oi];
@@ -555,8 +542,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
           asm volatile("ld.shared.u32 %0, [%1];" : "=r"(g) : "r"(xs_s) : "memory");
           if (g != 0x7FEDCBA9u) p.run.dbg[2048 + 148 * 64 + blockIdx.x * 16 + oi] = globaltimer();
         }
-        if (DYN || oi < p.dyn_ops) {
-          last_dyn = oi;
+        if constexpr (DYN) {
           for (;;) {
             if (j >= ld_volatile_smem(&op_end[oi])) break;  // the producer knows where op oi ends
             const uint32_t stage = j % kGemvStages;
@@ -571,11 +557,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) hp_gemv_kernel(const __grid_c
             j += kGemvConsumers;
           }
         }
-        if (!DYN && oi >= p.dyn_ops && last_dyn >= 0) {  // first static op after the dynamic prefix
-          j = ld_volatile_smem(&op_end[last_dyn]);
-          last_dyn = -1;
-        }
-        for (int u = gemv_first_unit(o, G); u < o.units && !DYN && oi >= p.dyn_ops; u += G, ++j) {
+        for (int u = gemv_first_unit(o, G); u < o.units && !DYN; u += G, ++j) {
           if (static_cast<int>(j % kGemvConsumers) != cw) continue;
           const uint32_t stage = j % kGemvStages;
           mbar_wait(&full[stage], (j / kGemvStages) & 1);

@@ -110,8 +110,7 @@ int encode_kblock_major(CUtensorMap* map, const void* base, uint64_t rows, uint6
 
 constexpr int kRedoCap = 8192;
 constexpr int kMaxChainOps = 512;
-constexpr int kGemvHeadKbDefault = 0;
-constexpr int kGemvDynOpsDefault = 0;  // dynamic prefix of the static GEMV chain (A/B: tools/gemv_dynops_ab.py)  // head prefetch (hp_gemv.cuh), A/B: tools/gemv_head_ab.py
+constexpr int kGemvHeadKbDefault = 0;  // head prefetch (hp_gemv.cuh), A/B: tools/gemv_head_ab.py
 constexpr bool kGemvDynamicDefault = false;  // decided by tools/gemv_dynamic_ab.py  // per-op chains (config-2 ResNet-50: ~160 ops); fused / GEMV plans are shorter
 
 // FFI callers may pass any id: every entry point that indexes a slot checks it first.
@@ -958,14 +957,6 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
     return e ? std::max(0, atoi(e)) : kGemvHeadKbDefault;
   }();
   p.head_kb = head_kb;
-  // The first ops of the static chain claim their units dynamically: when the doorbell fires
-  // while a preempted LP grid drains, the CTAs on free SMs take the first ops' units and the
-  // CTAs that start late join at the first static op instead of holding back every op.
-  static const int dyn_ops = [] {
-    const char* e = getenv("MS_GEMV_DYN_OPS");
-    return e ? std::max(0, atoi(e)) : kGemvDynOpsDefault;
-  }();
-  p.dyn_ops = dynamic ? 0 : dyn_ops;
   p.start_cnt = ch.phase_d + 2 * ch.gemv_descs.size();
   if (dynamic)
     MS_CUDA(launch_kc(hp_gemv_kernel<true>, ch.fused_grid, kGemvThreads, kGemvSmemBytes, d->hp, pdl, 1, p));
