@@ -261,6 +261,23 @@ def run_policy_leg(dev, w, horizon_s: float, seed: int, rate: float, exlp_s: flo
     return out
 
 
+def single_variant(allr, peak: float, step_s: float):
+    """Rank 0's single-CTA LP GEMM windows (see the single-CTA leg in main)."""
+    s = allr[0].get("single")
+    if not s:
+        return None
+    slo = allr[0]["slo"]
+    met = sum(1 for x in s["rows"] if x[4] and x[1] <= slo["ttft_ns"] and x[2] <= slo["tpot_ns"])
+    return {"kernel": f"tc_gemm_kernel<256> (LP 8192^3 bf16, {s['tiles_total']} 128x256 tiles)",
+            "achieved_tflops": round(2.0 * 8192 ** 3 / (s["lp_gemm_ms"] * 1e-3) / 1e12, 1),
+            "frac": round(2.0 * 8192 ** 3 / (s["lp_gemm_ms"] * 1e-3) / 1e12 / peak, 4),
+            "preempt_lp_in_flight": {"p50_us": _us(percentile(s["inflight"], 0.5)),
+                                     "p99_us": _us(percentile(s["inflight"], 0.99)), "n": len(s["inflight"])},
+            "lp_exit_p50_us": _us(percentile(s["lp_exit"], 0.5)), "lp_exit_p99_us": _us(percentile(s["lp_exit"], 0.99)),
+            "slo_attainment": round(met / max(1, len(s["rows"])), 4),
+            "lp_throughput_vs_exclusive": round(s["tiles"] / (s["windows"] * step_s) / max(1e-9, s["exlp_rate"]), 4)}
+
+
 def _us(v):
     return None if v is None else round(v / 1e3, 3)
 
@@ -370,6 +387,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--baseline-windows", type=int, default=8,
                     help="config-1 trace windows for the side runs (kernel-boundary baselines, governed variant)")
+    ap.add_argument("--single-cta-windows", type=int, default=2,
+                    help="config-1 windows run with the single-CTA LP GEMM beside the CTA-pair default; 0 skips")
     ap.add_argument("--cfg4-s", type=float, default=26.0,
                     help="config-4 leg (decode HP at 80%% load, governed): trace seconds (>= 300 requests); 0 skips")
     ap.add_argument("--cfg2-s", type=float, default=6.0,
@@ -477,6 +496,32 @@ def main():
             pb["samples"] += r["samples"]["preempt_ring_to_first_hp_cta"]
             pb["inflight"] += r["samples"]["preempt_ring_to_first_hp_cta_lp_in_flight"]
 
+    # --- single-CTA LP GEMM variant (MS_LP_GEMM_PAIR=0): the round-1 kernel on the same
+    # buffers and windows — slower GEMM (128x256 tiles), shorter drain (no pair stop
+    # agreement, 256-column epilogue); reported beside the CTA-pair default
+    single = None
+    if not profiling and args.single_cta_windows > 0:
+        os.environ["MS_LP_GEMM_PAIR"] = "0"
+        try:
+            k_single = dev.lp_register_gemm(w.a, w.b, w.c, w.N_LP, w.N_LP, w.N_LP, block_n=256)
+        finally:
+            os.environ.pop("MS_LP_GEMM_PAIR", None)
+        k_pair, calib_pair = w.lp, w.calib
+        w.lp = k_single
+        c1 = w.calibrate(reps=5, profile=False)
+        s_ex = live_run(dev, sc(0, args.step_s), "exclusive_lp", w.binding(), w.options(timeline=False))
+        single = {"rows": [], "tiles": 0, "inflight": [], "lp_exit": [], "lp_gemm_ms": c1["lp_gemm_ms"],
+                  "exlp_rate": s_ex["lp"]["tiles_per_s"], "tiles_total": k_single.total_tiles,
+                  "windows": args.single_cta_windows}
+        for i in range(args.single_cta_windows):
+            r = live_run(dev, sc(i, args.step_s), "splitkernel", w.binding(), w.options(timeline=False))
+            single["rows"] += r["requests"]["rows"]
+            single["tiles"] += r["lp"]["tiles_done"]
+            single["inflight"] += r["samples"]["preempt_ring_to_first_hp_cta_lp_in_flight"]
+            single["lp_exit"] += r["samples"]["preempt_flag_to_last_lp_exit"]
+        w.lp, w.calib = k_pair, calib_pair
+        dev.lp_unregister(k_single)
+
     # --- e2e: same metric through the C-ABI with the HP request buffers in pinned host
     # memory (H2D of the input at admission, D2H of the output before completion)
     e2e = live_run(dev, sc(0, args.step_s), "splitkernel", w.binding(e2e=True), w.options(timeline=False))
@@ -504,7 +549,7 @@ def main():
                                      reef_s=min(secs, 4.0))
         wx.close()
 
-    mine = {"cfg4": cfg4, "legs23": legs23, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "rows": rows,
+    mine = {"single": single, "cfg4": cfg4, "legs23": legs23, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "rows": rows,
             "tiles": tiles, "kb": kb, "exlp_rate": exlp_rate, "ex_rows": ex_rows, "step_ms": step_ms, "wall": wall,
             "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"], "launches": launches,
             "chains": chains, "clocks": clk.summary(), "calib": calib, "slo": slo, "pb": pb,
@@ -577,6 +622,7 @@ def main():
                                    "p99_us": _us(percentile(agg["pb_samples"], 0.99)),
                                    "preempt_lp_in_flight_p99_us": _us(percentile(agg["pb_inflight"], 0.99)),
                                    "clocks": {k: allr[0]["pb_clocks"].get(k) for k in ("sm_mhz", "reasons")}},
+        "single_cta_lp_gemm_variant": single_variant(allr, peak, args.step_s),
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": (f"{kname} (LP 8192^3 bf16, {calib.get('lp_gemm_tiles')} "

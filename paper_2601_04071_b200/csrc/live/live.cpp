@@ -741,6 +741,9 @@ json LiveRun::run() {
   // Release any still-armed gates so the HP stream drains.
   ms_hp_ring(dev_, last_seq_, nullptr);
   ms_dev_sync(dev_);
+  // The LP SM reserve was moved per launch (governor, SM caps): leave the device at the
+  // run's base reserve, so a later timing (calibration, profiler) sees the full LP grid.
+  ms_set_lp_sm_reserve(dev_, base_reserve_);
   {
     const int64_t a = mono_ns();
     if (calibrate_) check(ms_clock_calibrate(dev_, 200, &off1_, &rtt1), "ms_clock_calibrate");

@@ -17,6 +17,7 @@ from . import scenarios
 from .device import Device, _ck, lib as dev_lib
 
 SEED = 20260117
+DEFAULT_LP_SM_RESERVE = 1  # ms_b200.cu ms_dev::lp_sm_reserve (the HP gate's home)
 
 
 def _live_lib():
@@ -92,6 +93,7 @@ class Config1:
         also the on-B200 profile of the LP GEMM over tile prefixes (profiler.py), which the
         scenario carries as KernelSpec.measured_time — the reference's measured execution
         oracle for split plans (engine.hpp:461-481, splitter.hpp:141-207)."""
+        self.dev.set_lp_sm_reserve(DEFAULT_LP_SM_RESERVE)  # a live run may have left a governed reserve
         ms_gemm = self.dev.lp_time_full(self.lp, reps)
         waves = math.ceil(self.lp.total_tiles / (self.dev.info["sm_count"] // self.lp.tile_ctas))
         ms_chain = self.dev.hp_time_chain(self.chain, 20)
@@ -209,6 +211,7 @@ class Config4:
                 "hp": {"hp_decode": [self.chain]}}
 
     def calibrate(self, reps: int = 3) -> dict:
+        self.dev.set_lp_sm_reserve(DEFAULT_LP_SM_RESERVE)
         sm = self.dev.info["sm_count"]
         ms_gemm = self.dev.lp_time_full(self.lp_gemm, reps)
         ms_axpy = self.dev.lp_time_full(self.lp_axpy, reps)

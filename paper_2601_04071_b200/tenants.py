@@ -401,12 +401,13 @@ class TrainStepLP:
     def calibrate(self, reps: int = 2) -> dict:
         """Per-kernel full-run time (CUDA events) -> per-wave tile time of the pacing model
         (the on-B200 profile behind KernelSpec.block_time)."""
+        self.dev.set_lp_sm_reserve(1)  # a live run may have left a governed reserve
         sm = self.dev.info["sm_count"] - 1
         self.ms: dict[str, float] = {}
         for nm, k in self.kernels.items():
             ms = self.dev.lp_time_full(k, reps)
             self.ms[nm] = ms
-            resident = sm if nm != self.optim_name else 3 * sm
+            resident = (sm // k.tile_ctas) if nm != self.optim_name else 3 * sm
             waves = math.ceil(k.total_tiles / resident)
             self.tile_ns[nm] = max(500, int(ms * 1e6 / max(1, waves)))
             # two-point on-B200 profile (one wave, whole kernel) -> KernelSpec.measured_time
