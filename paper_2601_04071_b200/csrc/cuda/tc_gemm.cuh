@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(256, 1)
       const int unit_slice = cont ? 0 : static_cast<int>(tile % split);
       int mb = 0, nb = 0;
       if (keep || cont) tile_coords(unit_tile, p, mb, nb);
+      bool abandoned = false;  // preempted while storing: the unit goes to the redo list
       if (keep) {
         const int row_in_tile = q * 32 + lane;
         const int row = mb * kBM + row_in_tile;
@@ -493,6 +494,17 @@ __global__ void __launch_bounds__(256, 1)
                                   : nullptr;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
+          if (p.run.preemptible) {  // one decision per 32-column chunk for the 4 epilogue warps
+            if (q == 0 && lane == 0) s->red_stop = ld_volatile_smem(&s->preempt) != 0 ? 1u : 0u;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const bool stop = s->red_stop != 0;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (stop) {
+              if (q == 0 && lane == 0) push_redo(p.run, static_cast<unsigned long long>(tile));
+              abandoned = true;
+              break;
+            }
+          }
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(slot * BN + c0), r);
           tmem_ld_wait();
@@ -534,7 +546,7 @@ __global__ void __launch_bounds__(256, 1)
             cbuf_idx ^= 1;
           }
         }
-        if (q == 0 && lane == 0) ++s->tiles_done;
+        if (q == 0 && lane == 0 && !abandoned) ++s->tiles_done;
       }
       tc_fence_before();
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -543,7 +555,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(&s->tile_empty[slot]);
       }
       if (q == 0 && lane == 0) dbg_stamp_ext(p.run, 11);  // unit's TMEM drained / partial stored
-      if (split > 1 && p.tile_cnt && (keep || cont)) {
+      if (split > 1 && p.tile_cnt && ((keep && !abandoned) || cont)) {
         // split-K: arrive at this slice's level-0 group (or resume a parked group) and
         // reduce up the tree as far as this unit is the last arrival
         const int row_in_tile = q * 32 + lane;

@@ -82,6 +82,9 @@ struct Gemm2Ctl {
   uint32_t preempt;
   uint32_t producer_done;
   uint32_t tiles_done;
+  uint32_t epi_abort;  // peer: ordinal (j + 1) of the tile whose epilogue the leader abandoned
+  uint32_t epi_stop;   // epilogue warps' shared stop decision
+  uint32_t epi_done;   // epilogue finished (the leader's mirror poller may stop)
 };
 
 // ---- cluster helpers ----------------------------------------------------------------
@@ -186,6 +189,8 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(&s->stop_bar, 1);
     mbar_init(&s->mma_drain, 1);
     s->stop_req = 0;
+    s->epi_abort = 0;
+    s->epi_done = 0;
     s->preempt = 0;
     s->producer_done = 0;
     s->tiles_done = 0;
@@ -399,7 +404,8 @@ __global__ void __launch_bounds__(256, 1)
       dbg_stamp(p.run, 2);
     }
   } else if (warp == 2) {
-    if (lane == 0 && leader && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->producer_done);
+    // up until the epilogue is done: an epilogue in progress abandons its tile on a preemption
+    if (lane == 0 && leader && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->epi_done);
   } else if (warp == 3) {
     // (CTA 0's peer cannot exit before CTA 0 reaches the teardown cluster barrier)
     if (lane == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &s->preempt, &s->producer_done, 2);
@@ -412,6 +418,8 @@ __global__ void __launch_bounds__(256, 1)
     int cbuf_idx = 0;
     const uint32_t lead_tmem_empty = mapa_shared(smem_u32(&s->tmem_empty[0]), 0);
     const uint32_t lead_tile_empty = mapa_shared(smem_u32(&s->tile_empty[0]), 0);
+    const uint32_t peer_epi_abort = mapa_shared(smem_u32(&s->epi_abort), 1);
+    const int tid = threadIdx.x - 128;
     for (int j = 0;; ++j) {
       const int slot = j & 1;
       mbar_wait_cluster(&s->tile_full[slot], (j >> 1) & 1);
@@ -425,8 +433,28 @@ __global__ void __launch_bounds__(256, 1)
         int mb, nb;
         tile_coords(tile, p, mb, nb);
         const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
+        // A preemption during the store of a completed tile abandons it (the leader decides, at
+        // 32-column chunk boundaries, tells the peer, and parks the tile on the redo list): the
+        // 512-column epilogue is ~2.5 us of TMEM reads that a preempted grid need not wait for.
+        bool abandoned = false;
 #pragma unroll 1
         for (int c0 = 0; c0 < TN; c0 += 32) {
+          if (p.run.preemptible) {
+            if (tid == 0)
+              s->epi_stop = leader ? (ld_volatile_smem(&s->preempt) != 0 ? 1u : 0u)
+                                   : (ld_volatile_smem(&s->epi_abort) == static_cast<uint32_t>(j + 1) ? 1u : 0u);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const bool stop = s->epi_stop != 0;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (stop) {
+              if (tid == 0 && leader) {
+                st_cluster_u32(peer_epi_abort, static_cast<uint32_t>(j + 1));
+                push_redo(p.run, static_cast<unsigned long long>(tile));
+              }
+              abandoned = true;
+              break;
+            }
+          }
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(ts * TN + c0), r);
           tmem_ld_wait();
@@ -450,7 +478,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           cbuf_idx ^= 1;
         }
-        if (q == 0 && lane == 0 && leader) ++s->tiles_done;
+        if (q == 0 && lane == 0 && leader && !abandoned) ++s->tiles_done;
       }
       tc_fence_before();
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -460,7 +488,10 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
     if (lane == 0) bulk_wait_read<0>();
-    if (q == 0 && lane == 0) dbg_stamp(p.run, 3);
+    if (q == 0 && lane == 0) {
+      st_volatile_smem(&s->epi_done, 1u);
+      dbg_stamp(p.run, 3);
+    }
   }
 
   tc_fence_before();

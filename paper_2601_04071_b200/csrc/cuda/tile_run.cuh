@@ -111,8 +111,9 @@ __device__ __forceinline__ void poll_host(const TileRun& r, const uint32_t* pree
   uint32_t mirrored = 0;
   for (;;) {
     if (ld_volatile_smem(preempt)) break;  // CTA 0 is leaving anyway
+    // every other CTA has left (LP grids count exits in the low half of `top`, cta_exit)
     if (ld_volatile_smem(producer_done) &&
-        *reinterpret_cast<volatile unsigned int*>(&r.ctl->exited) + group >= gridDim.x)
+        static_cast<unsigned int>(*reinterpret_cast<volatile unsigned long long*>(&r.ctl->top)) + group >= gridDim.x)
       break;
     if (r.host_progress)
       st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(r.host_progress),
@@ -159,14 +160,33 @@ __device__ __forceinline__ void poll_host_aux(const TileRun& r, const uint32_t* 
 // two L2 round trips while the preempted CTAs' in-flight loads drain.)
 // `ctas`: CTAs this call accounts for (2: the leader of a CTA pair exits for both, after the
 // pair's teardown cluster barrier — half the atomics on `top` while a preempted grid drains).
+//
+// LP grids (persistent, at most one wave, no HP bookkeeping) publish differently: every CTA
+// but CTA 0 adds its count with a fire-and-forget release reduction and leaves at once — no
+// L2 round trip on its way out, so a preempted grid frees its SMs sooner — and CTA 0, which
+// stays until the others are gone anyway (its host poller), waits for the count and
+// publishes.  (HP kernels keep the last-arrival scheme: a spinning CTA 0 could hold a slot a
+// not-yet-resident CTA of a larger or PDL-overlapped grid needs.)
 __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_done_cta, unsigned int ctas = 1) {
   MsLpCtl* ctl = r.ctl;
   dbg_stamp(r, 5);
-  atomicAdd(&ctl->exited, ctas);  // relaxed: only CTA 0's host poller reads it
-  const unsigned long long w =
-      atom_add_acqrel_gpu_u64(&ctl->top, (static_cast<unsigned long long>(tiles_done_cta) << 32) | ctas);
-  dbg_stamp_ext(r, 1);
-  if (static_cast<unsigned int>(w) + ctas != gridDim.x) return;
+  const unsigned long long mine = (static_cast<unsigned long long>(tiles_done_cta) << 32) | ctas;
+  unsigned long long w;
+  if (r.hp_ctl == nullptr) {
+    if (blockIdx.x != 0) {
+      red_release_gpu_add_u64(&ctl->top, mine);  // after this CTA's redo pushes (release)
+      return;
+    }
+    const unsigned int others = gridDim.x - ctas;
+    while (static_cast<unsigned int>((w = ld_acquire_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->top)))) < others) {
+    }
+    dbg_stamp_ext(r, 1);
+  } else {
+    atomicAdd(&ctl->exited, ctas);  // relaxed: only CTA 0's host poller reads it
+    w = atom_add_acqrel_gpu_u64(&ctl->top, mine);
+    dbg_stamp_ext(r, 1);
+    if (static_cast<unsigned int>(w) + ctas != gridDim.x) return;
+  }
   const unsigned long long tiles_total = (w >> 32) + tiles_done_cta;
   // Issue every control-block read at once (each is an L2 round trip, slow while the
   // preempted CTAs' in-flight loads still drain).
