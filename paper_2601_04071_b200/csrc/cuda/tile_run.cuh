@@ -178,8 +178,10 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
       return;
     }
     const unsigned int others = gridDim.x - ctas;
-    while (static_cast<unsigned int>((w = ld_acquire_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->top)))) < others) {
-    }
+    // relaxed polling (no L1 invalidation per iteration), one acquire fence once complete
+    while (static_cast<unsigned int>((w = ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->top)))) < others)
+      __nanosleep(32);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     dbg_stamp_ext(r, 1);
   } else {
     atomicAdd(&ctl->exited, ctas);  // relaxed: only CTA 0's host poller reads it
