@@ -389,7 +389,7 @@ def main():
                     help="config-1 trace windows for the side runs (kernel-boundary baselines, governed variant)")
     ap.add_argument("--single-cta-windows", type=int, default=2,
                     help="config-1 windows run with the single-CTA LP GEMM beside the CTA-pair default; 0 skips")
-    ap.add_argument("--cfg4-s", type=float, default=26.0,
+    ap.add_argument("--cfg4-s", type=float, default=32.0,
                     help="config-4 leg (decode HP at 80%% load, governed): trace seconds (>= 300 requests); 0 skips")
     ap.add_argument("--cfg2-s", type=float, default=6.0,
                     help="config-2 leg (ResNet-50 bs=1 HP at 200 req/s + bs=64 training LP): trace seconds; 0 skips")

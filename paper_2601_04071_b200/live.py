@@ -248,9 +248,15 @@ class Config4:
         step_s = (self.calib or {}).get("hp_step_ms", 1.0) * 1e-3
         return utilisation / (80.0 * (step_s + 300e-6))
 
+    # Large-bubble threshold for the live runs (the reference's scheduler.threshold_ms,
+    # default 2 ms): with µs-scale preemption there is no reason to leave a gap between
+    # decode requests idle for 2 ms before harvesting it (the request-level kernel-boundary
+    # baseline relaunches LP the moment HP has no request); as for configs 2/3.
+    THRESHOLD_MS = 0.02
+
     def scenario(self, seed: int, horizon_s: float, rate: float | None = None) -> dict:
         return scenarios.config4(seed=seed, horizon_s=horizon_s, calib=self.calib or {},
-                                 rate=rate if rate is not None else self.hp_rate())
+                                 rate=rate if rate is not None else self.hp_rate(), threshold_ms=self.THRESHOLD_MS)
 
     def options(self, **kw) -> dict:
         c = self.calib or {}

@@ -94,8 +94,11 @@ def config1(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
     }
 
 
-def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, rate: float = 20.0) -> dict:
-    """Config 4: Llama-style 1B decode HP (bs=1) + LP GEMM training + LP HBM streamer."""
+def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, rate: float = 20.0,
+            threshold_ms: float | None = None) -> dict:
+    """Config 4: Llama-style 1B decode HP (bs=1) + LP GEMM training + LP HBM streamer.
+    `threshold_ms`: the scheduler's large-bubble threshold (scheduler.threshold_ms; None =
+    the reference default, 2 ms)."""
     c = dict(DEFAULT_CALIB, **(calib or {}))
     sc = {
         "name": "cfg4_decode_vs_gemm_and_stream",
@@ -121,6 +124,8 @@ def config4(seed: int = 1, horizon_s: float = 10.0, calib: dict | None = None, r
         "traces": [{"name": "hp_trace", "bursty": {"rate": rate, "burstiness": 1.0},
                     "iterations": {"dist": "uniform", "lo": 32, "hi": 128}}],
     }
+    if threshold_ms is not None:
+        sc["scheduler"] = {"threshold_ms": threshold_ms}
     return sc
 
 
