@@ -144,22 +144,34 @@ def test_session_external_tenant():
 
 
 def test_live_preemption_latency_targets():
-    """Regression guard on the north_star latency target (config 1, 1.5 s live window):
-    ring -> first HP CTA p99 <= 10 us over true preemptions (LP resident when HP turned
-    active, engine.hpp:954-960) and over all HP activations; the LP drain (flag -> last LP
-    CTA exit) stays within 2x of the target."""
+    """Regression guard on the north_star latency target (config 1, three 1.5 s live
+    windows pooled: >= 400 true preemptions, so a p99 is not decided by one or two rare
+    events — tools/pair_outlier_probe.py sees ~1 in 2,500 activations take 0.2-0.5 ms with
+    either LP GEMM kernel): ring -> first HP CTA p99 <= 10 us over true preemptions (LP
+    resident when HP turned active, engine.hpp:954-960) and over all HP activations; the
+    LP drain (flag -> last LP CTA exit) stays within 2x of the target."""
     from paper_2601_04071_b200.device import Device
     from paper_2601_04071_b200.live import Config1, live_run
     dev = Device(0)
     w = Config1(dev)
     w.calibrate(reps=2)
-    sk = live_run(dev, w.scenario(seed=21, horizon_s=1.5), "splitkernel", w.binding(), w.options(timeline=False))
-    infl = sk["preempt_ring_to_first_hp_cta_lp_in_flight"]
-    idle = sk["preempt_ring_to_first_hp_cta_lp_idle"]
-    assert infl["n"] >= 10 and infl["n"] + idle["n"] == sk["preempt_ring_to_first_hp_cta"]["n"]
-    assert infl["p99_ns"] <= 10_000, infl
-    assert sk["preempt_ring_to_first_hp_cta"]["p99_ns"] <= 10_000
-    assert sk["preempt_flag_to_last_lp_exit"]["p99_ns"] <= 20_000
+    infl, idle, allx, lx, n_total = [], [], [], [], 0
+    for k in range(3):
+        sk = live_run(dev, w.scenario(seed=21 + k, horizon_s=1.5), "splitkernel", w.binding(), w.options(timeline=False))
+        smp = sk["samples"]
+        infl += smp["preempt_ring_to_first_hp_cta_lp_in_flight"]
+        idle += smp["preempt_ring_to_first_hp_cta_lp_idle"]
+        allx += smp["preempt_ring_to_first_hp_cta"]
+        lx += smp["preempt_flag_to_last_lp_exit"]
+        n_total += sk["preempt_ring_to_first_hp_cta"]["n"]
+
+    def p99(xs):
+        s = sorted(xs)
+        return s[min(len(s) - 1, int(0.99 * len(s)))]
+    assert len(infl) >= 100 and len(infl) + len(idle) == n_total == len(allx)
+    assert p99(infl) <= 10_000, (len(infl), sorted(infl)[-8:])
+    assert p99(allx) <= 10_000
+    assert p99(lx) <= 20_000
     dev.close()
 
 
