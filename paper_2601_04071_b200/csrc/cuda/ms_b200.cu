@@ -1043,6 +1043,7 @@ int ms_dev_open(int ordinal, ms_dev** out) {
   if (cudaGetDeviceCount(&n) != cudaSuccess || n <= ordinal) return fail(MS_E_NODEV, "no CUDA device");
   auto* d = new ms_dev();
   d->ordinal = ordinal;
+  if (const char* e = getenv("MS_LP_SM_RESERVE")) d->lp_sm_reserve = std::max(0, atoi(e));  // A/B knob
   MS_CUDA(cudaSetDevice(ordinal));
   MS_CUDA(cudaGetDeviceProperties(&d->prop, ordinal));
   if (d->prop.major != 10) {

@@ -115,7 +115,7 @@ class LiveRun {
     // `small_bubble_sms` > 0 caps LP at that many SMs while harvesting a bubble INSIDE an HP
     // request (hint bubbles), so the co-running GEMM draws less power between HP iterations
     // and the HP chain keeps its clocks (B200 runs into its 1 kW cap under a full-GPU GEMM).
-    base_reserve_ = opts.value("lp_sm_reserve", 1);
+    base_reserve_ = opts.value("lp_sm_reserve", getenv("MS_LP_SM_RESERVE") ? std::max(0, atoi(getenv("MS_LP_SM_RESERVE"))) : 1);
     small_sms_ = opts.value("small_bubble_sms", 0);
     max_sms_ = opts.value("lp_max_sms", 0);  // > 0: LP never uses more SMs (power budget)
     // Hint bubbles are harvested up to their predicted end / safety and not extended past

@@ -17,7 +17,7 @@ from . import scenarios
 from .device import Device, _ck, lib as dev_lib
 
 SEED = 20260117
-DEFAULT_LP_SM_RESERVE = 1  # ms_b200.cu ms_dev::lp_sm_reserve (the HP gate's home)
+DEFAULT_LP_SM_RESERVE = int(__import__("os").environ.get("MS_LP_SM_RESERVE", "1"))  # ms_b200.cu ms_dev::lp_sm_reserve (the HP gate's home)
 
 
 def _live_lib():
