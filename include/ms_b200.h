@@ -240,6 +240,31 @@ int ms_hp_wait(ms_dev* dev, int chain_id, uint32_t seq, int64_t timeout_ns, ms_h
 /* Ping-pong through the host page; device_ns ~= host_ns + *offset_ns (min-RTT sample). */
 int ms_clock_calibrate(ms_dev* dev, int rounds, int64_t* offset_ns, int64_t* rtt_min_ns);
 
+/* ---- device-side event trace -------------------------------------------------------- */
+/* A ring of %globaltimer events written by the kernels themselves (posted stores into
+ * pinned host memory, no copy): the exit record of every LP run (start, first CTA that saw
+ * a preemption, exit), every HP chain (first CTA, done) and every doorbell gate release.
+ * A long live run can be logged incrementally by draining it (SURVEY.md §8b
+ * ms_trace_drain); the live scheduler's own Timeline is unaffected. */
+typedef struct ms_event {
+  uint64_t seq;   /* 1-based position in the trace */
+  uint64_t t_ns;  /* %globaltimer */
+  uint32_t kind;  /* MS_EV_* */
+  uint32_t id;    /* LP slot, HP chain control block, or doorbell seq (gate) */
+  uint64_t a, b;  /* per kind, see below */
+} ms_event;
+#define MS_EV_LP_START 1 /* a = run id */
+#define MS_EV_LP_SEEN 2  /* a = run id (first CTA that observed the preempt epoch) */
+#define MS_EV_LP_EXIT 3  /* a = run id, b = (tiles done << 32) | redo entries left; t = last exit */
+#define MS_EV_HP_FIRST 4 /* a = doorbell seq of the chain run */
+#define MS_EV_HP_DONE 5  /* a = doorbell seq */
+#define MS_EV_GATE 6     /* a = doorbell word (epoch << 32 | seq) as the gate saw it */
+/* capacity (events, a power of two) > 0 allocates and enables the ring; 0 disables it. */
+int ms_trace_enable(ms_dev* dev, size_t capacity);
+/* Copy up to `max` events in order, oldest first; returns the count (>= 0).  `lost` (may be
+ * null) receives the number of events overwritten before they were drained. */
+int ms_trace_drain(ms_dev* dev, ms_event* out, size_t max, uint64_t* lost);
+
 /* ---- kernel timing (CUDA events on the launching stream) ---------------------------- */
 /* Time `reps` back-to-back full runs of LP kernel `id` over [0, total); returns mean ms. */
 int ms_lp_time_full(ms_dev* dev, int id, int reps, float* ms_per_run);

@@ -210,6 +210,12 @@ struct ms_dev {
   HpChain chains[MS_MAX_HP_CHAINS];
   int next_hp_ctl = MS_MAX_LP;
   int stream_memops = 0;
+  // device-side event trace (ms_trace_enable / ms_trace_drain)
+  bool trace_on = false;
+  MsTrace* trace_dev = nullptr;          // device copy of the descriptor
+  MsTraceEvent* trace_ev = nullptr;      // pinned host ring
+  unsigned long long* trace_head = nullptr;
+  uint64_t trace_cap = 0, trace_read = 0, trace_lost = 0;
   uint32_t hp_seq = 0;  // monotonic doorbell sequence of this device
   unsigned long long* dbg = nullptr;  // per-CTA phase stamps of the next LP run (diagnostics)
   unsigned long long* dbg_buf = nullptr;
@@ -314,6 +320,7 @@ TileRun base_run(ms_dev* d, int ctl_index) {
   r.redo_out = d->dummy_redo + 16;
   r.host_line = reinterpret_cast<const uint64_t*>(&d->page_d->lp_line[0]);
   r.mirror = d->mirror;
+  r.trace = d->trace_on ? d->trace_dev : nullptr;
   return r;
 }
 
@@ -466,7 +473,8 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
     MS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(o.op.c), reinterpret_cast<const void*>(o.op.a),
                             static_cast<size_t>(o.op.m), cudaMemcpyDefault, d->hp));
     if (i + 1 == ch.ops.size()) {
-      hp_notify_kernel<<<1, 1, 0, d->hp>>>(d->hp_ctl + chain_id, &d->page_d->hp[chain_id], seq);
+      hp_notify_kernel<<<1, 1, 0, d->hp>>>(d->hp_ctl + chain_id, &d->page_d->hp[chain_id], seq,
+                                           d->trace_on ? d->trace_dev : nullptr, chain_id);
       MS_CUDA(cudaGetLastError());
     }
     return 0;
@@ -477,6 +485,7 @@ int launch_hp_op(ms_dev* d, int chain_id, const HpChain& ch, size_t i, uint32_t 
   while (last_k > 0 && is_copy(ch.ops[last_k].op)) --last_k;
   TileRun r = base_run(d, o.ctl_index);
   r.hp_ctl = d->hp_ctl + chain_id;
+  r.slot = chain_id;  // (HP runs are not preemptible: slot only names the chain in the trace)
   r.hp_rec = &d->page_d->hp[chain_id];
   r.hp_first = i == first_k;
   r.dbg = d->dbg;
@@ -920,6 +929,7 @@ int launch_gemv(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool p
   GemvParams p{};
   p.run = base_run(d, ch.fused_ctl);
   p.run.hp_ctl = d->hp_ctl + chain_id;
+  p.run.slot = chain_id;
   p.run.hp_rec = &d->page_d->hp[chain_id];
   p.run.hp_first = after_pull ? 0 : 1;
   p.run.pdl_wait = after_pull ? 1 : 0;
@@ -969,6 +979,7 @@ int launch_fused(ms_dev* d, int chain_id, const HpChain& ch, uint32_t seq, bool 
   FusedParams p{};
   p.run = base_run(d, ch.fused_ctl);
   p.run.hp_ctl = d->hp_ctl + chain_id;
+  p.run.slot = chain_id;
   p.run.hp_rec = &d->page_d->hp[chain_id];
   p.run.hp_first = after_pull ? 0 : 1;
   p.run.pdl_wait = after_pull ? 1 : 0;
@@ -1089,6 +1100,9 @@ int ms_dev_close(ms_dev* d) {
   cudaFree(d->hp_ctl);
   cudaFree(d->dummy_redo);
   cudaFreeHost(d->page);
+  if (d->trace_ev) cudaFreeHost(d->trace_ev);
+  if (d->trace_head) cudaFree(d->trace_head);
+  if (d->trace_dev) cudaFree(d->trace_dev);
   cudaStreamDestroy(d->lp);
   cudaStreamDestroy(d->hp);
   cudaStreamDestroy(d->aux);
@@ -1789,7 +1803,7 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
   if (overlap) {
     // e2e input: its own gate on the copy stream, so the H2D starts at the ring (no SM
     // work needed, it overlaps the LP drain); the chain waits for the copy's event.
-    gate_kernel<<<1, 32, gate_smem, d->hpcopy>>>(&d->page_d->doorbell, seq, nullptr, nullptr);  // (smem: stays off LP SMs)
+    gate_kernel<<<1, 32, gate_smem, d->hpcopy>>>(&d->page_d->doorbell, seq, nullptr, nullptr, nullptr);  // (smem: stays off LP SMs)
     MS_CUDA(cudaGetLastError());
     for (int i = 0; i < ch.lead_copies; ++i) {
       const ms_hp_op& op = ch.ops[i].op;
@@ -1798,7 +1812,8 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
     }
     MS_CUDA(cudaEventRecord(ch.in_ev, d->hpcopy));
   }
-  gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror);
+  gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror,
+                                                        d->trace_on ? d->trace_dev : nullptr);
   MS_CUDA(cudaGetLastError());
   if (pull) {
     for (int i = 0; i < ch.lead_copies; ++i) {
@@ -1880,6 +1895,67 @@ int ms_hp_wait(ms_dev* d, int cid, uint32_t seq, int64_t timeout_ns, ms_hp_times
 }
 
 // ------------------------------------------------------------------ clocks / timing
+int ms_trace_enable(ms_dev* d, size_t capacity) {
+  if (!d) return fail(MS_E_ARG, "null device");
+  if (capacity == 0) {
+    d->trace_on = false;
+    return 0;
+  }
+  if (capacity & (capacity - 1)) return fail(MS_E_ARG, "trace capacity must be a power of two");
+  if (capacity > (1u << 26)) return fail(MS_E_ARG, "trace capacity too large");
+  if (d->trace_ev && d->trace_cap != capacity)
+    return fail(MS_E_ARG, "trace already allocated with capacity " + std::to_string(d->trace_cap));
+  if (!d->trace_ev) {
+    // Stream-local operations only (a device-wide sync would wait for a parked HP gate).
+    MS_CUDA(cudaHostAlloc(&d->trace_ev, capacity * sizeof(MsTraceEvent), cudaHostAllocMapped));
+    std::memset(d->trace_ev, 0, capacity * sizeof(MsTraceEvent));
+    MS_CUDA(cudaMalloc(&d->trace_head, sizeof(unsigned long long)));
+    MS_CUDA(cudaMalloc(&d->trace_dev, sizeof(MsTrace)));
+    MsTrace t{};
+    MS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t.ev), d->trace_ev, 0));
+    t.head = d->trace_head;
+    t.cap_mask = static_cast<uint32_t>(capacity - 1);
+    MS_CUDA(cudaMemsetAsync(d->trace_head, 0, sizeof(unsigned long long), d->aux));
+    MS_CUDA(cudaMemcpyAsync(d->trace_dev, &t, sizeof(t), cudaMemcpyHostToDevice, d->aux));
+    MS_CUDA(cudaStreamSynchronize(d->aux));
+    d->trace_cap = capacity;
+    d->trace_read = 0;
+    d->trace_lost = 0;
+  }
+  d->trace_on = true;  // kernels launched from now on carry the trace
+  return 0;
+}
+
+int ms_trace_drain(ms_dev* d, ms_event* out, size_t max, uint64_t* lost) {
+  if (!d) return fail(MS_E_ARG, "null device");
+  static_assert(sizeof(ms_event) == sizeof(MsTraceEvent), "ms_event layout");
+  size_t n = 0;
+  if (d->trace_ev && out) {
+    const uint64_t mask = d->trace_cap - 1;
+    while (n < max) {
+      const uint64_t i = d->trace_read;
+      MsTraceEvent* e = d->trace_ev + (i & mask);
+      const uint64_t seq = __atomic_load_n(&e->seq, __ATOMIC_ACQUIRE);
+      if (seq == i + 1) {
+        ms_event ev;
+        std::memcpy(&ev, e, sizeof(ev));
+        if (__atomic_load_n(&e->seq, __ATOMIC_ACQUIRE) != seq) continue;  // overwritten while copied
+        ev.seq = seq;
+        out[n++] = ev;
+        d->trace_read = i + 1;
+      } else if (seq > i + 1) {  // the writer lapped the reader: skip to the oldest slot still held
+        const uint64_t next = seq - d->trace_cap;
+        d->trace_lost += next - i;
+        d->trace_read = next;
+      } else {
+        break;  // not written yet
+      }
+    }
+  }
+  if (lost) *lost = d->trace_lost;
+  return static_cast<int>(n);
+}
+
 int ms_clock_calibrate(ms_dev* d, int rounds, int64_t* offset_ns, int64_t* rtt_min) {
   if (rounds < 1) rounds = 1;
   unsigned long long* stamps = nullptr;

@@ -64,6 +64,22 @@ struct MsHostPage {
   uint32_t pong, pad4[31];
 };
 
+// Device-side event trace (ms_trace_enable / ms_trace_drain): events in pinned host memory,
+// positions handed out by a device-memory counter; `seq` is stored last (release) so the
+// host can tell a complete slot from one still being written or already overwritten.
+struct MsTraceEvent {  // == ms_event
+  uint64_t seq;
+  uint64_t t_ns;
+  uint32_t kind;
+  uint32_t id;
+  uint64_t a, b;
+};
+struct MsTrace {
+  MsTraceEvent* ev;          // host-mapped ring (device pointer)
+  unsigned long long* head;  // device memory: events written so far
+  uint32_t cap_mask;         // capacity - 1 (power of two)
+};
+
 struct MsDevMirror {
   uint32_t epoch[MS_MIRROR_COPIES * MS_MIRROR_STRIDE];
   uint64_t budget[MS_MAX_LP][16];

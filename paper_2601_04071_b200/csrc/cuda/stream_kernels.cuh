@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(const __grid_constant__ B
 // host page every ~RTT/4 instead of every RTT: the doorbell is seen sooner after it lands.
 constexpr int kGateWarps = 4;
 
-__global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpRecord* rec, MsDevMirror* mirror) {
+__global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpRecord* rec, MsDevMirror* mirror,
+                            const MsTrace* trace) {
   __shared__ uint32_t rung;
   __shared__ uint64_t word;
   if (threadIdx.x == 0) rung = 0;
@@ -297,6 +298,7 @@ __global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpReco
             const unsigned long long t = globaltimer();
             st_relaxed_sys_u64(&rec->t_gate, t);
             st_release_sys_u32(&rec->seq_gate, seq);
+            trace_emit(trace, 6u, seq, v, 0, t);
           }
         }
         break;
@@ -349,9 +351,11 @@ __global__ void __launch_bounds__(kPullThreads, kPullCtas) hp_pull_kernel(const 
 }
 
 // Completion record of a chain whose last op is a copy (e2e mode): written after the D2H.
-__global__ void hp_notify_kernel(MsHpCtl* ctl, MsHpRecord* rec, unsigned int seq) {
+__global__ void hp_notify_kernel(MsHpCtl* ctl, MsHpRecord* rec, unsigned int seq, const MsTrace* trace, int chain) {
   const unsigned long long t = globaltimer();
   const unsigned long long first = ctl->t_first_cta;
+  trace_emit(trace, 4u, static_cast<uint32_t>(chain), seq, 0, first);
+  trace_emit(trace, 5u, static_cast<uint32_t>(chain), seq, 0, t);
   st_relaxed_sys_v2(&rec->done_first, first, (static_cast<uint64_t>(seq) << 32) | ((t - first) & 0xFFFFFFFFull));
   ctl->t_first_cta = ~0ull;
 }

@@ -43,7 +43,21 @@ struct TileRun {
   unsigned long long* dbg;  // optional per-CTA phase timestamps [gridDim][8] (diagnostics)
   uint32_t* reset_words;    // zeroed by the last CTA to exit (grid-phase counters of a fused chain)
   int n_reset;
+  const MsTrace* trace;     // device-side event trace (null: off)
 };
+
+// One event into the trace ring (any thread; posted system-scope stores, seq last).
+__device__ __forceinline__ void trace_emit(const MsTrace* tr, uint32_t kind, uint32_t id, uint64_t a, uint64_t b,
+                                           uint64_t t) {
+  if (!tr) return;
+  const unsigned long long idx = atomicAdd(tr->head, 1ull);
+  MsTraceEvent* e = tr->ev + (idx & tr->cap_mask);
+  st_relaxed_sys_u64(&e->t_ns, t);
+  st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(&e->kind), (static_cast<uint64_t>(id) << 32) | kind);
+  st_relaxed_sys_u64(&e->a, a);  // (40-byte events: 8-byte aligned fields only)
+  st_relaxed_sys_u64(&e->b, b);
+  st_release_sys_u64(&e->seq, idx + 1);
+}
 
 __device__ __forceinline__ void dbg_stamp(const TileRun& r, int phase) {
   if (r.dbg) r.dbg[blockIdx.x * 8 + phase] = globaltimer();
@@ -214,8 +228,15 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
     st_relaxed_sys_u64(&e->preempted, preempted);
     st_release_sys_u64(&e->run_id, r.run_id);  // host acquires run_id, then reads the rest
   }
+  if (r.trace && r.exit_rec) {
+    trace_emit(r.trace, 1u, static_cast<uint32_t>(r.slot), r.run_id, 0, t_start);
+    if (preempted && t_seen != ~0ull) trace_emit(r.trace, 2u, static_cast<uint32_t>(r.slot), r.run_id, 0, t_seen);
+    trace_emit(r.trace, 3u, static_cast<uint32_t>(r.slot), r.run_id, (tiles_total << 32) | redo_n, t_exit);
+  }
   if (r.hp_ctl && r.hp_last && r.hp_rec) {
     const unsigned long long first = r.hp_ctl->t_first_cta;
+    trace_emit(r.trace, 4u, static_cast<uint32_t>(r.slot), r.hp_seq, 0, first);
+    trace_emit(r.trace, 5u, static_cast<uint32_t>(r.slot), r.hp_seq, 0, t_exit);
     st_relaxed_sys_v2(&r.hp_rec->done_first, first,
                       (static_cast<uint64_t>(r.hp_seq) << 32) | ((t_exit - first) & 0xFFFFFFFFull));
     r.hp_ctl->t_first_cta = ~0ull;

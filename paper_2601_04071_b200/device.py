@@ -68,6 +68,14 @@ class HpOp(C.Structure):
         return op
 
 
+class MsEvent(C.Structure):
+    _fields_ = [("seq", C.c_uint64), ("t_ns", C.c_uint64), ("kind", C.c_uint32), ("id", C.c_uint32),
+                ("a", C.c_uint64), ("b", C.c_uint64)]
+
+
+EVENT_KINDS = {1: "lp_start", 2: "lp_seen", 3: "lp_exit", 4: "hp_first", 5: "hp_done", 6: "gate"}
+
+
 class HpTimes(C.Structure):
     _fields_ = [("seq", C.c_uint32), ("done", C.c_uint32), ("t_gate", C.c_uint64),
                 ("t_first_cta", C.c_uint64), ("t_done", C.c_uint64)]
@@ -117,6 +125,8 @@ def lib() -> C.CDLL:
             "ms_lp_time_full": (I, [P, I, I, C.POINTER(F)]),
             "ms_lp_time_range": (I, [P, I, U64, U64, I, C.POINTER(F)]),
             "ms_hp_time_chain": (I, [P, I, I, C.POINTER(F)]),
+            "ms_trace_enable": (I, [P, C.c_size_t]),
+            "ms_trace_drain": (I, [P, C.POINTER(MsEvent), C.c_size_t, C.POINTER(U64)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -259,6 +269,20 @@ class Device:
 
     def lp_reset(self, k: LpKernel):
         _ck(lib().ms_lp_reset(self._h, k.id))
+
+    # ---- device-side event trace (include/ms_b200.h ms_trace_*)
+    def trace_enable(self, capacity: int = 1 << 14):
+        _ck(lib().ms_trace_enable(self._h, capacity))
+
+    def trace_drain(self, max_events: int = 1 << 14) -> tuple[list[dict], int]:
+        """Events written by the kernels since the last drain (oldest first) and the running
+        count of events overwritten before they were drained."""
+        buf = (MsEvent * max_events)()
+        lost = C.c_uint64()
+        n = _ck(lib().ms_trace_drain(self._h, buf, max_events, C.byref(lost)))
+        evs = [{"seq": e.seq, "t_ns": e.t_ns, "kind": EVENT_KINDS.get(e.kind, e.kind), "id": e.id, "a": e.a, "b": e.b}
+               for e in buf[:n]]
+        return evs, lost.value
 
     def lp_time_full(self, k: LpKernel, reps: int = 5) -> float:
         ms = C.c_float()

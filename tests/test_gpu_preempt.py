@@ -178,3 +178,77 @@ def test_doorbell_releases_armed_chain(dev):
     dev.hp_ring(seq)
     t = dev.hp_wait(chain, seq, 10)
     assert t["done"] and t["t_done"] >= t["t_first_cta"] >= t["t_gate"] > 0
+
+
+def test_device_trace_ring(dev):
+    """ms_trace_enable / ms_trace_drain: the kernels log their own exit records, HP chain
+    completions and gate releases into a ring in pinned host memory, drained in order; a
+    ring the host does not drain in time reports the overwritten events as lost."""
+    import time as _t
+    n = 2048
+    a, b, c = dev.alloc(n * n * 2), dev.alloc(n * n * 2), dev.alloc(n * n * 2)
+    dev.fill_synth(a, n * n, 8, 1, 1.0)
+    dev.fill_synth(b, n * n, 8, 2, float(np.float32(1 / math.sqrt(n))))
+    k = dev.lp_register_gemm(a, b, c, n, n, n, block_n=256)
+    dev.trace_enable(1 << 12)
+    dev.trace_drain()  # start from an empty window
+    dev.lp_run(k, 0, k.total_tiles)
+    spin(20e-6)
+    dev.preempt_raise()
+    st = dev.lp_wait(k, 30)
+    dev.lp_run(k, st["cursor"], k.total_tiles)
+    dev.lp_wait(k, 30)
+    act = [dev.alloc(128 * 1024 * 2) for _ in range(2)]
+    wgt = dev.alloc(1024 * 1024 * 2)
+    dev.fill_synth(act[0], 128 * 1024, 7, 3, 1.0)
+    dev.fill_synth(wgt, 1024 * 1024, 7, 4, 1 / 32)
+    chain = dev.hp_register_chain([dict(kind=1, block_n=64, a=act[0], b=wgt, c=act[1], bias=0, m=128, n=1024, k=1024)])
+    seq = dev.hp_next_seq()
+    dev.hp_arm(chain, seq)
+    _t.sleep(0.002)
+    dev.hp_ring(seq)
+    dev.hp_wait(chain, seq, 10)
+    evs, lost = dev.trace_drain()
+    assert lost == 0
+    assert [e["seq"] for e in evs] == list(range(evs[0]["seq"], evs[0]["seq"] + len(evs)))
+    lp = [e for e in evs if e["kind"] in ("lp_start", "lp_seen", "lp_exit") and e["id"] == k.id]
+    exits = [e for e in lp if e["kind"] == "lp_exit"]
+    assert len(exits) == 2 and len([e for e in lp if e["kind"] == "lp_start"]) == 2
+    assert exits[0]["a"] < exits[1]["a"]  # run ids
+    if st["preempted"]:
+        seen = [e for e in lp if e["kind"] == "lp_seen"]
+        assert len(seen) == 1 and seen[0]["a"] == exits[0]["a"] and seen[0]["t_ns"] <= exits[0]["t_ns"]
+    assert (exits[0]["b"] >> 32) + (exits[1]["b"] >> 32) == k.total_tiles  # tiles done over both runs
+    gate = [e for e in evs if e["kind"] == "gate" and e["id"] == seq]
+    first = [e for e in evs if e["kind"] == "hp_first" and e["a"] == seq]
+    done = [e for e in evs if e["kind"] == "hp_done" and e["a"] == seq]
+    assert len(gate) == 1 and len(first) == 1 and len(done) == 1
+    assert gate[0]["t_ns"] <= first[0]["t_ns"] <= done[0]["t_ns"]
+    for _ in range(12):  # 12 unpreempted runs = 24 events, all held by the 4096-slot ring
+        dev.lp_reset(k)
+        dev.lp_run(k, 0, k.total_tiles)
+        dev.lp_wait(k, 30)
+    evs2, lost2 = dev.trace_drain()
+    assert len(evs2) == 24 and lost2 == 0
+    # overflow: a second device handle with a 16-slot ring, 24 events before the drain
+    from paper_2601_04071_b200.device import Device
+    d2 = Device(0)
+    k2 = d2.lp_register_gemm(a, b, c, n, n, n, block_n=256)
+    d2.trace_enable(16)
+    for _ in range(12):
+        d2.lp_reset(k2)
+        d2.lp_run(k2, 0, k2.total_tiles)
+        d2.lp_wait(k2, 30)
+    evs3, lost3 = d2.trace_drain()
+    assert len(evs3) == 16 and lost3 == 8 and evs3[0]["seq"] == 9 and evs3[-1]["seq"] == 24
+    d2.lp_unregister(k2)
+    d2.close()
+    dev.trace_enable(0)
+    dev.lp_reset(k)
+    dev.lp_run(k, 0, k.total_tiles)
+    dev.lp_wait(k, 30)
+    assert dev.trace_drain()[0] == []  # disabled: nothing logged
+    dev.hp_unregister_chain(chain)
+    dev.lp_unregister(k)
+    for p_ in (a, b, c, act[0], act[1], wgt):
+        dev.free(p_)
