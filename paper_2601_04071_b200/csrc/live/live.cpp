@@ -582,6 +582,8 @@ class LiveRun {
   std::unique_ptr<PowerGovernor> governor_;
   std::vector<std::vector<uint64_t>> debug_;  // per preempted run: raw stamps + raise
   std::vector<std::string> debug_kernels_;    // kernel of each debug_ run
+  std::vector<ms_event> trace_;               // device-side events drained during the run
+  uint64_t trace_lost_ = 0;
   int n_sm_ = 148;
   int64_t t0_ = 0, off0_ = 0, off1_ = 0, c0_ = 0, c1_ = 0;
   uint32_t last_seq_ = 0;
@@ -675,6 +677,22 @@ json LiveRun::run() {
     if (calibrate_) check(ms_clock_calibrate(dev_, 200, &off0_, &rtt), "ms_clock_calibrate");
     c0_ = (a + mono_ns()) / 2;
   }
+  // Optional device-side event trace (include/ms_b200.h ms_trace_*): drained while the run
+  // goes on, so a long run is logged incrementally rather than rebuilt at the end.
+  const long long trace_cap = opts_.value("device_trace", 0ll);
+  if (trace_cap > 0) {
+    check(ms_trace_enable(dev_, static_cast<size_t>(trace_cap)), "ms_trace_enable");
+    ms_event sink[256];
+    while (ms_trace_drain(dev_, sink, 256, nullptr) > 0) {
+    }  // start from an empty window
+  }
+  auto drain_trace = [&]() {
+    if (trace_cap <= 0) return;
+    ms_event buf[256];
+    int n;
+    while ((n = ms_trace_drain(dev_, buf, 256, &trace_lost_)) > 0)
+      for (int i = 0; i < n; ++i) trace_.push_back(buf[i]);
+  };
   // Pre-arm segment 0 of every HP task; schedule arrivals.
   for (HpTask& h : hp_)
     if (!h.seg_kernels.empty()) arm(h, 0);
@@ -722,6 +740,7 @@ json LiveRun::run() {
         maybe_extend_budget();
       }
     }
+    if ((loops & 1023) == 0) drain_trace();
   }
   // Drain: stop LP, release the armed gates (a parked gate holds an SM slot a late LP CTA
   // may need to start, see its exit and leave), finish in-flight HP.
@@ -741,6 +760,8 @@ json LiveRun::run() {
   // Release any still-armed gates so the HP stream drains.
   ms_hp_ring(dev_, last_seq_, nullptr);
   ms_dev_sync(dev_);
+  drain_trace();
+  if (trace_cap > 0) ms_trace_enable(dev_, 0);
   // The LP SM reserve was moved per launch (governor, SM caps): leave the device at the
   // run's base reserve, so a later timing (calibration, profiler) sees the full LP grid.
   ms_set_lp_sm_reserve(dev_, base_reserve_);
@@ -850,6 +871,28 @@ json LiveRun::run() {
   for (const Ns x : ring_to_first_) c.push_back(json(static_cast<long long>(x)));
   raw["ring_to_first_hp_cta_all"] = std::move(c);
   raw["preempted_lp_runs"] = std::move(preempted_runs);
+  if (opts_.value("device_trace", 0ll) > 0) {
+    // [t (run-relative host ns), kind, id, a, b] of every drained device event
+    json dt = json::object(), rows = json::array();
+    std::map<uint32_t, long long> by_kind;
+    for (const ms_event& e : trace_) {
+      ++by_kind[e.kind];
+      json r = json::array();
+      r.push_back(json(static_cast<long long>(dev_to_host(e.t_ns))));
+      r.push_back(json(static_cast<long long>(e.kind)));
+      r.push_back(json(static_cast<long long>(e.id)));
+      r.push_back(json(static_cast<unsigned long long>(e.a)));
+      r.push_back(json(static_cast<unsigned long long>(e.b)));
+      rows.push_back(std::move(r));
+    }
+    json bk = json::object();
+    for (const auto& [k, n] : by_kind) bk[std::to_string(k)] = json(n);
+    dt["events"] = json(static_cast<unsigned long long>(trace_.size()));
+    dt["lost"] = json(static_cast<unsigned long long>(trace_lost_));
+    dt["by_kind"] = std::move(bk);
+    dt["rows"] = std::move(rows);
+    out["device_trace"] = std::move(dt);
+  }
   out["samples"] = std::move(raw);
   if (!debug_.empty()) {
     // phase p of CTA c relative to the raise, converted with the drift-corrected clock

@@ -176,6 +176,11 @@ int ms_set_lp_sm_reserve(ms_dev* d, int n) {
 int ms_debug_stamps(ms_dev*, int, unsigned long long*, size_t) { return 0; }
 uint64_t ms_lp_total_tiles(ms_dev* d, int id) { return d->lp[id].used ? d->lp[id].total : 0; }
 int ms_lp_tile_ctas(ms_dev*, int) { return 1; }
+int ms_trace_enable(ms_dev*, size_t) { return 0; }  // (the virtual device logs no device events)
+int ms_trace_drain(ms_dev*, ms_event*, size_t, uint64_t* lost) {
+  if (lost) *lost = 0;
+  return 0;
+}
 int ms_lp_reset(ms_dev* d, int id) {
   d->lp[id].redo_carry = 0;
   d->lp[id].exited = false;

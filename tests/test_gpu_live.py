@@ -193,3 +193,24 @@ def test_live_rejects_second_hp_task():
     with _pytest.raises(RuntimeError, match="rc=-2"):
         live_run(dev, sc, "splitkernel", b, w.options())
     dev.close()
+
+
+def test_live_device_trace():
+    """A live run with the device-side event trace drained while it runs: every LP run's
+    exit, every HP chain's completion and every gate release is in the log, in order, with
+    nothing lost."""
+    from paper_2601_04071_b200.device import Device
+    from paper_2601_04071_b200.live import Config1, live_run
+    dev = Device(0)
+    w = Config1(dev)
+    w.calibrate(reps=2)
+    r = live_run(dev, w.scenario(seed=5, horizon_s=0.6), "splitkernel", w.binding(),
+                 w.options(timeline=False, device_trace=1 << 15))
+    dt = r["device_trace"]
+    kinds = {int(k): v for k, v in dt["by_kind"].items()}
+    assert dt["lost"] == 0 and dt["events"] == len(dt["rows"]) > 0
+    assert kinds.get(3, 0) >= r["lp"]["launches"] - 1 and kinds.get(1, 0) == kinds.get(3, 0)  # LP start / exit
+    assert kinds.get(5, 0) >= r["hp_chains"] and kinds.get(6, 0) >= r["hp_chains"]  # HP done, gate releases
+    ts = [row[0] for row in dt["rows"] if row[1] in (3, 5)]
+    assert len(ts) > 10
+    dev.close()
