@@ -1285,7 +1285,8 @@ int ms_lp_set_slow_tiles(ms_dev* d, int id, const uint8_t* slow_groups, uint64_t
                          int max_inflight) {
   if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
   LpSlot& s = d->lp_slots[id];
-  if (s.desc.kind != MS_LP_AXPY) return fail(MS_E_ARG, "slow-tile admission is a streamer (MS_LP_AXPY) option");
+  if (s.desc.kind != MS_LP_AXPY && !(s.desc.kind == MS_LP_GEMM && !s.pair))
+    return fail(MS_E_ARG, "slow-tile admission: streamer (MS_LP_AXPY) or single-CTA GEMM kernels");
   MS_CUDA(cudaStreamSynchronize(d->lp));
   if (s.slow) cudaFree(s.slow);
   s.slow = nullptr;
@@ -1369,6 +1370,10 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
       const int stage_bytes = (kBM + s.desc.block_n) * kBK * 2;
       p.tma_inflight = e ? std::max(0, atoi(e)) : (s.split > 1 ? std::max(2, (96 * 1024) / stage_bytes) : 0);
     }
+    p.slow = s.slow;  // memory tier: bounded off-device admission (ms_lp_set_slow_tiles)
+    p.slow_sem = s.slow_sem;
+    p.slow_group = s.slow_group;
+    p.slow_max = s.slow_max;
     if (s.pair) {
       // one CTA pair per tile; pairs of SMs left after the reserve
       const int reserve = (d->lp_sm_reserve + 1) & ~1;  // whole TPCs

@@ -51,6 +51,13 @@ struct GemmParams {
   // for an HBM-bound shape (skinny training GEMMs with K up to 802,816) a full ring of loads
   // queued at the SM's share of HBM bandwidth is ~5 us of drain.
   int tma_inflight;
+  // Off-device admission (memory tier, ms_lp_set_slow_tiles): units u with slow[u / slow_group]
+  // read operand chunks that live in host DRAM / a peer's HBM; at most slow_max of them run
+  // at once device-wide (slow_sem), so a preemption drains at most slow_max units' loads
+  // over the slow link instead of one per CTA.
+  const uint8_t* slow;
+  unsigned int* slow_sem;
+  int slow_group, slow_max;
   // HP epilogue (split_k == 1 here; the split-K reduce kernel applies it otherwise):
   // C = act(acc + bias[col] (+ resid[row, col])), act 0 none / 1 ReLU / 2 tanh-GELU.
   const __nv_bfloat16* bias;
@@ -112,6 +119,7 @@ struct GemmSmemCtl {
   uint64_t mma_drain;
   long long tile_id[2];
   uint32_t tile_abort[2];
+  uint32_t tile_slow[2];  // the unit holds an off-device admission slot (released by the MMA warp)
   uint32_t stage_flag[8];  // 0: data, 1: data + last k-block, 2: aborted (no data)
   uint32_t tmem_base;
   uint32_t preempt;
@@ -334,8 +342,27 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) mbar_wait(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
         long long tile = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
+        uint32_t slow_held = 0;
+        if (tile >= 0 && !(tile & kRedEntry) && p.slow && p.slow[tile / p.slow_group]) {
+          // admission (as the streamer's): wait for one of slow_max slots; a preemption
+          // meanwhile parks the unit (read, then CAS: waiters never inflate the count)
+          for (;;) {
+            const unsigned c = *reinterpret_cast<volatile unsigned int*>(p.slow_sem);
+            if (c < static_cast<unsigned>(p.slow_max) && atomicCAS(p.slow_sem, c, c + 1) == c) {
+              slow_held = 1;
+              break;
+            }
+            if (p.run.preemptible && ld_volatile_smem(&s->preempt)) {
+              push_redo(p.run, static_cast<unsigned long long>(tile));
+              tile = -1;
+              break;
+            }
+            __nanosleep(256);
+          }
+        }
         s->tile_id[slot] = tile;
         s->tile_abort[slot] = 0;
+        s->tile_slow[slot] = slow_held;
         mbar_arrive(&s->tile_full[slot]);
         if (tile < 0) break;
         if (tile & kRedEntry) continue;  // reduction continuation: no MMA work
@@ -441,6 +468,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           if (flag != 0) break;
         }
+        if (s->tile_slow[slot]) atomicSub(p.slow_sem, 1u);  // every load of the unit has landed
         if (aborted) {
           if (!have_slot) mbar_wait(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);  // keep the slot order
           // Drain this tile's issued MMAs (TMEM must be quiescent before dealloc), park the

@@ -72,6 +72,33 @@ class MemoryTier:
         maps = [[c[0] != "local" for c in self.chunks(p)] for p in ptrs]
         return [any(col) for col in zip(*maps)]
 
+    def gemm_slow_units(self, a: int, b: int, m: int, n: int, k: int, block_n: int = 256, split: int = 1,
+                        group_m: int = 16) -> list[bool]:
+        """Per linear work unit of a single-CTA LP GEMM (C = A B^T, A [m, k], B [n, k] bf16,
+        K-contiguous; unit = tile * split + k-slice, tiles in the kernel's group-M raster,
+        tc_gemm.cuh tile_coords): True when the unit's A rows or B rows (its k-slice of them)
+        touch a chunk that lives off the device — the GEMM's ms_lp_set_slow_tiles map."""
+        off_a = [c[0] != "local" for c in self.chunks(a)]
+        off_b = [c[0] != "local" for c in self.chunks(b)]
+        tm, tn, kb = m // 128, n // block_n, k // 64
+        kps = kb // split
+
+        def touches(off, row0, rows, kb0):
+            lo = (row0 * k + kb0 * 64) * 2
+            hi = ((row0 + rows - 1) * k + (kb0 + kps) * 64) * 2  # (rows are contiguous runs of k)
+            return any(off[lo // self.CHUNK:hi // self.CHUNK + 1])
+
+        out = []
+        for t in range(tm * tn):
+            span = group_m * tn
+            g = t // span
+            first = g * group_m
+            gm = min(tm - first, group_m)
+            mb, nb = first + (t - g * span) % gm, (t - g * span) // gm
+            for sl in range(split):
+                out.append(touches(off_a, mb * 128, 128, sl * kps) or touches(off_b, nb * block_n, block_n, sl * kps))
+        return out
+
     def probe(self, link: int) -> tuple[float, int]:
         s, t = C.c_double(), C.c_int64()
         _ck(_lib().ms_tier_probe(self._h, link, C.byref(s), C.byref(t)))

@@ -35,8 +35,8 @@ def run_preempted(dev, k, preemptions=3):
             time.sleep(50e-6)
             dev.preempt_raise()
         st = dev.lp_wait(k, 60)
-        begin = st["cursor"]
-        if begin >= k.total_tiles:
+        begin = min(st["cursor"], k.total_tiles)
+        if begin >= k.total_tiles and st["redo_count"] == 0:   # parked units drained too
             return i + 1
     raise AssertionError("LP run did not finish")
 
@@ -110,3 +110,34 @@ def test_tier_errors(dev):
         tier.alloc(0, 4 * CHUNK, high_priority=True)
         with pytest.raises(DeviceError, match="exhausted by pinned"):
             tier.alloc(0, CHUNK, high_priority=True)
+
+
+def test_tier_gemm_operand_admission(dev):
+    """GEMM operands partly in host DRAM (the tier spilled them): with the per-unit slow map
+    (tier.gemm_slow_units) the single-CTA LP GEMM admits at most 2 off-device units at once,
+    and preempted + resumed runs stay bit-identical to an unconstrained run from HBM."""
+    from paper_2601_04071_b200.tier import MemoryTier
+    m, n, k = 4096, 2048, 8192                  # A 64 MB = 32 chunks, B 32 MB = 16 chunks
+    with MemoryTier(dev, {"hbm_gb": 0.08}) as tier:   # 38 chunks: B spills 10
+        a = tier.alloc(1, m * k * 2)
+        b = tier.alloc(1, n * k * 2)
+        c = dev.alloc(m * n * 2)
+        dev.fill_synth(a, m * k, 11, 1, 1.0)
+        dev.fill_synth(b, n * k, 11, 2, 1.0 / 90.5)
+        assert any(x[0] == "dram" for x in tier.chunks(b))
+        kern = dev.lp_register_gemm(a, b, c, m, n, k, block_n=256)
+        dev.lp_run(kern, 0, kern.total_tiles)
+        dev.lp_wait(kern, 60)
+        ref = d2h(dev, c, m * n)
+        slow = tier.gemm_slow_units(a, b, m, n, k, block_n=256)
+        assert len(slow) == kern.total_tiles and 0 < sum(slow) < len(slow)
+        dev.lp_set_slow_tiles(kern, slow, 1, 2)
+        dev.memset(c, 0, m * n * 2)
+        dev.lp_reset(kern)
+        assert run_preempted(dev, kern, preemptions=4) > 1
+        assert np.array_equal(d2h(dev, c, m * n), ref)
+        dev.lp_set_slow_tiles(kern, None, 0)
+        dev.lp_unregister(kern)
+        dev.free(c)
+        for p in (a, b):
+            tier.free(p)

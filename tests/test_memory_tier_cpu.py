@@ -79,3 +79,40 @@ def test_memory_manager_placement_and_live_extensions(tmp_path):
                     f"-L{LIB}", "-lmicroslice", f"-Wl,-rpath,{LIB}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stdout + out.stderr
+
+
+def test_gemm_slow_units_matches_bytewise_map():
+    """tier.gemm_slow_units (host side of GEMM-operand admission) against a brute-force map
+    of the bytes each (tile, k-slice) unit reads, on a stub tier with a chunk layout."""
+    import random
+    from paper_2601_04071_b200.tier import MemoryTier
+
+    CH = MemoryTier.CHUNK
+    m, n, k, bn, split, gm = 1024, 768, 2048, 256, 2, 4
+    rng = random.Random(5)
+    a, b = 0, (m * k * 2 + CH - 1) // CH * CH
+    place = {p: ["local" if rng.random() < 0.6 else "dram" for _ in range((sz * 2 + CH - 1) // CH)]
+             for p, sz in ((a, m * k), (b, n * k))}
+
+    class Stub:
+        CHUNK = CH
+        def chunks(self, p):
+            return [(t, -1, 0, False) for t in place[p]]
+
+    got = MemoryTier.gemm_slow_units(Stub(), a, b, m, n, k, block_n=bn, split=split, group_m=gm)
+    tm, tn, kps = m // 128, n // bn, k // 64 // split
+    want = []
+    for t in range(tm * tn):                          # tc_gemm.cuh tile_coords (group-M raster)
+        g, r = divmod(t, gm * tn)
+        rows = min(tm - g * gm, gm)
+        mb, nb = g * gm + r % rows, r // rows
+        for sl in range(split):
+            def off(p, row0, nrows):
+                for row in range(row0, row0 + nrows):
+                    lo = (row * k + sl * kps * 64) * 2
+                    hi = lo + kps * 64 * 2 - 1
+                    if any(place[p][c] != "local" for c in range(lo // CH, hi // CH + 1)):
+                        return True
+                return False
+            want.append(off(a, mb * 128, 128) or off(b, nb * bn, bn))
+    assert len(got) == tm * tn * split and got == want
