@@ -27,6 +27,7 @@ constexpr int kFusedBN = 128;
 constexpr int kFusedGemm = 1;
 constexpr int kFusedBiasGelu = 2;
 constexpr int kFusedSiluMul = 5;
+constexpr int kFusedAbsorbed = 6;  // BIAS_GELU computed by the previous GEMM's epilogue (gelu_c)
 
 // Scalar description of one op; copied into shared memory at kernel start (the grid-phase
 // acquires invalidate L1, so re-reading these from global on every use costs L2 trips).
@@ -43,6 +44,8 @@ struct FusedOpDesc {
   float* ws;
   const __nv_bfloat16* x;  // BIAS_GELU input
   const __nv_bfloat16* bias;
+  __nv_bfloat16* gelu_c;            // GEMM (cluster epilogue): also store gelu(C + gelu_bias) here
+  const __nv_bfloat16* gelu_bias;
 };
 
 struct alignas(64) FusedOp {
@@ -199,7 +202,6 @@ __device__ __forceinline__ void reduce_slices_any(const FusedOpDesc& o, int t, i
 // BIAS_GELU (tanh form; same arithmetic as bias_gelu_kernel and oracle tr_bias_gelu).
 __device__ __forceinline__ void bias_gelu_phase(const FusedOpDesc& o, int t, int G) {
   constexpr int B = 4;
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   const long long chunks = static_cast<long long>(o.m) * o.n / 8;
   const long long step = static_cast<long long>(G) * 128;
   for (long long i0 = static_cast<long long>(blockIdx.x) * 128 + t; i0 < chunks; i0 += step * B) {
@@ -224,11 +226,8 @@ __device__ __forceinline__ void bias_gelu_phase(const FusedOpDesc& o, int t, int
       for (int e = 0; e < 4; ++e) {
         const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&xs[e]);
         const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&bs[e]);
-        float v0 = __low2float(x2) + __low2float(b2);
-        float v1 = __high2float(x2) + __high2float(b2);
-        v0 = 0.5f * v0 * (1.0f + tanhf(k0 * (v0 + k1 * v0 * v0 * v0)));
-        v1 = 0.5f * v1 * (1.0f + tanhf(k0 * (v1 + k1 * v1 * v1 * v1)));
-        os[e] = pack_bf16x2(v0, v1);
+        os[e] = pack_bf16x2(bias_gelu_tanh(__low2float(x2), __low2float(b2)),
+                            bias_gelu_tanh(__high2float(x2), __high2float(b2)));
       }
       *reinterpret_cast<uint4*>(o.c + i * 8) = out;
     }
@@ -246,6 +245,14 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, ui
   constexpr int kChunks = W / 4;  // 16-byte chunks per strip row
   const uint32_t r = cluster_ctarank();
   const int row = q * 32 + lane;
+  int mb, nb, kb0;
+  fused_unit_coords(o, u, mb, nb, kb0);
+  uint4 gbias[W / 8];  // bias strip of the absorbed gelu op: its L2 trips overlap the exchange
+  if (o.gelu_c) {
+#pragma unroll
+    for (int v = 0; v < W / 8; ++v)
+      gbias[v] = *reinterpret_cast<const uint4*>(o.gelu_bias + static_cast<size_t>(nb) * kFusedBN + r * W + 8 * v);
+  }
   if (leader) mbar_arrive_expect_tx(recv_full, static_cast<uint32_t>(Cfg::kRecvBytes));
   const uint32_t recv_local = smem_u32(recv);
   const uint32_t bar_local = smem_u32(recv_full);
@@ -307,8 +314,6 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, ui
       }
     }
   }
-  int mb, nb, kb0;
-  fused_unit_coords(o, u, mb, nb, kb0);
   uint4* dst = reinterpret_cast<uint4*>(o.c + static_cast<size_t>(mb * kBM + row) * o.n +
                                         static_cast<size_t>(nb) * kFusedBN + r * W);
 #pragma unroll
@@ -319,6 +324,21 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, ui
     w.z = pack_bf16x2(out[8 * v + 4], out[8 * v + 5]);
     w.w = pack_bf16x2(out[8 * v + 6], out[8 * v + 7]);
     dst[v] = w;
+    if (o.gelu_c) {  // the chain's next op, gelu(C + bias), on the bf16-rounded C as the phase does
+      const size_t col = static_cast<size_t>(nb) * kFusedBN + r * W + 8 * v;
+      const uint32_t* ws = &w.x;
+      const uint32_t* bs = &gbias[v].x;
+      uint4 g;
+      uint32_t* gs = &g.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&ws[e]);
+        const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&bs[e]);
+        gs[e] = pack_bf16x2(bias_gelu_tanh(__low2float(x2), __low2float(b2)),
+                            bias_gelu_tanh(__high2float(x2), __high2float(b2)));
+      }
+      reinterpret_cast<uint4*>(o.gelu_c + static_cast<size_t>(mb * kBM + row) * o.n + col)[0] = g;
+    }
   }
 }
 
@@ -624,6 +644,8 @@ __global__ void __launch_bounds__(256, 1) hp_fused_kernel(const __grid_constant_
           if (leader) dbg_stamp_ext(p.run, 41 + oi * 2);
           group_arrive(p.phase_cnt + o.ready_phase, leader, nullptr, 0, p.full_fence);
         }
+      } else if (o.kind == kFusedAbsorbed) {
+        continue;  // written by the previous GEMM's epilogue, published with its phase
       } else {
         // BIAS_GELU (tanh form, same arithmetic as bias_gelu_kernel / oracle tr_bias_gelu)
         if (leader) dbg_stamp_ext(p.run, oi * 8 + 4);

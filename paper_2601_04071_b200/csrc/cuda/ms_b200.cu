@@ -747,6 +747,7 @@ int plan_fused(ms_dev* d, HpChain& ch) {
       max_units = std::max(max_units, g.tiles * split);
     }
   const bool any_gemm = !gemms.empty();
+  const bool absorb_gelu = !getenv("MS_FUSED_NO_EPI_GELU");
   int np = 0, grid = std::min(std::max(max_units, 1), max_grid);
   for (int i = first; i <= last; ++i) {
     const HpOpRt& o = ch.ops[i];
@@ -785,6 +786,20 @@ int plan_fused(ms_dev* d, HpChain& ch) {
         f.d.mma_phase = np++;
         f.d.ready_phase = split > 1 ? np++ : f.d.mma_phase;
       }
+    } else if (i > first && o.op.kind == MS_HP_BIAS_GELU && absorb_gelu && cs > 1 &&
+               prog.ops[i - first - 1].d.kind == kFusedGemm && prog.ops[i - first - 1].d.mma_phase < 0 &&
+               !prog.ops[i - first - 1].d.swiglu && bn == kFusedBN &&
+               reinterpret_cast<uint64_t>(prog.ops[i - first - 1].d.c) == o.op.a &&
+               prog.ops[i - first - 1].d.m == f.d.m && prog.ops[i - first - 1].d.n == f.d.n) {
+      // gelu(C + bias) straight after a cluster-reduced GEMM on its own output: computed in
+      // that GEMM's epilogue from the same bf16-rounded C (bit-identical to the phase), so
+      // the chain saves a grid phase and a 2-pass sweep over C.
+      FusedOpDesc& g = prog.ops[i - first - 1].d;
+      g.gelu_c = f.d.c;
+      g.gelu_bias = reinterpret_cast<const __nv_bfloat16*>(o.op.bias);
+      f.d.kind = kFusedAbsorbed;
+      f.d.mma_phase = -1;
+      f.d.ready_phase = g.ready_phase;
     } else {
       f.d.kind = o.op.kind == MS_HP_SILU_MUL ? kFusedSiluMul : kFusedBiasGelu;
       f.d.x = reinterpret_cast<const __nv_bfloat16*>(o.op.a);

@@ -303,6 +303,14 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// gelu(x + b), tanh form (oracle tr_bias_gelu): ONE definition for the bias+GELU sites that
+// must agree bit for bit (per-op kernel, fused-chain phase, fused-chain GEMM epilogue).
+__device__ __forceinline__ float bias_gelu_tanh(float x, float b) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float v = x + b;
+  return 0.5f * v * (1.0f + tanhf(k0 * (v + k1 * v * v * v)));
+}
+
 // ---- thread-block clusters / distributed shared memory ----------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -209,11 +209,8 @@ __global__ void __launch_bounds__(256) bias_gelu_kernel(const __grid_constant__ 
       for (int i = 0; i < 4; ++i) {
         const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&xs[i]);
         const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&bs[i]);
-        float v0 = __low2float(x2) + __low2float(b2);
-        float v1 = __high2float(x2) + __high2float(b2);
-        v0 = 0.5f * v0 * (1.0f + tanhf(k0 * (v0 + k1 * v0 * v0 * v0)));
-        v1 = 0.5f * v1 * (1.0f + tanhf(k0 * (v1 + k1 * v1 * v1 * v1)));
-        os[i] = pack_bf16x2(v0, v1);
+        os[i] = pack_bf16x2(bias_gelu_tanh(__low2float(x2), __low2float(b2)),
+                            bias_gelu_tanh(__high2float(x2), __high2float(b2)));
       }
       *reinterpret_cast<uint4*>(p.out + static_cast<size_t>(r) * p.cols + c) = o;
     }

@@ -44,4 +44,6 @@ for trial in range(3):
             x = x[x > 0]
             cols.append(f"{nm}={np.median(x - t0) / 1e3:6.2f}/{np.max(x - t0) / 1e3:6.2f}" if len(x) else f"{nm}=  -  ")
         print(f"op{oi}: " + " ".join(cols))
+dev.debug_stamps(False)
+print("chain ms (hp_time_chain, 20 reps):", [round(dev.hp_time_chain(ch, 20), 4) for _ in range(3)])
 dev.close()
