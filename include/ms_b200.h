@@ -143,8 +143,9 @@ int ms_lp_set_budget(ms_dev* dev, int id, uint64_t budget);
  * LP kernel `id` touch off-device chunks when slow_groups[g] != 0; at most max_inflight
  * such tiles run at once device-wide, which bounds the preemption drain over PCIe /
  * NVLink to max_inflight tiles.  slow_groups == NULL disables.  Streamers (MS_LP_AXPY) and
- * single-CTA GEMMs (tiles = the kernel's linear work units, k-split units included; the
- * host maps each unit's A / B panels onto the tier's chunks, tier.py gemm_slow_units). */
+ * GEMMs, single-CTA or on CTA pairs (tiles = the kernel's linear work units, k-split units
+ * included; the host maps each unit's A / B panels onto the tier's chunks, tier.py
+ * gemm_slow_units). */
 int ms_lp_set_slow_tiles(ms_dev* dev, int id, const uint8_t* slow_groups, uint64_t n_groups, int tiles_per_group,
                          int max_inflight);
 /* Non-blocking: fills *st; returns 1 if the last launch has exited, 0 if running. */

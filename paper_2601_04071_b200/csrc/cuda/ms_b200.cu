@@ -1300,8 +1300,8 @@ int ms_lp_set_slow_tiles(ms_dev* d, int id, const uint8_t* slow_groups, uint64_t
                          int max_inflight) {
   if (id < 0 || id >= MS_MAX_LP || !d->lp_slots[id].used) return fail(MS_E_ARG, "bad LP id");
   LpSlot& s = d->lp_slots[id];
-  if (s.desc.kind != MS_LP_AXPY && !(s.desc.kind == MS_LP_GEMM && !s.pair))
-    return fail(MS_E_ARG, "slow-tile admission: streamer (MS_LP_AXPY) or single-CTA GEMM kernels");
+  if (s.desc.kind != MS_LP_AXPY && s.desc.kind != MS_LP_GEMM)
+    return fail(MS_E_ARG, "slow-tile admission: streamer (MS_LP_AXPY) or GEMM kernels");
   MS_CUDA(cudaStreamSynchronize(d->lp));
   if (s.slow) cudaFree(s.slow);
   s.slow = nullptr;

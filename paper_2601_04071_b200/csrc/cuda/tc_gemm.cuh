@@ -155,6 +155,24 @@ __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, in
 constexpr int kRedFan = 4;
 constexpr unsigned long long kRedEntry = 1ull << 62;
 
+// Off-device admission of one unit (memory tier): when the unit's operands touch off-device
+// chunks, wait for one of slow_max device-wide slots (read, then CAS: waiters never inflate
+// the count).  A preemption meanwhile parks the unit on the redo list and sets tile = -1.
+// Returns 1 when a slot was taken (the MMA warp returns it after the unit's last k-block).
+__device__ __forceinline__ uint32_t slow_admit(const GemmParams& p, const uint32_t* preempt, long long& tile) {
+  if (tile < 0 || (tile & kRedEntry) || !p.slow || !p.slow[tile / p.slow_group]) return 0;
+  for (;;) {
+    const unsigned c = *reinterpret_cast<volatile unsigned int*>(p.slow_sem);
+    if (c < static_cast<unsigned>(p.slow_max) && atomicCAS(p.slow_sem, c, c + 1) == c) return 1;
+    if (p.run.preemptible && ld_volatile_smem(preempt)) {
+      push_redo(p.run, static_cast<unsigned long long>(tile));
+      tile = -1;
+      return 0;
+    }
+    __nanosleep(256);
+  }
+}
+
 __device__ __forceinline__ int red_level_count(int S, int level) {
   int n = S;
   for (int i = 0; i < level; ++i) n = (n + kRedFan - 1) / kRedFan;
@@ -342,24 +360,7 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) mbar_wait(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
         long long tile = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
-        uint32_t slow_held = 0;
-        if (tile >= 0 && !(tile & kRedEntry) && p.slow && p.slow[tile / p.slow_group]) {
-          // admission (as the streamer's): wait for one of slow_max slots; a preemption
-          // meanwhile parks the unit (read, then CAS: waiters never inflate the count)
-          for (;;) {
-            const unsigned c = *reinterpret_cast<volatile unsigned int*>(p.slow_sem);
-            if (c < static_cast<unsigned>(p.slow_max) && atomicCAS(p.slow_sem, c, c + 1) == c) {
-              slow_held = 1;
-              break;
-            }
-            if (p.run.preemptible && ld_volatile_smem(&s->preempt)) {
-              push_redo(p.run, static_cast<unsigned long long>(tile));
-              tile = -1;
-              break;
-            }
-            __nanosleep(256);
-          }
-        }
+        const uint32_t slow_held = slow_admit(p, &s->preempt, tile);
         s->tile_id[slot] = tile;
         s->tile_abort[slot] = 0;
         s->tile_slow[slot] = slow_held;

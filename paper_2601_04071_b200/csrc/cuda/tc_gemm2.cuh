@@ -85,6 +85,7 @@ struct Gemm2Ctl {
   uint32_t epi_abort;  // peer: ordinal (j + 1) of the tile whose epilogue the leader abandoned
   uint32_t epi_stop;   // epilogue warps' shared stop decision
   uint32_t epi_done;   // epilogue finished (the leader's mirror poller may stop)
+  uint32_t tile_slow[2];  // leader: the tile holds an off-device admission slot (tc_gemm.cuh slow_admit)
 };
 
 // ---- cluster helpers ----------------------------------------------------------------
@@ -223,6 +224,7 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) mbar_wait_cluster(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
         long long tile = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
+        s->tile_slow[slot] = slow_admit(p, &s->preempt, tile);
         s->tile_id[slot] = tile;
         s->tile_start[slot] = pos;
         s->tile_abort[slot] = 0;
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(256, 1)
           ++pos;
           if (flag == 1 || flag == 2) break;
         }
+        if (s->tile_slow[slot]) atomicSub(p.slow_sem, 1u);  // every load of the tile has landed
         if (aborted) {
           if (!have_slot) mbar_wait_cluster(&s->tmem_empty[ts], ((j / NS) & 1) ^ 1);  // keep the slot order
           umma_commit_pair(&s->mma_drain);

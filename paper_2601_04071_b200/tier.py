@@ -73,14 +73,16 @@ class MemoryTier:
         return [any(col) for col in zip(*maps)]
 
     def gemm_slow_units(self, a: int, b: int, m: int, n: int, k: int, block_n: int = 256, split: int = 1,
-                        group_m: int = 16) -> list[bool]:
-        """Per linear work unit of a single-CTA LP GEMM (C = A B^T, A [m, k], B [n, k] bf16,
-        K-contiguous; unit = tile * split + k-slice, tiles in the kernel's group-M raster,
-        tc_gemm.cuh tile_coords): True when the unit's A rows or B rows (its k-slice of them)
-        touch a chunk that lives off the device — the GEMM's ms_lp_set_slow_tiles map."""
+                        group_m: int = 16, block_m: int = 128) -> list[bool]:
+        """Per linear work unit of an LP GEMM (C = A B^T, A [m, k], B [n, k] bf16, K-contiguous;
+        unit = tile * split + k-slice, tiles in the kernel's group-M raster, tc_gemm.cuh
+        tile_coords): True when the unit's A rows or B rows (its k-slice of them) touch a chunk
+        that lives off the device — the GEMM's ms_lp_set_slow_tiles map.  Single-CTA kernel:
+        block_m 128, group_m 16; CTA pairs (tc_gemm2.cuh): block_m 256, block_n 256 or 512,
+        group_m 8."""
         off_a = [c[0] != "local" for c in self.chunks(a)]
         off_b = [c[0] != "local" for c in self.chunks(b)]
-        tm, tn, kb = m // 128, n // block_n, k // 64
+        tm, tn, kb = m // block_m, n // block_n, k // 64
         kps = kb // split
 
         def touches(off, row0, rows, kb0):
@@ -96,7 +98,8 @@ class MemoryTier:
             gm = min(tm - first, group_m)
             mb, nb = first + (t - g * span) % gm, (t - g * span) // gm
             for sl in range(split):
-                out.append(touches(off_a, mb * 128, 128, sl * kps) or touches(off_b, nb * block_n, block_n, sl * kps))
+                out.append(touches(off_a, mb * block_m, block_m, sl * kps) or
+                           touches(off_b, nb * block_n, block_n, sl * kps))
         return out
 
     def probe(self, link: int) -> tuple[float, int]:

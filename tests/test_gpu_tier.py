@@ -112,10 +112,13 @@ def test_tier_errors(dev):
             tier.alloc(0, CHUNK, high_priority=True)
 
 
-def test_tier_gemm_operand_admission(dev):
+@pytest.mark.parametrize("pair", [0, 1])
+def test_tier_gemm_operand_admission(dev, pair):
     """GEMM operands partly in host DRAM (the tier spilled them): with the per-unit slow map
-    (tier.gemm_slow_units) the single-CTA LP GEMM admits at most 2 off-device units at once,
-    and preempted + resumed runs stay bit-identical to an unconstrained run from HBM."""
+    (tier.gemm_slow_units) the LP GEMM — single-CTA (tc_gemm.cuh) or on CTA pairs
+    (tc_gemm2.cuh) — admits at most 2 off-device units at once, and preempted + resumed runs
+    stay bit-identical to an unconstrained run from HBM."""
+    import os
     from paper_2601_04071_b200.tier import MemoryTier
     m, n, k = 4096, 2048, 8192                  # A 64 MB = 32 chunks, B 32 MB = 16 chunks
     with MemoryTier(dev, {"hbm_gb": 0.08}) as tier:   # 38 chunks: B spills 10
@@ -125,11 +128,20 @@ def test_tier_gemm_operand_admission(dev):
         dev.fill_synth(a, m * k, 11, 1, 1.0)
         dev.fill_synth(b, n * k, 11, 2, 1.0 / 90.5)
         assert any(x[0] == "dram" for x in tier.chunks(b))
-        kern = dev.lp_register_gemm(a, b, c, m, n, k, block_n=256)
+        os.environ["MS_LP_GEMM_PAIR"] = str(2 * pair)
+        try:
+            kern = dev.lp_register_gemm(a, b, c, m, n, k, block_n=256)
+        finally:
+            os.environ.pop("MS_LP_GEMM_PAIR")
+        assert kern.tile_ctas == 1 + pair
         dev.lp_run(kern, 0, kern.total_tiles)
         dev.lp_wait(kern, 60)
         ref = d2h(dev, c, m * n)
-        slow = tier.gemm_slow_units(a, b, m, n, k, block_n=256)
+        if pair:
+            tn = n * (m // 256) // kern.total_tiles
+            slow = tier.gemm_slow_units(a, b, m, n, k, block_m=256, block_n=tn, group_m=8)
+        else:
+            slow = tier.gemm_slow_units(a, b, m, n, k, block_n=256)
         assert len(slow) == kern.total_tiles and 0 < sum(slow) < len(slow)
         dev.lp_set_slow_tiles(kern, slow, 1, 2)
         dev.memset(c, 0, m * n * 2)
