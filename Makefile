@@ -8,7 +8,7 @@ CXX := g++
 NVCC := nvcc
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-dangling-reference -Iinclude
 NVFLAGS := -std=c++20 -O3 -lineinfo -Xcompiler -fPIC -gencode arch=compute_100a,code=sm_100a \
-           -Iinclude -I$(PKG)/csrc/cuda -Xptxas -v --expt-relaxed-constexpr
+           -Iinclude -I$(PKG)/csrc/cuda -Xptxas -v --expt-relaxed-constexpr $(NVEXTRA)
 
 HOST_SRC := $(wildcard $(PKG)/csrc/host/*.cpp)
 HOST_OBJ := $(patsubst $(PKG)/csrc/host/%.cpp,build/host/%.o,$(HOST_SRC))

@@ -22,6 +22,10 @@
 
 namespace msdev {
 
+#ifndef MS_FUSED_MAX_STAGES
+#define MS_FUSED_MAX_STAGES 8  // ring depth cap (A/B builds: make NVEXTRA=-DMS_FUSED_MAX_STAGES=n)
+#endif
+
 constexpr int kFusedMaxOps = 96;
 constexpr int kFusedBN = 128;
 constexpr int kFusedGemm = 1;
@@ -67,7 +71,7 @@ struct FusedCfg {
   static constexpr int kRecvSliceBytes = CS > 1 ? kBM * kStripCols * 4 : 0;
   static constexpr int kRecvBytes = CS > 1 ? (CS - 1) * kRecvSliceBytes : 0;
   static constexpr int kStagesRaw = (220 * 1024 - kRecvBytes) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kStages = kStagesRaw > MS_FUSED_MAX_STAGES ? MS_FUSED_MAX_STAGES : kStagesRaw;
   static constexpr int kTmemCols = 2 * BN;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kRecvBytes + 1024;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN);
