@@ -238,25 +238,17 @@ __device__ __forceinline__ void bias_gelu_phase(const FusedOpDesc& o, int t, int
   }
 }
 
-// Cluster-mode epilogue of one unit (CS > 1): send the other ranks' strips of this CTA's
-// fp32 partial, sum the received slices with its own strip in slice order, store bf16.
+// k-slice exchange of one unit through distributed shared memory.  (Through L2 instead —
+// global stores, a release reduction per destination, acquire + loads — measured 64 vs 57 us
+// per config-1 chain: the 48 KB of stores + release per CTA took 5.9 us against 3.0 us over
+// DSMEM, competing with the next op's weight stream for L2; profiles/r02c_fused_xchg_*.txt.)
 template <int CS>
-__device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, uint32_t tmem_row, uint8_t* recv,
-                                                 uint64_t* recv_full, uint32_t recv_parity, int q, int lane,
-                                                 bool leader, const TileRun& run, int oi) {
+__device__ __forceinline__ void exchange_dsmem(uint32_t tmem_row, uint8_t* recv, uint64_t* recv_full,
+                                               uint32_t recv_parity, uint32_t r, int row, bool leader,
+                                               const TileRun& run, int oi, float (&out)[FusedCfg<CS>::kStripCols]) {
   using Cfg = FusedCfg<CS>;
   constexpr int W = Cfg::kStripCols;
-  constexpr int kChunks = W / 4;  // 16-byte chunks per strip row
-  const uint32_t r = cluster_ctarank();
-  const int row = q * 32 + lane;
-  int mb, nb, kb0;
-  fused_unit_coords(o, u, mb, nb, kb0);
-  uint4 gbias[W / 8];  // bias strip of the absorbed gelu op: its L2 trips overlap the exchange
-  if (o.gelu_c) {
-#pragma unroll
-    for (int v = 0; v < W / 8; ++v)
-      gbias[v] = *reinterpret_cast<const uint4*>(o.gelu_bias + static_cast<size_t>(nb) * kFusedBN + r * W + 8 * v);
-  }
+  constexpr int kChunks = W / 4;
   if (leader) mbar_arrive_expect_tx(recv_full, static_cast<uint32_t>(Cfg::kRecvBytes));
   const uint32_t recv_local = smem_u32(recv);
   const uint32_t bar_local = smem_u32(recv_full);
@@ -295,7 +287,6 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, ui
   mbar_wait(recv_full, recv_parity);
   if (leader) dbg_stamp_ext(run, 40 + oi * 6 + 1);
   // slice order 0..CS-1 (bit-identical to the global-partial reduction)
-  float out[W];
 #pragma unroll
   for (int i = 0; i < W; ++i) out[i] = 0.f;
 #pragma unroll
@@ -318,6 +309,28 @@ __device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, ui
       }
     }
   }
+}
+
+// Cluster-mode epilogue of one unit (CS > 1): send the other ranks' strips of this CTA's
+// fp32 partial, sum the received slices with its own strip in slice order, store bf16.
+template <int CS>
+__device__ __forceinline__ void cluster_epilogue(const FusedOpDesc& o, int u, uint32_t tmem_row, uint8_t* recv,
+                                                 uint64_t* recv_full, uint32_t recv_parity, int q, int lane,
+                                                 bool leader, const TileRun& run, int oi) {
+  using Cfg = FusedCfg<CS>;
+  constexpr int W = Cfg::kStripCols;
+  const uint32_t r = cluster_ctarank();
+  const int row = q * 32 + lane;
+  int mb, nb, kb0;
+  fused_unit_coords(o, u, mb, nb, kb0);
+  uint4 gbias[W / 8];  // bias strip of the absorbed gelu op: its L2 trips overlap the exchange
+  if (o.gelu_c) {
+#pragma unroll
+    for (int v = 0; v < W / 8; ++v)
+      gbias[v] = *reinterpret_cast<const uint4*>(o.gelu_bias + static_cast<size_t>(nb) * kFusedBN + r * W + 8 * v);
+  }
+  float out[W];
+  exchange_dsmem<CS>(tmem_row, recv, recv_full, recv_parity, r, row, leader, run, oi, out);
   uint4* dst = reinterpret_cast<uint4*>(o.c + static_cast<size_t>(mb * kBM + row) * o.n +
                                         static_cast<size_t>(nb) * kFusedBN + r * W);
 #pragma unroll
