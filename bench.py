@@ -625,8 +625,10 @@ def main():
         "single_cta_lp_gemm_variant": single_variant(allr, peak, args.step_s),
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": (f"{kname} (LP 8192^3 bf16, {calib.get('lp_gemm_tiles')} "
-                                + ("256x512 tiles on CTA pairs)" if pair else "128x256 tiles)")),
+                     "kernel": (f"{kname} (LP 8192^3 bf16, "
+                                + ("512 256x512 tiles on CTA pairs, the last wave's as 256-column halves: "
+                                   f"{calib.get('lp_gemm_tiles')} units)" if pair
+                                   else f"{calib.get('lp_gemm_tiles')} 128x256 tiles)")),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)"},
         "e2e": {"value": _us(percentile(E2E, 0.99)), "unit": "us",
                 "h2d_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),

@@ -125,6 +125,8 @@ struct LpSlot {
   bool used = false;
   bool pair = false;  // GEMM on CTA pairs (tc_gemm2.cuh): 256 x pair_tn tiles
   int pair_tn = 256;
+  long long half_base = 0;  // pair_tn 512: units >= half_base are 256-column halves of the last wave's tiles
+  int half_units = 0;
   ms_lp_desc desc{};
   uint64_t total_tiles = 0;
   int tiles_m = 0, tiles_n = 0;
@@ -1249,6 +1251,25 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
       MS_CUDA(cudaMemset(s.tile_cnt, 0, sizeof(unsigned int) * tiles * s.split));
     }
     s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n * s.split;
+    // Wave tail (pairs, 256 x 512 tiles): 512 tiles of 8192^3 on the 73 pairs left beside the
+    // gate's TPC are 7 waves + 1 tile, and that tile alone runs ~half a wave while every
+    // other pair idles.  When the last wave is at most half full, its tiles run as two
+    // 256-column halves each (units half_base.., tc_gemm2.cuh pair_unit), on twice the pairs.
+    // Sized for the default reserve; MS_LP_PAIR_HALF_TAIL=0 disables.
+    s.half_base = 0;
+    s.half_units = 0;
+    if (s.pair && s.pair_tn == 512) {
+      const char* e = getenv("MS_LP_PAIR_HALF_TAIL");
+      const int pairs = (d->prop.multiProcessorCount - ((d->lp_sm_reserve + 1) & ~1)) / 2;
+      const uint64_t tiles = s.total_tiles;
+      const uint64_t tail = pairs > 0 ? tiles % static_cast<uint64_t>(pairs) : 0;
+      if (!(e && atoi(e) == 0) && pairs > 0 && tiles >= static_cast<uint64_t>(pairs) && tail > 0 &&
+          2 * tail <= static_cast<uint64_t>(pairs)) {
+        s.half_base = static_cast<long long>(tiles - tail);
+        s.half_units = static_cast<int>(2 * tail);
+        s.total_tiles = tiles + tail;
+      }
+    }
     if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
     if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, s.pair ? 128 : bn)) return rc;
     if (int rc = encode_c(&s.tma_c, reinterpret_cast<void*>(desc->c), desc->m, desc->n)) return rc;
@@ -1307,7 +1328,9 @@ int ms_lp_set_slow_tiles(ms_dev* d, int id, const uint8_t* slow_groups, uint64_t
   s.slow = nullptr;
   if (!slow_groups || n_groups == 0) return 0;  // disable
   if (tiles_per_group <= 0 || max_inflight <= 0) return fail(MS_E_ARG, "tiles_per_group and max_inflight must be > 0");
-  if (n_groups * static_cast<uint64_t>(tiles_per_group) < s.total_tiles)
+  // (CTA-pair GEMMs: one entry per tile; the half-tile units of the last wave use their tile's)
+  const uint64_t map_len = s.half_units ? static_cast<uint64_t>(s.half_base) + s.half_units / 2 : s.total_tiles;
+  if (n_groups * static_cast<uint64_t>(tiles_per_group) < map_len)
     return fail(MS_E_ARG, "slow-tile map does not cover the kernel's tiles");
   MS_CUDA(cudaMalloc(&s.slow, n_groups));
   MS_CUDA(cudaMemcpy(s.slow, slow_groups, n_groups, cudaMemcpyHostToDevice));
@@ -1389,6 +1412,8 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.slow_sem = s.slow_sem;
     p.slow_group = s.slow_group;
     p.slow_max = s.slow_max;
+    p.half_base = s.half_base;
+    p.half_units = s.half_units;
     if (s.pair) {
       // one CTA pair per tile; pairs of SMs left after the reserve
       const int reserve = (d->lp_sm_reserve + 1) & ~1;  // whole TPCs

@@ -58,6 +58,11 @@ struct GemmParams {
   const uint8_t* slow;
   unsigned int* slow_sem;
   int slow_group, slow_max;
+  // CTA-pair kernel, 256 x 512 tiles (tc_gemm2.cuh): the last wave's tiles run as two
+  // 256 x 256 column halves on two pairs — units u >= half_base (half_units of them, 0 =
+  // none) are (tile half_base + (u - half_base) / 2, half (u - half_base) % 2).
+  long long half_base;
+  int half_units;
   // HP epilogue (split_k == 1 here; the split-K reduce kernel applies it otherwise):
   // C = act(acc + bias[col] (+ resid[row, col])), act 0 none / 1 ReLU / 2 tanh-GELU.
   const __nv_bfloat16* bias;
@@ -156,11 +161,12 @@ constexpr int kRedFan = 4;
 constexpr unsigned long long kRedEntry = 1ull << 62;
 
 // Off-device admission of one unit (memory tier): when the unit's operands touch off-device
-// chunks, wait for one of slow_max device-wide slots (read, then CAS: waiters never inflate
+// chunks (slow map entry map_idx: the unit itself, or a CTA-pair unit's tile), wait for one of slow_max device-wide slots (read, then CAS: waiters never inflate
 // the count).  A preemption meanwhile parks the unit on the redo list and sets tile = -1.
 // Returns 1 when a slot was taken (the MMA warp returns it after the unit's last k-block).
-__device__ __forceinline__ uint32_t slow_admit(const GemmParams& p, const uint32_t* preempt, long long& tile) {
-  if (tile < 0 || (tile & kRedEntry) || !p.slow || !p.slow[tile / p.slow_group]) return 0;
+__device__ __forceinline__ uint32_t slow_admit(const GemmParams& p, const uint32_t* preempt, long long& tile,
+                                               long long map_idx) {
+  if (tile < 0 || (tile & kRedEntry) || !p.slow || !p.slow[map_idx / p.slow_group]) return 0;
   for (;;) {
     const unsigned c = *reinterpret_cast<volatile unsigned int*>(p.slow_sem);
     if (c < static_cast<unsigned>(p.slow_max) && atomicCAS(p.slow_sem, c, c + 1) == c) return 1;
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) mbar_wait(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
         long long tile = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
-        const uint32_t slow_held = slow_admit(p, &s->preempt, tile);
+        const uint32_t slow_held = slow_admit(p, &s->preempt, tile, tile);
         s->tile_id[slot] = tile;
         s->tile_abort[slot] = 0;
         s->tile_slow[slot] = slow_held;

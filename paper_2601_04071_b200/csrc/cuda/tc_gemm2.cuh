@@ -61,6 +61,17 @@ struct Gemm2Cfg {
 };
 constexpr int kGemm2MaxStages = 6;
 
+// Work unit -> (tile, mask of the 256-column halves it computes): see GemmParams::half_base.
+__device__ __forceinline__ long long pair_unit(long long u, const GemmParams& p, uint32_t& hmask) {
+  if (p.half_units > 0 && u >= p.half_base) {
+    const long long v = u - p.half_base;
+    hmask = 1u << (v & 1);
+    return p.half_base + v / 2;
+  }
+  hmask = 3u;
+  return u;
+}
+
 // Stage flags (leader): 0 data, 1 data + last k-block, 2 terminal (no data), 3 peer-only
 // bytes of an aborted tile (discard).
 struct Gemm2Ctl {
@@ -224,7 +235,9 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) mbar_wait_cluster(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
         long long tile = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
-        s->tile_slow[slot] = slow_admit(p, &s->preempt, tile);
+        uint32_t hmask = 3u;
+        const long long tl = tile >= 0 ? pair_unit(tile, p, hmask) : -1;
+        s->tile_slow[slot] = slow_admit(p, &s->preempt, tile, tl);
         s->tile_id[slot] = tile;
         s->tile_start[slot] = pos;
         s->tile_abort[slot] = 0;
@@ -235,7 +248,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive_cluster(peer_tile_full + slot * 8);  // release.cluster: the stores above first
         if (tile < 0) break;
         int mb, nb;
-        tile_coords(tile, p, mb, nb);
+        tile_coords(tl, p, mb, nb);
+        hmask &= (1u << Cfg::kBHalves) - 1;
+        const uint32_t stage_bytes = Cfg::kHalfBytes * (1u + __popc(hmask));  // one CTA's bytes per k-block
         const uint32_t pos0 = pos;
         int lead_stop = num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -250,12 +265,13 @@ __global__ void __launch_bounds__(256, 1)
             break;
           }
           s->stage_flag[st] = (kb == num_kb - 1) ? 1u : 0u;
-          mbar_arrive_expect_tx(&s->full[st], 2 * Cfg::kStageBytes);  // both CTAs' halves
+          mbar_arrive_expect_tx(&s->full[st], 2 * stage_bytes);  // both CTAs' halves
           const uint32_t fb = smem_u32(&s->full[st]);
           tma_load_2d_pair(smem_u32(smem_a + st * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256);
 #pragma unroll
           for (int h = 0; h < Cfg::kBHalves; ++h)
-            tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
+            if ((hmask >> h) & 1u)
+              tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
                              nb * TN + h * 256);
           ++pos;
         }
@@ -268,12 +284,12 @@ __global__ void __launch_bounds__(256, 1)
           stop_phase ^= 1;
           const int ps = static_cast<int>(ld_volatile_smem(&s->peer_stop[0]));
           for (int kb = ps; kb < lead_stop; ++kb)  // armed for both halves, the peer's never comes
-            mbar_complete_tx(&s->full[(pos0 + kb) % S], Cfg::kStageBytes);
+            mbar_complete_tx(&s->full[(pos0 + kb) % S], stage_bytes);
           for (int kb = lead_stop; kb < ps; ++kb) {  // only the peer's half comes
             const uint32_t st = pos % S;
             mbar_wait(&s->empty[st], ((pos / S) & 1) ^ 1);
             s->stage_flag[st] = 3u;
-            mbar_arrive_expect_tx(&s->full[st], Cfg::kStageBytes);
+            mbar_arrive_expect_tx(&s->full[st], stage_bytes);
             ++pos;
           }
           const uint32_t st = pos % S;  // terminal position: ends the tile for the MMA warp
@@ -298,8 +314,9 @@ __global__ void __launch_bounds__(256, 1)
         const long long tile = *reinterpret_cast<volatile long long*>(&s->tile_id[slot]);
         if (tile < 0) break;
         uint32_t pos = *reinterpret_cast<volatile uint32_t*>(&s->tile_start[slot]);
+        uint32_t hmask;
         int mb, nb;
-        tile_coords(tile, p, mb, nb);
+        tile_coords(pair_unit(tile, p, hmask), p, mb, nb);
         const uint32_t ord = static_cast<uint32_t>(j + 1);
         bool reported = false;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -314,8 +331,9 @@ __global__ void __launch_bounds__(256, 1)
           tma_load_2d_pair(smem_u32(smem_a + st * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256 + 128);
 #pragma unroll
           for (int h = 0; h < Cfg::kBHalves; ++h)
-            tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
-                             nb * TN + h * 256 + 128);
+            if ((hmask >> h) & 1u)
+              tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
+                               nb * TN + h * 256 + 128);
           ++pos;
         }
         // Next announcement; a stop request for this tile that comes after every k-block was
@@ -345,6 +363,8 @@ __global__ void __launch_bounds__(256, 1)
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
         if (s->tile_id[slot] < 0) break;
+        uint32_t hmask;
+        pair_unit(s->tile_id[slot], p, hmask);
         const int ts = j % NS;  // accumulator slot
         // (see tc_gemm.cuh: a preemption seen while the epilogue holds the accumulator lets the
         // MMA warp consume this tile's positions first, so the stop agreement is not held
@@ -380,6 +400,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int k = 0; k < kBK / kUmmaK; ++k)
 #pragma unroll
               for (int h = 0; h < Cfg::kBHalves; ++h) {
+                if (!((hmask >> h) & 1u)) continue;
                 const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes));
                 umma_bf16_pair(d_tmem + h * 256, a0 + 2ull * k, b0 + 2ull * k, Cfg::kIdesc, (kb | k) != 0 ? 1u : 0u);
               }
@@ -433,15 +454,17 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const bool keep = !*reinterpret_cast<volatile uint32_t*>(&s->tile_abort[slot]);
       if (keep) {
+        uint32_t hmask;
         int mb, nb;
-        tile_coords(tile, p, mb, nb);
+        tile_coords(pair_unit(tile, p, hmask), p, mb, nb);
+        const int c_lo = hmask == 2u ? 256 : 0, c_hi = hmask == 1u ? 256 : TN;  // the unit's columns
         const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
         // A preemption during the store of a completed tile abandons it (the leader decides, at
         // 32-column chunk boundaries, tells the peer, and parks the tile on the redo list): the
         // 512-column epilogue is ~2.5 us of TMEM reads that a preempted grid need not wait for.
         bool abandoned = false;
 #pragma unroll 1
-        for (int c0 = 0; c0 < TN; c0 += 32) {
+        for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
           if (p.run.preemptible) {
             if (tid == 0)
               s->epi_stop = leader ? (ld_volatile_smem(&s->preempt) != 0 ? 1u : 0u)

@@ -87,6 +87,58 @@ def test_budget_bounds_the_run(dev, gemm):
     assert np.array_equal(d2h(dev, c, n * n), ref)
 
 
+def test_gemm_pair_half_tail_units(dev):
+    """CTA pairs with 256 x 512 tiles: when the last wave is at most half full, its tiles run
+    as two 256-column halves (tc_gemm2.cuh pair_unit; 4864 x 2048 = 76 tiles on 73 pairs ->
+    73 full tiles + 6 half units).  Same bits as the single-CTA kernel, uninterrupted and
+    preempted + resumed (half units parked on the redo list like tiles)."""
+    import os
+    from paper_2601_04071_b200.live import DEFAULT_LP_SM_RESERVE
+    m, n, kk = 4864, 2048, 1024
+    a, b, c = dev.alloc(m * kk * 2), dev.alloc(n * kk * 2), dev.alloc(m * n * 2)
+    dev.fill_synth(a, m * kk, 9, 1, 1.0)
+    dev.fill_synth(b, n * kk, 9, 2, float(np.float32(1 / math.sqrt(kk))))
+    dev.set_lp_sm_reserve(DEFAULT_LP_SM_RESERVE)
+    pairs = (dev.info["sm_count"] - ((DEFAULT_LP_SM_RESERVE + 1) & ~1)) // 2
+    tiles = (m // 256) * (n // 512)
+    tail = tiles % pairs
+    os.environ["MS_LP_GEMM_PAIR"] = "2"
+    try:
+        k = dev.lp_register_gemm(a, b, c, m, n, kk, block_n=256)
+    finally:
+        os.environ.pop("MS_LP_GEMM_PAIR")
+    assert k.tile_ctas == 2
+    assert k.total_tiles == (tiles + tail if tiles >= pairs and 0 < 2 * tail <= pairs else tiles)
+    k1 = dev.lp_register_gemm(a, b, c, m, n, kk, block_n=256)  # single-CTA reference (pairs auto: too few tiles)
+    assert k1.tile_ctas == 1
+    dev.lp_run(k1, 0, k1.total_tiles)
+    dev.lp_wait(k1, 30)
+    ref = d2h(dev, c, m * n)
+    dev.lp_unregister(k1)
+    dev.memset(c, 0, m * n * 2)
+    dev.lp_run(k, 0, k.total_tiles)
+    st = dev.lp_wait(k, 30)
+    assert st["tiles_done"] == k.total_tiles
+    assert np.array_equal(d2h(dev, c, m * n), ref)
+    dev.memset(c, 0, m * n * 2)
+    dev.lp_reset(k)
+    begin, runs = 0, 0
+    while True:
+        dev.lp_run(k, begin, k.total_tiles)
+        runs += 1
+        spin((3e-6, 20e-6, 60e-6, 9e-6)[runs % 4])
+        dev.preempt_raise()
+        st = dev.lp_wait(k, 30)
+        begin = st["cursor"]
+        if begin >= k.total_tiles and st["redo_count"] == 0:
+            break
+        assert runs < 3000
+    assert np.array_equal(d2h(dev, c, m * n), ref)
+    dev.lp_unregister(k)
+    for p_ in (a, b, c):
+        dev.free(p_)
+
+
 @pytest.mark.parametrize("pair", [0, 1, 2])  # single CTA / pairs with 256 x 256 / 256 x 512 tiles
 def test_gemm_cta_pair_kernel_preempt_resume(dev, pair):
     """The cta_group::2 LP GEMM (MS_LP_GEMM_PAIR=1, tc_gemm2.cuh) and the single-CTA one
