@@ -190,9 +190,9 @@ def aggregate_ranks(allr, H: float, Hb: float) -> dict:
             tot += len(rws)
         return round(met / max(1, tot), 4)
 
-    pool = lambda k: [x for r in allr for x in r[k]]  # noqa: E731
+    pool = lambda k: [x for r in allr for x in r.get(k, [])]  # noqa: E731
     kb = lambda p_, k: [x for r in allr for x in r["kb"][p_][k]]  # noqa: E731
-    return {"S": pool("samples"), "INF": pool("inflight"), "IDL": pool("idle"), "LX": pool("lp_exit"),
+    return {"S": pool("samples"), "INF": pool("inflight"), "IDL": pool("idle"), "LX": pool("lp_exit"), "LF": pool("lp_free"),
             "E2E": pool("e2e"),
             "ex_rate": sum(r["exlp_rate"] for r in allr),
             "lp_rate": sum(r["tiles"] for r in allr) / H,
@@ -452,6 +452,7 @@ def main():
     torch.cuda.synchronize(local)
     barrier(ws)
     samples, inflight, idle, lp_exit, rows, tiles, launches, chains, pinned = [], [], [], [], [], 0, 0, 0, -1
+    lp_free = []
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         for i in range(args.steps):
@@ -461,6 +462,7 @@ def main():
             inflight += smp["preempt_ring_to_first_hp_cta_lp_in_flight"]
             idle += smp["preempt_ring_to_first_hp_cta_lp_idle"]
             lp_exit += smp["preempt_flag_to_last_lp_exit"]
+            lp_free += smp.get("preempt_flag_to_lp_sms_free", [])
             rows += r["requests"]["rows"]
             tiles += r["lp"]["tiles_done"]
             launches += r["lp"]["launches"]
@@ -549,7 +551,7 @@ def main():
                                      reef_s=min(secs, 4.0))
         wx.close()
 
-    mine = {"single": single, "cfg4": cfg4, "legs23": legs23, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "rows": rows,
+    mine = {"single": single, "cfg4": cfg4, "legs23": legs23, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "lp_free": lp_free, "rows": rows,
             "tiles": tiles, "kb": kb, "exlp_rate": exlp_rate, "ex_rows": ex_rows, "step_ms": step_ms, "wall": wall,
             "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"], "launches": launches,
             "chains": chains, "clocks": clk.summary(), "calib": calib, "slo": slo, "pb": pb,
@@ -567,6 +569,7 @@ def main():
 
     agg = aggregate_ranks(allr, H, Hb)
     S_, INF, IDL, LX, E2E = agg["S"], agg["INF"], agg["IDL"], agg["LX"], agg["E2E"]
+    LF = agg["LF"]
     ex_rate, lp_rate, kb_rate, pb_rate = agg["ex_rate"], agg["lp_rate"], agg["kb_rate"], agg["pb_rate"]
     att_sk, att_ex = agg["att"], agg["att_ex"]
 
@@ -603,6 +606,9 @@ def main():
         "preempt_lp_in_flight": {"p50_us": _us(percentile(INF, 0.5)), "p99_us": p99_inf, "n": len(INF)},
         "preempt_lp_idle": {"p50_us": _us(percentile(IDL, 0.5)), "p99_us": _us(percentile(IDL, 0.99)), "n": len(IDL)},
         "lp_exit_p50_us": _us(percentile(LX, 0.50)), "lp_exit_p99_us": _us(percentile(LX, 0.99)),
+        "lp_exit_def": "flag raise -> LP exit record (CTA 0, after every other CTA has left)",
+        "lp_sms_free_p50_us": _us(percentile(LF, 0.50)), "lp_sms_free_p99_us": _us(percentile(LF, 0.99)),
+        "lp_sms_free_def": "flag raise -> the last LP CTA but CTA 0 left its SM and CTA 0's work is done",
         "slo_attainment": att_sk, "slo_attainment_exclusive": att_ex,
         "lp_throughput_vs_exclusive": round(lp_rate / max(1e-9, ex_rate), 4),
         "lp_vs_kernel_boundary": round(lp_rate / max(1e-9, kb_rate["reef"]), 3),

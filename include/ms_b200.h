@@ -111,6 +111,8 @@ typedef struct ms_lp_status {
   int32_t done;               /* the run has exited */
   int64_t t_launch_host;      /* host ns at ms_lp_run */
   uint64_t t_start, t_seen, t_exit; /* device ns: first CTA start, first epoch observation, last exit */
+  uint64_t t_free;            /* device ns: LP grids' SMs released (every CTA but the one that
+                                 aggregates the exit record gone, and that one's work done) */
 } ms_lp_status;
 
 /* Register a preemptible LP kernel; *total_tiles = size of its linear tile space. */

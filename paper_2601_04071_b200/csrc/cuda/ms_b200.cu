@@ -125,12 +125,14 @@ struct LpSlot {
   bool used = false;
   bool pair = false;  // GEMM on CTA pairs (tc_gemm2.cuh): 256 x pair_tn tiles
   int pair_tn = 256;
-  long long half_base = 0;  // pair_tn 512: units >= half_base are 256-column halves of the last wave's tiles
-  int half_units = 0;
+  long long half_base = 0;  // pair_tn 512: units >= half_base are column parts of the last wave's tiles
+  int half_units = 0;       // part units (tail_parts per tile)
+  int tail_parts = 2;       // 2: 256-column halves, 4: 128-column quarters
   ms_lp_desc desc{};
   uint64_t total_tiles = 0;
   int tiles_m = 0, tiles_n = 0;
   CUtensorMap tma_a{}, tma_b{}, tma_c{};
+  CUtensorMap tma_bq{};  // pair GEMMs: B with 64-row boxes (quarter units)
   unsigned long long* redo[2] = {nullptr, nullptr};
   uint64_t run_id = 0;
   uint64_t redo_carry = 0;  // redo entries waiting in redo[run_id % 2] for the next run
@@ -1252,26 +1254,38 @@ int ms_lp_register(ms_dev* d, const ms_lp_desc* desc, int* id, uint64_t* total_t
     }
     s.total_tiles = static_cast<uint64_t>(s.tiles_m) * s.tiles_n * s.split;
     // Wave tail (pairs, 256 x 512 tiles): 512 tiles of 8192^3 on the 73 pairs left beside the
-    // gate's TPC are 7 waves + 1 tile, and that tile alone runs ~half a wave while every
-    // other pair idles.  When the last wave is at most half full, its tiles run as two
-    // 256-column halves each (units half_base.., tc_gemm2.cuh pair_unit), on twice the pairs.
-    // Sized for the default reserve; MS_LP_PAIR_HALF_TAIL=0 disables.
+    // gate's TPC are 7 waves + 1 tile, and that tile alone takes ~0.7 of a wave (71 of 802 us,
+    // profiles/r02s3_gemm_wave_probe.json) while every other pair idles.  When the last wave
+    // is at most half (a quarter) full, its tiles run as 256-column halves (128-column
+    // quarters) on twice (four times) the pairs: units half_base.., tc_gemm2.cuh pair_unit.
+    // Measured (profiles/r02s3_gemm_wave_probe_quarters.json, one box): 7 waves 705 us, whole
+    // tail tile +44 us, halves +23 us, quarters +23 us — a lone part unit is bound by its ring's
+    // load latency (4 stages in flight: ~0.18 us per k-block whatever the unit's width), so
+    // quarters only spend twice the pairs; halves are the default, MS_LP_PAIR_TAIL_PARTS=4
+    // selects quarters (parity-tested), MS_LP_PAIR_HALF_TAIL=0 disables the split.
     s.half_base = 0;
     s.half_units = 0;
+    s.tail_parts = 2;
     if (s.pair && s.pair_tn == 512) {
       const char* e = getenv("MS_LP_PAIR_HALF_TAIL");
+      const char* ep = getenv("MS_LP_PAIR_TAIL_PARTS");
+      const uint64_t max_parts = ep ? static_cast<uint64_t>(std::max(2, std::min(4, atoi(ep)))) : 2;
       const int pairs = (d->prop.multiProcessorCount - ((d->lp_sm_reserve + 1) & ~1)) / 2;
       const uint64_t tiles = s.total_tiles;
       const uint64_t tail = pairs > 0 ? tiles % static_cast<uint64_t>(pairs) : 0;
       if (!(e && atoi(e) == 0) && pairs > 0 && tiles >= static_cast<uint64_t>(pairs) && tail > 0 &&
           2 * tail <= static_cast<uint64_t>(pairs)) {
+        const uint64_t parts = (max_parts >= 4 && 4 * tail <= static_cast<uint64_t>(pairs)) ? 4 : 2;
+        s.tail_parts = static_cast<int>(parts);
         s.half_base = static_cast<long long>(tiles - tail);
-        s.half_units = static_cast<int>(2 * tail);
-        s.total_tiles = tiles + tail;
+        s.half_units = static_cast<int>(parts * tail);
+        s.total_tiles = tiles - tail + parts * tail;
       }
     }
     if (int rc = encode_2d(&s.tma_a, reinterpret_cast<void*>(desc->a), desc->m, desc->k, kBM)) return rc;
     if (int rc = encode_2d(&s.tma_b, reinterpret_cast<void*>(desc->b), desc->n, desc->k, s.pair ? 128 : bn)) return rc;
+    if (s.pair)
+      if (int rc = encode_2d(&s.tma_bq, reinterpret_cast<void*>(desc->b), desc->n, desc->k, 64)) return rc;
     if (int rc = encode_c(&s.tma_c, reinterpret_cast<void*>(desc->c), desc->m, desc->n)) return rc;
   } else if (desc->kind == MS_LP_AXPY) {
     s.desc.tile_elems = desc->tile_elems ? desc->tile_elems : 8192;
@@ -1329,7 +1343,7 @@ int ms_lp_set_slow_tiles(ms_dev* d, int id, const uint8_t* slow_groups, uint64_t
   if (!slow_groups || n_groups == 0) return 0;  // disable
   if (tiles_per_group <= 0 || max_inflight <= 0) return fail(MS_E_ARG, "tiles_per_group and max_inflight must be > 0");
   // (CTA-pair GEMMs: one entry per tile; the half-tile units of the last wave use their tile's)
-  const uint64_t map_len = s.half_units ? static_cast<uint64_t>(s.half_base) + s.half_units / 2 : s.total_tiles;
+  const uint64_t map_len = s.half_units ? static_cast<uint64_t>(s.half_base) + s.half_units / s.tail_parts : s.total_tiles;
   if (n_groups * static_cast<uint64_t>(tiles_per_group) < map_len)
     return fail(MS_E_ARG, "slow-tile map does not cover the kernel's tiles");
   MS_CUDA(cudaMalloc(&s.slow, n_groups));
@@ -1414,6 +1428,7 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
     p.slow_max = s.slow_max;
     p.half_base = s.half_base;
     p.half_units = s.half_units;
+    p.tail_parts = s.tail_parts;
     if (s.pair) {
       // one CTA pair per tile; pairs of SMs left after the reserve
       const int reserve = (d->lp_sm_reserve + 1) & ~1;  // whole TPCs
@@ -1422,10 +1437,10 @@ int ms_lp_run_ex(ms_dev* d, int id, uint64_t begin, uint64_t end, uint64_t budge
       p.group_m = s.desc.group_m ? s.desc.group_m : 8;
       if (s.pair_tn == 512)
         MS_CUDA(launch_kc(tc_gemm2_kernel<512>, 2 * pairs, 256, Gemm2Cfg<512>::kSmemBytes, d->lp, false, 2, s.tma_a,
-                          s.tma_b, s.tma_c, p));
+                          s.tma_b, s.tma_bq, s.tma_c, p));
       else
         MS_CUDA(launch_kc(tc_gemm2_kernel<256>, 2 * pairs, 256, Gemm2Cfg<256>::kSmemBytes, d->lp, false, 2, s.tma_a,
-                          s.tma_b, s.tma_c, p));
+                          s.tma_b, s.tma_bq, s.tma_c, p));
       return 0;
     }
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(work, d->prop.multiProcessorCount - d->lp_sm_reserve)));
@@ -1601,6 +1616,7 @@ int ms_lp_poll(ms_dev* d, int id, ms_lp_status* st) {
   st->t_start = e.t_start;
   st->t_seen = e.t_seen;
   st->t_exit = e.t_exit;
+  st->t_free = e.t_free;
   st->done = 1;
   s.redo_carry = e.redo_count;
   return 1;

@@ -21,7 +21,7 @@
 #define MS_MIRROR_COPIES 8
 #define MS_MIRROR_STRIDE 32  // uint32 elements = 128 B
 
-struct MsLpExit {                 // device -> host, one per LP slot (64 B)
+struct MsLpExit {                 // device -> host, one per LP slot (72 B)
   uint64_t run_id;                // written last (release); host waits for its run id
   uint64_t cursor;                // next never-claimed tile of [begin, end)
   uint64_t redo_count;            // claimed-but-unfinished tiles carried to the next run
@@ -30,6 +30,7 @@ struct MsLpExit {                 // device -> host, one per LP slot (64 B)
   uint64_t t_seen;                // first CTA to observe the preempt epoch (0 = none)
   uint64_t t_exit;                // last CTA exit
   uint64_t preempted;             // 1 if the run ended because of the epoch
+  uint64_t t_free;                // LP grids: every CTA but CTA 0 gone and CTA 0's work done
 };
 
 struct MsHpRecord {               // device -> host, one per HP chain slot (64 B)
@@ -87,7 +88,7 @@ struct MsDevMirror {
 
 struct alignas(128) MsLpCtl {
   unsigned long long claim;       // virtual claim index: redo_in entries first, then fresh tiles
-  unsigned long long tiles_done;  // (unused by the kernels; kept for layout stability)
+  unsigned long long t_free;      // LP grids: max over CTAs != 0 of their exit (0 = none yet)
   unsigned long long t_start;     // min over CTAs
   unsigned long long t_seen;      // min over CTAs that saw the epoch
   unsigned int exited;            // CTAs finished (relaxed; read by CTA 0's host poller)

@@ -427,7 +427,7 @@ __global__ void init_ctl_kernel(MsLpCtl* ctl, int n, MsHpCtl* hp, int n_hp) {  /
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     ctl[i].claim = 0;
-    ctl[i].tiles_done = 0;
+    ctl[i].t_free = 0;
     ctl[i].t_start = ~0ull;
     ctl[i].t_seen = ~0ull;
     ctl[i].exited = 0;

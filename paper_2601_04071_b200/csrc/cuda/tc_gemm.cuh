@@ -58,11 +58,12 @@ struct GemmParams {
   const uint8_t* slow;
   unsigned int* slow_sem;
   int slow_group, slow_max;
-  // CTA-pair kernel, 256 x 512 tiles (tc_gemm2.cuh): the last wave's tiles run as two
-  // 256 x 256 column halves on two pairs — units u >= half_base (half_units of them, 0 =
-  // none) are (tile half_base + (u - half_base) / 2, half (u - half_base) % 2).
+  // CTA-pair kernel, 256 x 512 tiles (tc_gemm2.cuh): the last wave's tiles run as
+  // tail_parts column parts on as many pairs — units u >= half_base (half_units of them, 0 =
+  // none) are (tile half_base + (u - half_base) / tail_parts, part (u - half_base) % tail_parts).
   long long half_base;
   int half_units;
+  int tail_parts;  // 2: the last wave's units are 256-column halves, 4: 128-column quarters
   // HP epilogue (split_k == 1 here; the split-K reduce kernel applies it otherwise):
   // C = act(acc + bias[col] (+ resid[row, col])), act 0 none / 1 ReLU / 2 tanh-GELU.
   const __nv_bfloat16* bias;
@@ -478,14 +479,15 @@ __global__ void __launch_bounds__(256, 1)
         if (s->tile_slow[slot]) atomicSub(p.slow_sem, 1u);  // every load of the unit has landed
         if (aborted) {
           if (!have_slot) mbar_wait(&s->tmem_empty[slot], ((j >> 1) & 1) ^ 1);  // keep the slot order
-          // Drain this tile's issued MMAs (TMEM must be quiescent before dealloc), park the
-          // tile on the redo list, and tell the epilogue to skip it with a plain arrive.
+          // Tell the epilogue to skip the tile (it reads nothing of it) with a plain arrive,
+          // then drain this tile's issued MMAs (TMEM must be quiescent before dealloc) and park
+          // the tile on the redo list: both before this thread reaches the teardown barrier.
+          s->tile_abort[slot] = 1;
+          mbar_arrive(&s->tmem_full[slot]);
           umma_commit(&s->mma_drain);
           mbar_wait(&s->mma_drain, drain_phase);
           drain_phase ^= 1;
           push_redo(p.run, static_cast<unsigned long long>(s->tile_id[slot]));
-          s->tile_abort[slot] = 1;
-          mbar_arrive(&s->tmem_full[slot]);
         } else {
           umma_commit(&s->tmem_full[slot]);
         }

@@ -58,17 +58,23 @@ struct Gemm2Cfg {
   static constexpr int kCStageBytes = 4 * 2 * 32 * 64;
   static constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kCStageBytes + 1024;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(256, 256);
+  static constexpr uint32_t kIdescQ = umma_idesc_bf16(256, 128);  // quarter units (TN = 512)
 };
 constexpr int kGemm2MaxStages = 6;
 
-// Work unit -> (tile, mask of the 256-column halves it computes): see GemmParams::half_base.
-__device__ __forceinline__ long long pair_unit(long long u, const GemmParams& p, uint32_t& hmask) {
+// Work unit -> (tile, its columns [c_lo, c_lo + cw) of the TN-wide tile): see
+// GemmParams::half_base.  Whole tiles have cw = TN; the last wave's units are the tile's
+// 256-column halves or 128-column quarters (p.tail_parts).
+template <int TN>
+__device__ __forceinline__ long long pair_unit(long long u, const GemmParams& p, int& c_lo, int& cw) {
   if (p.half_units > 0 && u >= p.half_base) {
     const long long v = u - p.half_base;
-    hmask = 1u << (v & 1);
-    return p.half_base + v / 2;
+    cw = TN / p.tail_parts;
+    c_lo = static_cast<int>(v % p.tail_parts) * cw;
+    return p.half_base + v / p.tail_parts;
   }
-  hmask = 3u;
+  c_lo = 0;
+  cw = TN;
   return u;
 }
 
@@ -165,6 +171,7 @@ __device__ __forceinline__ void mbar_complete_tx(uint64_t* bar, uint32_t bytes) 
 template <int TN>
 __global__ void __launch_bounds__(256, 1)
     tc_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                    const __grid_constant__ CUtensorMap tma_bq,  // B, 64-row boxes (quarter units)
                     const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ GemmParams p) {
   using Cfg = Gemm2Cfg<TN>;
   constexpr int S = Cfg::kStages;
@@ -212,6 +219,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tma_a);
     prefetch_tmap(&tma_b);
+    prefetch_tmap(&tma_bq);
     prefetch_tmap(&tma_c);
   }
   if (warp == 2) tmem_alloc_pair(&s->tmem_base, Cfg::kTmemCols);
@@ -235,8 +243,8 @@ __global__ void __launch_bounds__(256, 1)
         if (j >= 2) mbar_wait_cluster(&s->tile_empty[slot], ((j >> 1) & 1) ^ 1);
         long long tile = -1;
         if (!(p.run.preemptible && ld_volatile_smem(&s->preempt))) tile = claim_tile(p.run);
-        uint32_t hmask = 3u;
-        const long long tl = tile >= 0 ? pair_unit(tile, p, hmask) : -1;
+        int c_lo = 0, cw = TN;
+        const long long tl = tile >= 0 ? pair_unit<TN>(tile, p, c_lo, cw) : -1;
         s->tile_slow[slot] = slow_admit(p, &s->preempt, tile, tl);
         s->tile_id[slot] = tile;
         s->tile_start[slot] = pos;
@@ -249,8 +257,8 @@ __global__ void __launch_bounds__(256, 1)
         if (tile < 0) break;
         int mb, nb;
         tile_coords(tl, p, mb, nb);
-        hmask &= (1u << Cfg::kBHalves) - 1;
-        const uint32_t stage_bytes = Cfg::kHalfBytes * (1u + __popc(hmask));  // one CTA's bytes per k-block
+        // one CTA's bytes per k-block: 128 rows of A + cw / 2 columns of B
+        const uint32_t stage_bytes = Cfg::kHalfBytes + static_cast<uint32_t>(cw) * kBK;
         const uint32_t pos0 = pos;
         int lead_stop = num_kb;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -268,20 +276,26 @@ __global__ void __launch_bounds__(256, 1)
           mbar_arrive_expect_tx(&s->full[st], 2 * stage_bytes);  // both CTAs' halves
           const uint32_t fb = smem_u32(&s->full[st]);
           tma_load_2d_pair(smem_u32(smem_a + st * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256);
+          if (cw == TN) {
 #pragma unroll
-          for (int h = 0; h < Cfg::kBHalves; ++h)
-            if ((hmask >> h) & 1u)
+            for (int h = 0; h < Cfg::kBHalves; ++h)
               tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
-                             nb * TN + h * 256);
+                               nb * TN + h * 256);
+          } else {  // a part unit: its columns into the stage's first B slot
+            tma_load_2d_pair(smem_u32(smem_b + st * Cfg::kBHalves * Cfg::kHalfBytes), cw == 128 ? &tma_bq : &tma_b, fb,
+                             kb * kBK, nb * TN + c_lo);
+          }
           ++pos;
         }
         if (lead_stop < num_kb) {
+          dbg_stamp_ext(p.run, 20);  // diagnostics (drain probe): leader producer stopped
           // agree on the end of this tile's stream with the peer (see the header); the answer
           // is one st.async completing the armed stop barrier (no release fence on the path)
           mbar_arrive_expect_tx(&s->stop_bar, 16);
           st_cluster_u32(peer_stop_req, static_cast<uint32_t>(j + 1));
           mbar_wait(&s->stop_bar, stop_phase);
           stop_phase ^= 1;
+          dbg_stamp_ext(p.run, 21);  // peer's stop report received
           const int ps = static_cast<int>(ld_volatile_smem(&s->peer_stop[0]));
           for (int kb = ps; kb < lead_stop; ++kb)  // armed for both halves, the peer's never comes
             mbar_complete_tx(&s->full[(pos0 + kb) % S], stage_bytes);
@@ -297,6 +311,7 @@ __global__ void __launch_bounds__(256, 1)
           s->stage_flag[st] = 2u;
           mbar_arrive(&s->full[st]);
           ++pos;
+          dbg_stamp_ext(p.run, 22);  // terminal position issued
         }
       }
       st_volatile_smem(&s->producer_done, 1u);
@@ -314,9 +329,8 @@ __global__ void __launch_bounds__(256, 1)
         const long long tile = *reinterpret_cast<volatile long long*>(&s->tile_id[slot]);
         if (tile < 0) break;
         uint32_t pos = *reinterpret_cast<volatile uint32_t*>(&s->tile_start[slot]);
-        uint32_t hmask;
-        int mb, nb;
-        tile_coords(pair_unit(tile, p, hmask), p, mb, nb);
+        int c_lo, cw, mb, nb;
+        tile_coords(pair_unit<TN>(tile, p, c_lo, cw), p, mb, nb);
         const uint32_t ord = static_cast<uint32_t>(j + 1);
         bool reported = false;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -325,15 +339,20 @@ __global__ void __launch_bounds__(256, 1)
               ld_volatile_smem(&s->stop_req) == ord) {
             report(kb);
             reported = true;
+            dbg_stamp_ext(p.run, 23);  // peer producer stopped
             break;
           }
           const uint32_t fb = mapa_shared(smem_u32(&s->full[st]), 0);
           tma_load_2d_pair(smem_u32(smem_a + st * Cfg::kHalfBytes), &tma_a, fb, kb * kBK, mb * 256 + 128);
+          if (cw == TN) {
 #pragma unroll
-          for (int h = 0; h < Cfg::kBHalves; ++h)
-            if ((hmask >> h) & 1u)
+            for (int h = 0; h < Cfg::kBHalves; ++h)
               tma_load_2d_pair(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes), &tma_b, fb, kb * kBK,
                                nb * TN + h * 256 + 128);
+          } else {  // the second half of the part unit's columns (cta_group::2 splits N)
+            tma_load_2d_pair(smem_u32(smem_b + st * Cfg::kBHalves * Cfg::kHalfBytes), cw == 128 ? &tma_bq : &tma_b, fb,
+                             kb * kBK, nb * TN + c_lo + cw / 2);
+          }
           ++pos;
         }
         // Next announcement; a stop request for this tile that comes after every k-block was
@@ -363,8 +382,8 @@ __global__ void __launch_bounds__(256, 1)
         const int slot = j & 1;
         mbar_wait(&s->tile_full[slot], (j >> 1) & 1);
         if (s->tile_id[slot] < 0) break;
-        uint32_t hmask;
-        pair_unit(s->tile_id[slot], p, hmask);
+        int c_lo, cw;
+        pair_unit<TN>(s->tile_id[slot], p, c_lo, cw);
         const int ts = j % NS;  // accumulator slot
         // (see tc_gemm.cuh: a preemption seen while the epilogue holds the accumulator lets the
         // MMA warp consume this tile's positions first, so the stop agreement is not held
@@ -384,7 +403,10 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&s->full[st], (pos / S) & 1);
           tc_fence_after();
           const uint32_t flag = s->stage_flag[st];
-          if (!aborted && p.run.preemptible && ld_volatile_smem(&s->preempt)) aborted = true;
+          if (!aborted && p.run.preemptible && ld_volatile_smem(&s->preempt)) {
+            aborted = true;
+            dbg_stamp_ext(p.run, 24);  // MMA warp saw the preemption
+          }
           if (flag >= 2) aborted = true;
           if (aborted) {
             // no MMA reads this position: release it in both CTAs
@@ -396,14 +418,22 @@ __global__ void __launch_bounds__(256, 1)
               mbar_wait(&s->empty[bp % S], (bp / S) & 1);
             }
             const uint64_t a0 = umma_desc_k_sw128(smem_u32(smem_a + st * Cfg::kHalfBytes));
+            if (cw == TN) {
 #pragma unroll
-            for (int k = 0; k < kBK / kUmmaK; ++k)
+              for (int k = 0; k < kBK / kUmmaK; ++k)
 #pragma unroll
-              for (int h = 0; h < Cfg::kBHalves; ++h) {
-                if (!((hmask >> h) & 1u)) continue;
-                const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes));
-                umma_bf16_pair(d_tmem + h * 256, a0 + 2ull * k, b0 + 2ull * k, Cfg::kIdesc, (kb | k) != 0 ? 1u : 0u);
-              }
+                for (int h = 0; h < Cfg::kBHalves; ++h) {
+                  const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + (st * Cfg::kBHalves + h) * Cfg::kHalfBytes));
+                  umma_bf16_pair(d_tmem + h * 256, a0 + 2ull * k, b0 + 2ull * k, Cfg::kIdesc, (kb | k) != 0 ? 1u : 0u);
+                }
+            } else {  // part unit: one UMMA (N = cw) into its columns of the accumulator
+              const uint64_t b0 = umma_desc_k_sw128(smem_u32(smem_b + st * Cfg::kBHalves * Cfg::kHalfBytes));
+              const uint32_t idesc = cw == 128 ? Cfg::kIdescQ : Cfg::kIdesc;
+#pragma unroll
+              for (int k = 0; k < kBK / kUmmaK; ++k)
+                umma_bf16_pair(d_tmem + static_cast<uint32_t>(c_lo), a0 + 2ull * k, b0 + 2ull * k, idesc,
+                               (kb | k) != 0 ? 1u : 0u);
+            }
             umma_commit_pair_mc(&s->empty[st], 0x3);
           }
           ++consumed;
@@ -412,15 +442,21 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (s->tile_slow[slot]) atomicSub(p.slow_sem, 1u);  // every load of the tile has landed
         if (aborted) {
+          dbg_stamp_ext(p.run, 25);  // aborted tile's ring positions consumed
           if (!have_slot) mbar_wait_cluster(&s->tmem_empty[ts], ((j / NS) & 1) ^ 1);  // keep the slot order
-          umma_commit_pair(&s->mma_drain);
-          mbar_wait(&s->mma_drain, drain_phase);
-          drain_phase ^= 1;
-          push_redo(p.run, static_cast<unsigned long long>(s->tile_id[slot]));
+          // The epilogues read nothing of an aborted tile: tell them first, so their teardown
+          // does not wait behind the MMA drain and the redo push (an L2 round trip); both
+          // complete before this thread reaches the teardown barrier (TMEM dealloc, cta_exit).
           s->tile_abort[slot] = 1;
           st_cluster_u32(peer_tile_abort + slot * 4, 1u);
           mbar_arrive(&s->tmem_full[ts]);
           mbar_arrive_cluster(peer_tmem_full + ts * 8);  // release.cluster: the abort flag first
+          dbg_stamp_ext(p.run, 27);  // epilogues told
+          umma_commit_pair(&s->mma_drain);
+          mbar_wait(&s->mma_drain, drain_phase);
+          drain_phase ^= 1;
+          dbg_stamp_ext(p.run, 26);  // queued MMAs drained
+          push_redo(p.run, static_cast<unsigned long long>(s->tile_id[slot]));
         } else {
           umma_commit_pair_mc(&s->tmem_full[ts], 0x3);
         }
@@ -429,10 +465,16 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 2) {
     // up until the epilogue is done: an epilogue in progress abandons its tile on a preemption
-    if (lane == 0 && leader && p.run.preemptible) poll_mirror(p.run, &s->preempt, &s->epi_done);
+    if (lane == 0 && leader && p.run.preemptible) {
+      poll_mirror(p.run, &s->preempt, &s->epi_done);
+      dbg_stamp_ext(p.run, 31);  // mirror poller left
+    }
   } else if (warp == 3) {
     // (CTA 0's peer cannot exit before CTA 0 reaches the teardown cluster barrier)
-    if (lane == 0 && p.run.preemptible && blockIdx.x == 0) poll_host(p.run, &s->preempt, &s->producer_done, 2);
+    if (lane == 0 && p.run.preemptible && blockIdx.x == 0) {
+      poll_host(p.run, &s->preempt, &s->producer_done, 2);
+      dbg_stamp_ext(p.run, 30);  // host poller left
+    }
     // auxiliary host pollers on the next leaders (see tile_run.cuh poll_host_aux)
     if (lane == 0 && p.run.preemptible && leader && blockIdx.x >= 2 && blockIdx.x <= 2 * kAuxPollers)
       poll_host_aux(p.run, &s->preempt, &s->producer_done, 150u * blockIdx.x);
@@ -453,16 +495,16 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait_cluster(&s->tmem_full[ts], (j / NS) & 1);
       tc_fence_after();
       const bool keep = !*reinterpret_cast<volatile uint32_t*>(&s->tile_abort[slot]);
+      if (!keep && q == 0 && lane == 0) dbg_stamp_ext(p.run, 28);  // epilogue: aborted tile seen
+      bool abandoned = false;
       if (keep) {
-        uint32_t hmask;
-        int mb, nb;
-        tile_coords(pair_unit(tile, p, hmask), p, mb, nb);
-        const int c_lo = hmask == 2u ? 256 : 0, c_hi = hmask == 1u ? 256 : TN;  // the unit's columns
+        int c_lo, cw, mb, nb;
+        tile_coords(pair_unit<TN>(tile, p, c_lo, cw), p, mb, nb);
+        const int c_hi = c_lo + cw;  // the unit's columns
         const int row0 = mb * 256 + static_cast<int>(rank) * 128 + q * 32;
         // A preemption during the store of a completed tile abandons it (the leader decides, at
         // 32-column chunk boundaries, tells the peer, and parks the tile on the redo list): the
         // 512-column epilogue is ~2.5 us of TMEM reads that a preempted grid need not wait for.
-        bool abandoned = false;
 #pragma unroll 1
         for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
           if (p.run.preemptible) {
@@ -473,11 +515,8 @@ __global__ void __launch_bounds__(256, 1)
             const bool stop = s->epi_stop != 0;
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (stop) {
-              if (tid == 0 && leader) {
-                st_cluster_u32(peer_epi_abort, static_cast<uint32_t>(j + 1));
-                push_redo(p.run, static_cast<unsigned long long>(tile));
-              }
-              abandoned = true;
+              if (tid == 0 && leader) st_cluster_u32(peer_epi_abort, static_cast<uint32_t>(j + 1));
+              abandoned = true;  // (parked on the redo list after the slot is released)
               break;
             }
           }
@@ -512,7 +551,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive_cluster(lead_tmem_empty + ts * 8);
         mbar_arrive_cluster(lead_tile_empty + slot * 8);
       }
+      if (abandoned && tid == 0 && leader) push_redo(p.run, static_cast<unsigned long long>(tile));
     }
+    if (q == 0 && lane == 0) dbg_stamp_ext(p.run, 29);  // epilogue: end announcement seen
     if (lane == 0) bulk_wait_read<0>();
     if (q == 0 && lane == 0) {
       st_volatile_smem(&s->epi_done, 1u);

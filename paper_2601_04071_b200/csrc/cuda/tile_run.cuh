@@ -185,18 +185,24 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
   MsLpCtl* ctl = r.ctl;
   dbg_stamp(r, 5);
   const unsigned long long mine = (static_cast<unsigned long long>(tiles_done_cta) << 32) | ctas;
-  unsigned long long w;
+  unsigned long long w, t_free = 0;
   if (r.hp_ctl == nullptr) {
     if (blockIdx.x != 0) {
+      // this CTA's SMs are free from here: the max over CTAs is the grid's SM-release time
+      // (CTA 0 then spends an L2 round trip or two aggregating the exit record on one SM)
+      red_relaxed_gpu_max_u64(&ctl->t_free, globaltimer());
       red_release_gpu_add_u64(&ctl->top, mine);  // after this CTA's redo pushes (release)
       return;
     }
+    const unsigned long long t_own = globaltimer();
     const unsigned int others = gridDim.x - ctas;
     // relaxed polling (no L1 invalidation per iteration), one acquire fence once complete
     while (static_cast<unsigned int>((w = ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->top)))) < others)
       __nanosleep(32);
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     dbg_stamp_ext(r, 1);
+    const unsigned long long tf = ld_relaxed_gpu_u64(reinterpret_cast<const uint64_t*>(&ctl->t_free));
+    t_free = tf > t_own ? tf : t_own;
   } else {
     atomicAdd(&ctl->exited, ctas);  // relaxed: only CTA 0's host poller reads it
     w = atom_add_acqrel_gpu_u64(&ctl->top, mine);
@@ -226,6 +232,7 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
     st_relaxed_sys_u64(&e->t_seen, t_seen == ~0ull ? 0ull : t_seen);
     st_relaxed_sys_u64(&e->t_exit, t_exit);
     st_relaxed_sys_u64(&e->preempted, preempted);
+    st_relaxed_sys_u64(&e->t_free, t_free ? t_free : t_exit);
     st_release_sys_u64(&e->run_id, r.run_id);  // host acquires run_id, then reads the rest
   }
   if (r.trace && r.exit_rec) {
@@ -248,6 +255,7 @@ __device__ __forceinline__ void cta_exit(const TileRun& r, unsigned int tiles_do
   ctl->t_seen = ~0ull;
   ctl->redo_out_n = 0;
   ctl->preempted = 0;
+  ctl->t_free = 0;
   __threadfence();
   ctl->exited = 0;
 }

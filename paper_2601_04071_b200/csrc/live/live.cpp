@@ -536,7 +536,8 @@ class LiveRun {
         --debug_runs_;
       }
     }
-    lp_samples_.push_back(LpSample{st.preempted && preempt_raised_ ? t_raise_ : -1, st.t_seen, st.t_exit, st.t_start,
+    lp_samples_.push_back(LpSample{st.preempted && preempt_raised_ ? t_raise_ : -1, st.t_seen, st.t_exit,
+                                   st.t_free ? st.t_free : st.t_exit, st.t_start,
                                    static_cast<int>(hp_.size()) + lp_cur_, l.kernel,
                                    "tiles=" + std::to_string(st.tiles_done) + ";cursor=" + std::to_string(st.cursor) +
                                        ";redo=" + std::to_string(st.redo_count) +
@@ -598,7 +599,7 @@ class LiveRun {
   };
   struct LpSample {
     Ns raise;  // -1: not a preemption we raised
-    uint64_t seen, exit, start;
+    uint64_t seen, exit, free, start;  // free: the grid's SMs released (ms_lp_status::t_free)
     int stream;
     std::string kernel, detail;
   };
@@ -624,6 +625,7 @@ class LiveRun {
   Ns harvest_gap_ = 0, t_raise_ = 0, harvest_deadline_ = 0;
   uint64_t lp_budget_ = 0, run_begin_ = 0, run_redo_in_ = 0;
   uint64_t lp_tiles_done_ = 0, lp_launches_ = 0, lp_preemptions_ = 0, budget_extensions_ = 0;
+  std::vector<Ns> lp_free_lat_;
   std::vector<Ns> ring_to_first_, preempt_delays_, lp_exit_lat_, lp_seen_lat_, gate_to_first_, chain_durations_;
   std::vector<Ns> lp_queued_exit_lat_;
   std::vector<Ns> preempt_inflight_, preempt_idle_;  // HP activations with / without LP resident  // preempted runs that had not started at the raise
@@ -806,6 +808,7 @@ json LiveRun::run() {
         lp_queued_exit_lat_.push_back(dev_to_host(smp.exit) - smp.raise);
       } else {
         lp_exit_lat_.push_back(dev_to_host(smp.exit) - smp.raise);
+        lp_free_lat_.push_back(dev_to_host(smp.free) - smp.raise);
         if (smp.seen) lp_seen_lat_.push_back(dev_to_host(smp.seen) - smp.raise);
       }
     }
@@ -848,6 +851,7 @@ json LiveRun::run() {
   out["hp_done_detect_lag"] = summarize(detect_lag_);
   out["bubble_timer_late"] = summarize(timer_late_);
   out["preempt_flag_to_last_lp_exit"] = summarize(lp_exit_lat_);
+  out["preempt_flag_to_lp_sms_free"] = summarize(lp_free_lat_);
   out["preempt_flag_to_first_lp_seen"] = summarize(lp_seen_lat_);
   out["preempt_flag_to_exit_of_queued_lp_runs"] = summarize(lp_queued_exit_lat_);
   std::vector<Ns> g2f;
@@ -861,6 +865,9 @@ json LiveRun::run() {
   for (const Ns x : lp_exit_lat_) b.push_back(json(static_cast<long long>(x)));
   raw["preempt_ring_to_first_hp_cta"] = std::move(a);
   raw["preempt_flag_to_last_lp_exit"] = std::move(b);
+  json bf = json::array();
+  for (const Ns x : lp_free_lat_) bf.push_back(json(static_cast<long long>(x)));
+  raw["preempt_flag_to_lp_sms_free"] = std::move(bf);
   json fi = json::array();
   for (const Ns x : preempt_inflight_) fi.push_back(json(static_cast<long long>(x)));
   raw["preempt_ring_to_first_hp_cta_lp_in_flight"] = std::move(fi);

@@ -41,7 +41,7 @@ class LpStatus(C.Structure):
                 ("redo_in", C.c_uint64), ("cursor", C.c_uint64), ("redo_count", C.c_uint64),
                 ("tiles_done", C.c_uint64), ("preempted", C.c_int32), ("done", C.c_int32),
                 ("t_launch_host", C.c_int64), ("t_start", C.c_uint64), ("t_seen", C.c_uint64),
-                ("t_exit", C.c_uint64)]
+                ("t_exit", C.c_uint64), ("t_free", C.c_uint64)]
 
     def asdict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

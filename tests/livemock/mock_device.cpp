@@ -113,6 +113,7 @@ void finish(ms_dev& d, MockLp& l, int64_t t_exit) {
   s.t_start = static_cast<uint64_t>(r.start);
   s.t_seen = pre ? static_cast<uint64_t>(std::max(r.start, r.raise)) : 0;
   s.t_exit = static_cast<uint64_t>(t_exit);
+  s.t_free = static_cast<uint64_t>(t_exit);
   l.redo_carry = s.redo_count;
   l.exited = true;
   r.active = false;

@@ -87,11 +87,13 @@ def test_budget_bounds_the_run(dev, gemm):
     assert np.array_equal(d2h(dev, c, n * n), ref)
 
 
-def test_gemm_pair_half_tail_units(dev):
-    """CTA pairs with 256 x 512 tiles: when the last wave is at most half full, its tiles run
-    as two 256-column halves (tc_gemm2.cuh pair_unit; 4864 x 2048 = 76 tiles on 73 pairs ->
-    73 full tiles + 6 half units).  Same bits as the single-CTA kernel, uninterrupted and
-    preempted + resumed (half units parked on the redo list like tiles)."""
+@pytest.mark.parametrize("max_parts", [4, 2])
+def test_gemm_pair_half_tail_units(dev, max_parts):
+    """CTA pairs with 256 x 512 tiles: when the last wave is at most a quarter (half) full, its
+    tiles run as four 128-column quarters (two 256-column halves) (tc_gemm2.cuh pair_unit;
+    4864 x 2048 = 76 tiles on 73 pairs -> 73 full tiles + 12 quarter units, or 6 half units
+    with MS_LP_PAIR_TAIL_PARTS=2).  Same bits as the single-CTA kernel, uninterrupted and
+    preempted + resumed (part units parked on the redo list like tiles)."""
     import os
     from paper_2601_04071_b200.live import DEFAULT_LP_SM_RESERVE
     m, n, kk = 4864, 2048, 1024
@@ -103,12 +105,16 @@ def test_gemm_pair_half_tail_units(dev):
     tiles = (m // 256) * (n // 512)
     tail = tiles % pairs
     os.environ["MS_LP_GEMM_PAIR"] = "2"
+    os.environ["MS_LP_PAIR_TAIL_PARTS"] = str(max_parts)
     try:
         k = dev.lp_register_gemm(a, b, c, m, n, kk, block_n=256)
     finally:
         os.environ.pop("MS_LP_GEMM_PAIR")
+        os.environ.pop("MS_LP_PAIR_TAIL_PARTS")
     assert k.tile_ctas == 2
-    assert k.total_tiles == (tiles + tail if tiles >= pairs and 0 < 2 * tail <= pairs else tiles)
+    parts = 4 if max_parts == 4 and 4 * tail <= pairs else 2
+    assert k.total_tiles == (tiles - tail + parts * tail if tiles >= pairs and 0 < 2 * tail <= pairs else tiles)
+    assert k.total_tiles > tiles
     k1 = dev.lp_register_gemm(a, b, c, m, n, kk, block_n=256)  # single-CTA reference (pairs auto: too few tiles)
     assert k1.tile_ctas == 1
     dev.lp_run(k1, 0, k1.total_tiles)
