@@ -525,6 +525,7 @@ class LiveRun {
     l.cursor = st.cursor;
     l.redo = st.redo_count;
     lp_tiles_done_ += st.tiles_done;
+    if (st.t_exit > st.t_start) lp_busy_ns_ += st.t_exit - st.t_start;
     if (st.preempted) lp_preemptions_++;
     if (debug_runs_ > 0) {
       std::vector<uint64_t> buf(148 * 8 + 1, 0);
@@ -624,7 +625,7 @@ class LiveRun {
   int lp_cur_ = -1, lp_rr_ = 0;
   Ns harvest_gap_ = 0, t_raise_ = 0, harvest_deadline_ = 0;
   uint64_t lp_budget_ = 0, run_begin_ = 0, run_redo_in_ = 0;
-  uint64_t lp_tiles_done_ = 0, lp_launches_ = 0, lp_preemptions_ = 0, budget_extensions_ = 0;
+  uint64_t lp_tiles_done_ = 0, lp_launches_ = 0, lp_preemptions_ = 0, budget_extensions_ = 0, lp_busy_ns_ = 0;
   std::vector<Ns> lp_free_lat_;
   std::vector<Ns> ring_to_first_, preempt_delays_, lp_exit_lat_, lp_seen_lat_, gate_to_first_, chain_durations_;
   std::vector<Ns> lp_queued_exit_lat_;
@@ -753,6 +754,7 @@ json LiveRun::run() {
     ms_lp_status st{};
     check(ms_lp_wait(dev_, lp_[lp_cur_].dev_id, 30'000'000'000ll, &st), "ms_lp_wait");
     lp_tiles_done_ += st.tiles_done;
+    if (st.t_exit > st.t_start) lp_busy_ns_ += st.t_exit - st.t_start;
   }
   for (HpTask& h : hp_)
     if (h.inflight) {
@@ -955,6 +957,8 @@ json LiveRun::run() {
   lp["parents_completed"] = json(static_cast<long long>(art_.lp_parent_completions));
   lp["work_units"] = json(art_.lp_work_units);
   lp["launches"] = json(static_cast<unsigned long long>(lp_launches_));
+  // device time the LP grids were resident (first CTA start -> exit record, summed over runs)
+  lp["busy_ns"] = json(static_cast<unsigned long long>(lp_busy_ns_));
   lp["preemptions"] = json(static_cast<unsigned long long>(lp_preemptions_));
   lp["budget_extensions"] = json(static_cast<unsigned long long>(budget_extensions_));
   out["lp"] = std::move(lp);
