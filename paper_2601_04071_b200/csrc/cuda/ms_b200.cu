@@ -1885,7 +1885,11 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
       q.n16 = static_cast<unsigned long long>(op.m) / 16;
       q.hp_ctl = d->hp_ctl + cid;
       q.done = ch.pull_done + i;
-      MS_CUDA(launch_k(hp_pull_kernel, kPullCtas, kPullThreads, 0, d->hp, true, q));
+      static const int pull_ctas = [] {  // A/B knob (tools/e2e_tail_probe.py)
+        const char* e = std::getenv("MS_PULL_CTAS");
+        return e ? std::max(1, std::min(atoi(e), 64)) : kPullCtas;
+      }();
+      MS_CUDA(launch_k(hp_pull_kernel, pull_ctas, kPullThreads, 0, d->hp, true, q));
     }
     return launch_chain(d, cid, ch, seq, false, static_cast<size_t>(ch.lead_copies), true);
   }

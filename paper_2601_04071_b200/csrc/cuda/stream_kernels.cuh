@@ -318,9 +318,15 @@ struct PullParams {
   MsHpCtl* hp_ctl;
   unsigned int* done;    // CTAs finished (self-resetting)
 };
-constexpr int kPullThreads = 256, kPullCtas = 7, kPullUnroll = 4;
+// Grid: 56 CTAs (16 KB of reads in flight each).  The pull is bound by reads in flight, and
+// with LP resident the PCIe read latency grows: 7 CTAs took ring -> input resident p50 43 us
+// with LP in flight vs 25 us on an idle GPU; 28 / 56 CTAs 29 / 27 us (split-kernel p99 30.4 /
+// 29.2 vs 46.6 us, exclusive ~25-26 either way; tools/e2e_tail_probe.py,
+// profiles/r02s3_e2e_tail_probe_*.json).  The CTAs need no shared memory, so they fit beside
+// the LP CTAs on any SM.  MS_PULL_CTAS overrides.
+constexpr int kPullThreads = 256, kPullCtas = 56, kPullCtasPerSm = 7, kPullUnroll = 4;
 
-__global__ void __launch_bounds__(kPullThreads, kPullCtas) hp_pull_kernel(const __grid_constant__ PullParams p) {
+__global__ void __launch_bounds__(kPullThreads, kPullCtasPerSm) hp_pull_kernel(const __grid_constant__ PullParams p) {
   pdl_launch_dependents();  // the chain kernel may become resident now; it waits for our completion
   const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * kPullThreads;
   for (unsigned long long i0 = blockIdx.x * static_cast<unsigned long long>(kPullThreads) + threadIdx.x; i0 < p.n16;
