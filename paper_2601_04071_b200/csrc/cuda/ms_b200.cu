@@ -1873,7 +1873,11 @@ int ms_hp_arm(ms_dev* d, int cid, uint32_t seq) {
     }
     MS_CUDA(cudaEventRecord(ch.in_ev, d->hpcopy));
   }
-  gate_kernel<<<1, 32 * kGateWarps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror,
+  static const int gate_warps = [] {  // A/B knob (tools/gate_pollers_ab.py)
+    const char* e = std::getenv("MS_GATE_WARPS");
+    return e ? std::max(1, std::min(atoi(e), 32)) : kGateWarps;
+  }();
+  gate_kernel<<<1, 32 * gate_warps, gate_smem, d->hp>>>(&d->page_d->doorbell, seq, &d->page_d->hp[cid], d->mirror,
                                                         d->trace_on ? d->trace_dev : nullptr);
   MS_CUDA(cudaGetLastError());
   if (pull) {
