@@ -264,12 +264,16 @@ __global__ void __launch_bounds__(256) silu_mul_kernel(const __grid_constant__ B
 // no launch needed) first pushes the preempt epoch into the device mirror — every LP CTA
 // sees it on its next L2 poll, without waiting for the LP leader's own PCIe round trip —
 // then lets the PDL-launched chain kernel be scheduled.
-// Sixteen pollers (lane 0 of warps 0-15), started ~40 ns apart, so a PCIe read reaches the
-// host page every ~RTT/16 instead of every RTT: the doorbell is seen sooner after it lands.
+// Eight pollers (lane 0 of warps 0-7), started ~75 ns apart, so a PCIe read reaches the
+// host page every ~RTT/8 instead of every RTT: the doorbell is seen sooner after it lands.
 // Live config-1 A/B (tools/gate_pollers_ab.py, profiles/r02s3_gate_pollers_ab.json, 4 x 2.5 s
 // windows each): ring -> first HP CTA p50 / p99 3.90 / 7.81 us with 4 pollers, 3.75 / 7.42
-// with 8, 3.65 / 7.34 with 16 (LP in flight p99 8.05 / 7.82 / 7.59).  MS_GATE_WARPS overrides.
-constexpr int kGateWarps = 16;
+// with 8, 3.65 / 7.34 with 16 (LP in flight p99 8.05 / 7.82 / 7.59).  But the LP drain of
+// configs 2/3 (single-CTA k-split GEMMs + optimizer streamer) degrades with the poll rate:
+// flag -> last LP exit p99 config 2 / 3 = 11-12 / 15 us with 4 pollers, 13 / 14-15 with 8,
+// 17-19 / 20-21 with 16 (tools/drain23_probe.py, profiles/r02s3_drain23_gate_warps/), so 8.
+// MS_GATE_WARPS overrides.
+constexpr int kGateWarps = 8;
 
 __global__ void gate_kernel(const uint64_t* doorbell, unsigned int seq, MsHpRecord* rec, MsDevMirror* mirror,
                             const MsTrace* trace) {
