@@ -193,7 +193,7 @@ def aggregate_ranks(allr, H: float, Hb: float) -> dict:
     pool = lambda k: [x for r in allr for x in r.get(k, [])]  # noqa: E731
     kb = lambda p_, k: [x for r in allr for x in r["kb"][p_][k]]  # noqa: E731
     return {"S": pool("samples"), "INF": pool("inflight"), "IDL": pool("idle"), "LX": pool("lp_exit"), "LF": pool("lp_free"),
-            "E2E": pool("e2e"),
+            "E2E": pool("e2e"), "E2E_INF": pool("e2e_inf"), "E2E_IDLE": pool("e2e_idle"),
             "ex_rate": sum(r["exlp_rate"] for r in allr),
             "lp_rate": sum(r["tiles"] for r in allr) / H,
             "kb_rate": {p_: sum(r["kb"][p_]["tiles"] for r in allr) / Hb for p_ in ("reef", "reef_req")},
@@ -538,6 +538,8 @@ def main():
     # memory (H2D of the input at admission, D2H of the output before completion)
     e2e = live_run(dev, sc(0, args.step_s), "splitkernel", w.binding(e2e=True), w.options(timeline=False))
     e2e_samples = e2e["samples"]["preempt_ring_to_first_hp_cta"]
+    e2e_inf = e2e["samples"].get("preempt_ring_to_first_hp_cta_lp_in_flight", [])
+    e2e_idle = e2e["samples"].get("preempt_ring_to_first_hp_cta_lp_idle", [])
 
     cfg4 = None
     if args.cfg4_s > 0 and not profiling:
@@ -564,7 +566,8 @@ def main():
     mine = {"single": single, "cfg4": cfg4, "legs23": legs23, "samples": samples, "inflight": inflight, "idle": idle, "lp_exit": lp_exit, "lp_free": lp_free, "rows": rows,
             "burst_ms": burst_ms, "lp_busy_ns": lp_busy_ns, "lp_units_total": lp_units_total,
             "tiles": tiles, "kb": kb, "exlp_rate": exlp_rate, "ex_rows": ex_rows, "step_ms": step_ms, "wall": wall,
-            "e2e": e2e_samples, "e2e_chains": e2e["hp_chains"], "launches": launches,
+            "e2e": e2e_samples, "e2e_inf": e2e_inf, "e2e_idle": e2e_idle, "e2e_chains": e2e["hp_chains"],
+            "launches": launches,
             "chains": chains, "clocks": clk.summary(), "calib": calib, "slo": slo, "pb": pb,
             "pb_clocks": pclk.summary(), "core": pinned, "nb": nb}
     allr = gather(mine, ws)
@@ -666,7 +669,12 @@ def main():
                 "h2d_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),
                 "d2h_bytes_per_step": int(128 * 4096 * 2 * allr[0]["e2e_chains"]),
                 "what": "same metric through ms_live_run with the request input H2D (pinned host) at admission and "
-                        "the output D2H before completion"},
+                        "the output D2H before completion",
+                "p50": _us(percentile(E2E, 0.5)),
+                "lp_in_flight": {"p50": _us(percentile(agg["E2E_INF"], 0.5)), "p99": _us(percentile(agg["E2E_INF"], 0.99)),
+                                 "n": len(agg["E2E_INF"])},
+                "lp_idle": {"p50": _us(percentile(agg["E2E_IDLE"], 0.5)), "p99": _us(percentile(agg["E2E_IDLE"], 0.99)),
+                            "n": len(agg["E2E_IDLE"])}},
         "gpu_launches": int(sum(r["launches"] + 6 * r["chains"] for r in allr)),
         "clocks": allr[0]["clocks"],
         "host": dict(host_info(), scheduler_cores=[r["core"] for r in allr]),
